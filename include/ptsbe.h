@@ -1,0 +1,157 @@
+/*
+ * ptsbe.h -- C ABI of libptsbe.so, the sm_100a batched-execution engine of the
+ * PTSBE (pre-trajectory sampling with batched execution) hot path.
+ *
+ * The reference ("trajsim", /root/reference/pkg/src/trajsim) is pure Python and
+ * has no FFI; each entry point below replaces one Python function of its
+ * hot path (file:line in the reference):
+ *
+ *   ptsbe_create / ptsbe_destroy  <- statevector.init_zero          statevector.py:64-69
+ *                                    (device-resident batch of 2^n-amplitude states)
+ *   ptsbe_load_program            <- the op loop of prepare_state   execute.py:85-97
+ *                                    (gate + fixed Kraus stream, lowered to fused passes)
+ *   ptsbe_run_batch               <- prepare_state x B              execute.py:74-98
+ *                                    apply_gate/apply_matrix         statevector.py:118-126
+ *                                    apply_kraus_normalized          statevector.py:136-145
+ *   ptsbe_sample                  <- sample_shots x B               statevector.py:148-163
+ *                                    ShotBatch.from_indices          statevector.py:44-47
+ *   ptsbe_get_state/ptsbe_set_state <- ComplexState.amplitudes      statevector.py:18-32
+ *   ptsbe_last_error              <- exception text                 errors.py:5-25
+ *
+ * Conventions
+ *   - Every function returns a ptsbe_status; 0 is success.  Per-trajectory
+ *     annihilation is NOT a call failure: it is reported in out_status[b].
+ *   - The caller owns every pointer it passes; the handle owns device memory.
+ *     Pointers are HOST pointers unless PTSBE_DEVICE_PTRS is set in `flags`,
+ *     in which case they are device pointers on the handle's device.
+ *   - One handle per (host thread, device); a handle is not thread-safe.
+ *     Work is queued on the handle's own CUDA stream (ptsbe_stream).
+ *   - Basis index bit q is qubit q (statevector.py:20).  For a 2-qubit op the
+ *     first-listed target is the most significant bit of the 4x4 local index
+ *     (statevector.py:86, circuit.py:25-26).
+ */
+#ifndef PTSBE_H
+#define PTSBE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PTSBE_ABI_VERSION 1
+
+typedef enum {
+  PTSBE_OK = 0,
+  PTSBE_ERR_VALIDATION = 1,   /* -> ValidationError   (errors.py:17)  */
+  PTSBE_ERR_ANNIHILATED = 2,  /* -> AnnihilatedStateError (errors.py:25), per trajectory */
+  PTSBE_ERR_CUDA = 3,         /* -> ExecutionError    (errors.py:21)  */
+  PTSBE_ERR_NCCL = 4          /* -> ExecutionError                     */
+} ptsbe_status;
+
+typedef enum { PTSBE_C64 = 0, PTSBE_C128 = 1 } ptsbe_dtype;
+
+/* trajectory status values written to out_status[] */
+#define PTSBE_TRAJ_OK 0
+#define PTSBE_TRAJ_ANNIHILATED 2
+
+/* flags */
+#define PTSBE_DEVICE_PTRS 0x1u  /* pointer arguments are device pointers */
+#define PTSBE_NO_SYNC     0x2u  /* do not synchronise the stream before returning
+                                   (only meaningful with PTSBE_DEVICE_PTRS) */
+
+/* rng modes of ptsbe_sample */
+#define PTSBE_RNG_PCG64   0  /* numpy PCG64 stream per trajectory: rng_state[4*b..] =
+                                {state_hi, state_lo, inc_hi, inc_lo}; bit-exact uniforms
+                                of Generator(PCG64).random(m)  (execute.py:44-45,145-146) */
+#define PTSBE_RNG_PHILOX  1  /* device Philox4x32-10, key rng_state[b] (production) */
+#define PTSBE_RNG_KEYS    2  /* caller supplies the uniforms as 53-bit integers
+                                u = key * 2^-53 in `keys` (concatenated per trajectory) */
+
+/* One entry of the program's op stream (gate or noise site), in application
+ * order (execute.py:85-97). */
+typedef struct {
+  int32_t kind;   /* 0 = gate with fixed matrix, 1 = noise site (outcome chosen per trajectory) */
+  int32_t arity;  /* 1 or 2 */
+  int32_t t0;     /* first-listed target qubit (MSB of local index) */
+  int32_t t1;     /* second target (arity 2), else -1 */
+  int32_t ref;    /* kind 0: matrix index; kind 1: site id */
+  int32_t pass;   /* index of the fused HBM pass that executes this op */
+} ptsbe_op;
+
+/* A noise channel as the device sees it: outcome k uses matrix mat_base + k. */
+typedef struct {
+  int32_t n_outcomes;
+  int32_t mat_base;
+  int32_t general;        /* 1: non-unitary Kraus, renormalise + weight (statevector.py:136-145) */
+  int32_t arity;
+  uint64_t identity_mask; /* bit k: outcome k is exactly the identity (skipped bit-exactly) */
+} ptsbe_channel;
+
+/* A fused pass: all ops with .pass == index act inside tiles spanned by qubit_mask. */
+typedef struct {
+  uint64_t qubit_mask;    /* tile qubit set; must contain qubits 0..low_bits-1 */
+  int32_t tile_bits;      /* popcount(qubit_mask) */
+  int32_t low_bits;       /* contiguous low qubits in the set (>= 3) */
+} ptsbe_pass;
+
+typedef struct ptsbe_engine ptsbe_engine;
+
+int ptsbe_abi_version(void);
+
+int ptsbe_create(int device, int n_qubits, int dtype, int batch_cap, ptsbe_engine** out);
+int ptsbe_destroy(ptsbe_engine* h);
+
+/* mats: n_mats matrices, each 4x4 complex128 row-major padded (32 doubles,
+ * re/im interleaved); a 1-qubit matrix uses the leading 2x2 (entries 0,1,2,3). */
+int ptsbe_load_program(ptsbe_engine* h,
+                       const ptsbe_op* ops, int n_ops,
+                       const double* mats, int n_mats,
+                       const ptsbe_channel* chans, int n_chans,
+                       const int32_t* site_chan, int n_sites,
+                       const ptsbe_pass* passes, int n_passes);
+
+/* Prepare B states (B <= batch_cap).  sel[b*n_sites + s] = Kraus outcome at
+ * site s (0 = default).  Writes realized weights (execute.py:97) and status. */
+int ptsbe_run_batch(ptsbe_engine* h, const uint8_t* sel, int B,
+                    double* out_weight, int32_t* out_status, uint32_t flags);
+
+/* Sample shots[b] shots from each prepared state (b < B).  Output is one
+ * contiguous CSR stream: trajectory b's distinct outcomes occupy entries
+ * [u_b, u_b + out_nuniq[b]) of out_idx / out_cnt, u_b = sum of earlier
+ * out_nuniq, ascending basis index (qubit q = bit q) with its shot count.
+ * out_idx / out_cnt need room for sum(shots) entries.  rng_state / keys
+ * depend on rng_mode (see above). */
+int ptsbe_sample(ptsbe_engine* h, int B, const int64_t* shots, int rng_mode,
+                 const uint64_t* rng_state, const uint64_t* keys,
+                 uint64_t* out_idx, uint32_t* out_cnt, int64_t* out_nuniq,
+                 uint32_t flags);
+
+/* Copy state b (normalised, engine dtype, interleaved re/im) to / from `buf`. */
+int ptsbe_get_state(ptsbe_engine* h, int b, void* buf, uint32_t flags);
+int ptsbe_set_state(ptsbe_engine* h, int b, const void* buf, uint32_t flags);
+
+/* Apply the loaded program to the batch states as they are (no |0> init);
+ * used by the single-state inner API (apply_matrix & co). */
+int ptsbe_apply_program(ptsbe_engine* h, const uint8_t* sel, int B,
+                        double* out_weight, int32_t* out_status, uint32_t flags);
+
+/* Misc */
+int ptsbe_device_memory(int device, uint64_t* free_bytes, uint64_t* total_bytes);
+int ptsbe_synchronize(ptsbe_engine* h);
+void* ptsbe_stream(ptsbe_engine* h);            /* cudaStream_t of the handle */
+int ptsbe_info(ptsbe_engine* h, int64_t* out, int n);  /* {n, dtype, cap, n_passes, tile_bits, ...} */
+int ptsbe_last_error(ptsbe_engine* h, char* buf, size_t len);
+/* Per-launch timing of the fused-pass kernel: when enabled, every pass launch
+ * is bracketed by CUDA events on the handle's stream; profile_read syncs and
+ * returns the accumulated kernel milliseconds and launch count. */
+int ptsbe_profile(ptsbe_engine* h, int enable);
+int ptsbe_profile_read(ptsbe_engine* h, double* total_ms, int64_t* launches);
+/* Kernel launches issued by this handle since creation (for bench gpu_launches). */
+int64_t ptsbe_launch_count(ptsbe_engine* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PTSBE_H */

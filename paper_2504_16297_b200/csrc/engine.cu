@@ -1,0 +1,671 @@
+// engine.cu -- libptsbe.so: the C ABI (include/ptsbe.h) over the sm_100a kernels.
+//
+// Host orchestration only: device buffers, program upload, pass launches,
+// sampler pipeline.  No torch, no Python; the Python package binds this with
+// ctypes (paper_2504_16297_b200/_native.py), which releases the GIL per call.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ptsbe.h"
+#include "pass_kernels.cuh"
+#include "sample_kernels.cuh"
+
+using namespace ptsbe;
+
+struct PassHost {
+  uint64_t qmask;
+  int L, c;
+  int op_begin, n_ops;
+  int slot_begin, n_slots;
+};
+
+struct ptsbe_engine {
+  int dev = 0, n = 0, dtype = 0, cap = 0;
+  size_t amp_bytes = 8;
+  cudaStream_t stream = nullptr;
+  void* states = nullptr;
+  // per-batch
+  uint8_t* d_sel = nullptr;
+  double* d_weight = nullptr;
+  double* d_nst = nullptr;
+  int32_t* d_status = nullptr;
+  int32_t* d_fail = nullptr;
+  int last_B = 0;
+  bool final_general = false;   // stored states carry norm^2 = nst (not yet rescaled)
+  // program
+  bool loaded = false;
+  int n_sites = 0, n_mats = 0;
+  std::vector<PassHost> passes;
+  DevOp* d_ops = nullptr;
+  void* d_mats = nullptr;
+  DevChan* d_chans = nullptr;
+  int32_t* d_site_chan = nullptr;
+  int32_t* d_slot_site = nullptr;
+  double* d_partials = nullptr;
+  size_t partial_cap = 0;
+  // sampler scratch
+  int sbits = 0;
+  long long nblk = 0;
+  uint64_t* d_bs = nullptr;
+  uint64_t* d_total = nullptr;
+  int64_t* d_off = nullptr;
+  int64_t* d_m = nullptr;
+  int64_t* d_nuniq = nullptr;
+  int64_t* d_uoff = nullptr;
+  uint64_t* d_rng = nullptr;
+  size_t shot_cap = 0;
+  uint64_t* d_keys = nullptr;
+  uint64_t* d_tmp = nullptr;
+  uint64_t* d_idx = nullptr;
+  uint64_t* d_runidx = nullptr;
+  uint32_t* d_runcnt = nullptr;
+  size_t chunk_cap = 0;
+  uint64_t* d_chunks = nullptr;
+  long long launches = 0;
+  // optional per-launch timing of the pass kernels (CUDA events on h->stream)
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev;
+  int ev_used = 0;
+  double pass_ms_total = 0.0;
+  long long pass_launches = 0;
+  std::string err;
+};
+
+namespace {
+
+int fail(ptsbe_engine* h, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (h) h->err = buf;
+  return code;
+}
+
+#define CK(h, expr)                                                                     \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail((h), PTSBE_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define CKL(h)                                                                          \
+  do {                                                                                  \
+    (h)->launches++;                                                                    \
+    cudaError_t e_ = cudaGetLastError();                                                \
+    if (e_ != cudaSuccess)                                                              \
+      return fail((h), PTSBE_ERR_CUDA, "kernel launch failed: %s", cudaGetErrorString(e_)); \
+  } while (0)
+
+template <typename T>
+int dalloc(ptsbe_engine* h, T** p, size_t count) {
+  if (*p) { cudaFree(*p); *p = nullptr; }
+  if (count == 0) return 0;
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    return fail(h, PTSBE_ERR_CUDA, "cudaMalloc(%zu bytes) failed: %s", count * sizeof(T), cudaGetErrorString(e));
+  }
+  return 0;
+}
+
+// Copy between a user pointer (host or device per flags) and device memory.
+int copy_in(ptsbe_engine* h, void* dst_dev, const void* src, size_t bytes, uint32_t flags) {
+  if (bytes == 0) return 0;
+  CK(h, cudaMemcpyAsync(dst_dev, src, bytes,
+                        (flags & PTSBE_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                        h->stream));
+  return 0;
+}
+int copy_out(ptsbe_engine* h, void* dst, const void* src_dev, size_t bytes, uint32_t flags) {
+  if (bytes == 0) return 0;
+  CK(h, cudaMemcpyAsync(dst, src_dev, bytes,
+                        (flags & PTSBE_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                        h->stream));
+  return 0;
+}
+
+size_t pass_smem(int L, int c, size_t amp_bytes) {
+  return ((size_t)1 << L) * amp_bytes + (((size_t)1 << L) >> c) * 8 + 32 * 8;
+}
+
+template <typename R>
+int launch_passes(ptsbe_engine* h, int B, bool from_zero) {
+  const size_t per_slot = (size_t)B;
+  bool prev_general = false;
+  if (h->passes.empty()) {
+    if (from_zero) {
+      init_zero_kernel<R><<<1184, 256, 0, h->stream>>>(h->states, h->n, B);
+      CKL(h);
+    }
+    h->final_general = false;
+    return 0;
+  }
+  for (size_t pi = 0; pi < h->passes.size(); ++pi) {
+    const PassHost& ph = h->passes[pi];
+    PassParams p;
+    p.states = h->states;
+    p.n = h->n;
+    p.L = ph.L;
+    p.c = ph.c;
+    p.qmask = ph.qmask;
+    p.ops = h->d_ops + ph.op_begin;
+    p.n_ops = ph.n_ops;
+    p.sel = h->d_sel;
+    p.S = h->n_sites;
+    p.site_chan = h->d_site_chan;
+    p.chans = h->d_chans;
+    p.mats = h->d_mats;
+    p.nst = h->d_nst;
+    p.use_scale = prev_general ? 1 : 0;
+    p.gen_zero = (pi == 0 && from_zero) ? 1 : 0;
+    p.partials = h->d_partials;
+    p.status = h->d_status;
+    p.B = B;
+    p.tiles = 1ll << (h->n - ph.L);
+    const size_t smem = pass_smem(ph.L, ph.c, sizeof(typename Cplx<R>::V));
+    dim3 grid((unsigned)p.tiles, (unsigned)B);
+    if (h->profiling) {
+      while ((int)h->ev.size() < h->ev_used + 2) {
+        cudaEvent_t e;
+        CK(h, cudaEventCreate(&e));
+        h->ev.push_back(e);
+      }
+      CK(h, cudaEventRecord(h->ev[h->ev_used], h->stream));
+    }
+    pass_kernel<R><<<grid, 256, smem, h->stream>>>(p);
+    CKL(h);
+    if (h->profiling) {
+      CK(h, cudaEventRecord(h->ev[h->ev_used + 1], h->stream));
+      h->ev_used += 2;
+    }
+    if (ph.n_slots > 0) {
+      (void)per_slot;
+      norm_finalize<<<B, 256, 0, h->stream>>>(h->d_partials, ph.n_slots, B, p.tiles,
+                                              h->d_slot_site + ph.slot_begin, h->d_nst, h->d_weight,
+                                              h->d_status, h->d_fail);
+      CKL(h);
+    }
+    prev_general = ph.n_slots > 0;
+  }
+  h->final_general = prev_general;
+  return 0;
+}
+
+template <typename R>
+int rescale_if_needed(ptsbe_engine* h) {
+  if (!h->final_general || h->last_B == 0) return 0;
+  scale_states<R><<<1184, 256, 0, h->stream>>>(h->states, h->n, h->last_B, h->d_nst, 1);
+  CKL(h);
+  std::vector<double> ones(h->last_B, 1.0);
+  CK(h, cudaMemcpyAsync(h->d_nst, ones.data(), ones.size() * 8, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  h->final_general = false;
+  return 0;
+}
+
+int run_common(ptsbe_engine* h, const uint8_t* sel, int B, double* out_weight, int32_t* out_status,
+               uint32_t flags, bool from_zero) {
+  if (!h) return PTSBE_ERR_VALIDATION;
+  if (!h->loaded) return fail(h, PTSBE_ERR_VALIDATION, "no program loaded");
+  if (B < 0 || B > h->cap) return fail(h, PTSBE_ERR_VALIDATION, "batch %d exceeds capacity %d", B, h->cap);
+  if (B == 0) return 0;
+  CK(h, cudaSetDevice(h->dev));
+  if (h->n_sites > 0) {
+    if (!sel) return fail(h, PTSBE_ERR_VALIDATION, "selection table is required");
+    if (int r = copy_in(h, h->d_sel, sel, (size_t)B * h->n_sites, flags)) return r;
+  }
+  batch_reset<<<(B + 255) / 256, 256, 0, h->stream>>>(h->d_weight, h->d_nst, h->d_status, h->d_fail, B);
+  CKL(h);
+  h->last_B = B;
+  int r = h->dtype == PTSBE_C64 ? launch_passes<float>(h, B, from_zero) : launch_passes<double>(h, B, from_zero);
+  if (r) return r;
+  if (out_weight)
+    if (int e = copy_out(h, out_weight, h->d_weight, (size_t)B * 8, flags)) return e;
+  if (out_status)
+    if (int e = copy_out(h, out_status, h->d_status, (size_t)B * 4, flags)) return e;
+  if (!(flags & PTSBE_NO_SYNC) || !(flags & PTSBE_DEVICE_PTRS)) CK(h, cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int ensure_shots(ptsbe_engine* h, size_t total, size_t chunks) {
+  if (total > h->shot_cap) {
+    size_t cap = std::max(total, h->shot_cap * 2);
+    int r = 0;
+    r |= dalloc(h, &h->d_keys, cap);
+    r |= dalloc(h, &h->d_tmp, cap);
+    r |= dalloc(h, &h->d_idx, cap);
+    r |= dalloc(h, &h->d_runidx, cap);
+    r |= dalloc(h, &h->d_runcnt, cap);
+    if (r) return PTSBE_ERR_CUDA;
+    h->shot_cap = cap;
+  }
+  if (chunks > h->chunk_cap) {
+    size_t cap = std::max(chunks, h->chunk_cap * 2);
+    if (dalloc(h, &h->d_chunks, cap)) return PTSBE_ERR_CUDA;
+    h->chunk_cap = cap;
+  }
+  return 0;
+}
+
+template <typename R>
+int sample_impl(ptsbe_engine* h, int B, const int64_t* shots, int rng_mode, const uint64_t* rng_state,
+                const uint64_t* keys, uint64_t* out_idx, uint32_t* out_cnt, int64_t* out_nuniq,
+                uint32_t flags) {
+  std::vector<int64_t> m(B), off(B);
+  if (flags & PTSBE_DEVICE_PTRS) {
+    CK(h, cudaMemcpyAsync(m.data(), shots, (size_t)B * 8, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+  } else {
+    std::memcpy(m.data(), shots, (size_t)B * 8);
+  }
+  long long total = 0;
+  std::vector<uint64_t> chunks;
+  for (int b = 0; b < B; ++b) {
+    if (m[b] < 0) return fail(h, PTSBE_ERR_VALIDATION, "shot count must be >= 0, got %lld", (long long)m[b]);
+    off[b] = total;
+    for (long long s = 0; s < m[b]; s += 32) chunks.push_back(((uint64_t)b << 40) | (uint64_t)s);
+    total += m[b];
+  }
+  if (int r = ensure_shots(h, (size_t)std::max<long long>(total, 1), std::max<size_t>(chunks.size(), 1))) return r;
+  CK(h, cudaMemcpyAsync(h->d_m, m.data(), (size_t)B * 8, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(h->d_off, off.data(), (size_t)B * 8, cudaMemcpyHostToDevice, h->stream));
+  if (!chunks.empty())
+    CK(h, cudaMemcpyAsync(h->d_chunks, chunks.data(), chunks.size() * 8, cudaMemcpyHostToDevice, h->stream));
+  const long long n_chunks = (long long)chunks.size();
+
+  SampleParams sp;
+  sp.states = h->states;
+  sp.n = h->n;
+  sp.sbits = h->sbits;
+  sp.nblk = h->nblk;
+  sp.B = B;
+  sp.nst = h->d_nst;
+  sp.status = h->d_status;
+  sp.bs = h->d_bs;
+  sp.total = h->d_total;
+  sp.off = h->d_off;
+  sp.m = h->d_m;
+
+  if (total > 0) {
+    dim3 g1((unsigned)((h->nblk + 7) / 8), (unsigned)B);
+    sample_blocksum<R><<<g1, 256, 0, h->stream>>>(sp);
+    CKL(h);
+    sample_blockscan<<<B, 1024, 0, h->stream>>>(sp);
+    CKL(h);
+    const unsigned gw = (unsigned)((n_chunks * 32 + 255) / 256);
+    if (rng_mode == PTSBE_RNG_PCG64) {
+      if (int r = copy_in(h, h->d_rng, rng_state, (size_t)B * 4 * 8, flags)) return r;
+      keys_pcg64<<<gw, 256, 0, h->stream>>>(h->d_chunks, n_chunks, h->d_rng, h->d_off, h->d_m, h->d_status,
+                                            h->d_keys);
+      CKL(h);
+    } else if (rng_mode == PTSBE_RNG_PHILOX) {
+      if (int r = copy_in(h, h->d_rng, rng_state, (size_t)B * 8, flags)) return r;
+      keys_philox_sorted<<<B, 1024, 0, h->stream>>>(h->d_rng, h->d_off, h->d_m, h->d_status, h->d_keys);
+      CKL(h);
+    } else if (rng_mode == PTSBE_RNG_KEYS) {
+      if (int r = copy_in(h, h->d_keys, keys, (size_t)total * 8, flags)) return r;
+    } else {
+      return fail(h, PTSBE_ERR_VALIDATION, "unknown rng mode %d", rng_mode);
+    }
+    if (rng_mode != PTSBE_RNG_PHILOX) {
+      seg_radix_sort<<<B, 1024, 0, h->stream>>>(h->d_keys, h->d_tmp, h->d_off, h->d_m, h->d_status, 53);
+      CKL(h);
+    }
+    sample_resolve<R><<<gw, 256, 0, h->stream>>>(sp, h->d_chunks, n_chunks, h->d_keys, h->d_idx);
+    CKL(h);
+  }
+  sample_rle<<<B, 1024, 0, h->stream>>>(h->d_idx, h->d_off, h->d_m, h->d_status, h->d_runidx, h->d_runcnt,
+                                        h->d_nuniq);
+  CKL(h);
+  std::vector<int64_t> nu(B), uoff(B);
+  CK(h, cudaMemcpyAsync(nu.data(), h->d_nuniq, (size_t)B * 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  long long U = 0;
+  long long maxnu = 0;
+  for (int b = 0; b < B; ++b) { uoff[b] = U; U += nu[b]; maxnu = std::max<long long>(maxnu, nu[b]); }
+  if (flags & PTSBE_DEVICE_PTRS) {
+    CK(h, cudaMemcpyAsync(out_nuniq, h->d_nuniq, (size_t)B * 8, cudaMemcpyDeviceToDevice, h->stream));
+  } else {
+    std::memcpy(out_nuniq, nu.data(), (size_t)B * 8);
+  }
+  if (U > 0) {
+    CK(h, cudaMemcpyAsync(h->d_uoff, uoff.data(), (size_t)B * 8, cudaMemcpyHostToDevice, h->stream));
+    // compact into keys/tmp scratch, then hand out one contiguous CSR stream
+    uint64_t* cidx = h->d_keys;
+    uint32_t* ccnt = reinterpret_cast<uint32_t*>(h->d_tmp);
+    dim3 gc((unsigned)std::min<long long>((maxnu + 255) / 256, 4096), (unsigned)B);
+    compact_runs<<<gc, 256, 0, h->stream>>>(h->d_runidx, h->d_runcnt, h->d_off, h->d_nuniq, h->d_uoff, cidx, ccnt);
+    CKL(h);
+    if (int r = copy_out(h, out_idx, cidx, (size_t)U * 8, flags)) return r;
+    if (int r = copy_out(h, out_cnt, ccnt, (size_t)U * 4, flags)) return r;
+  }
+  if (!(flags & PTSBE_NO_SYNC) || !(flags & PTSBE_DEVICE_PTRS)) CK(h, cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ptsbe_abi_version(void) { return PTSBE_ABI_VERSION; }
+
+int ptsbe_create(int device, int n_qubits, int dtype, int batch_cap, ptsbe_engine** out) {
+  if (!out) return PTSBE_ERR_VALIDATION;
+  *out = nullptr;
+  if (n_qubits < 1 || n_qubits > 40) return PTSBE_ERR_VALIDATION;
+  if (dtype != PTSBE_C64 && dtype != PTSBE_C128) return PTSBE_ERR_VALIDATION;
+  if (batch_cap < 1) return PTSBE_ERR_VALIDATION;
+  ptsbe_engine* h = new ptsbe_engine();
+  h->dev = device;
+  h->n = n_qubits;
+  h->dtype = dtype;
+  h->cap = batch_cap;
+  h->amp_bytes = dtype == PTSBE_C64 ? 8 : 16;
+  h->sbits = std::min(n_qubits, 9);
+  h->nblk = 1ll << (n_qubits - h->sbits);
+  int r = 0;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    r = fail(h, PTSBE_ERR_CUDA, "device %d unavailable: %s", device, cudaGetErrorString(e));
+  }
+  if (!r) {
+    const size_t bytes = (size_t)batch_cap * ((size_t)1 << n_qubits) * h->amp_bytes;
+    e = cudaMalloc(&h->states, bytes);
+    if (e != cudaSuccess) r = fail(h, PTSBE_ERR_CUDA, "cannot allocate %zu bytes of state: %s", bytes, cudaGetErrorString(e));
+  }
+  if (!r) r = dalloc(h, &h->d_weight, batch_cap);
+  if (!r) r = dalloc(h, &h->d_nst, batch_cap);
+  if (!r) r = dalloc(h, &h->d_status, batch_cap);
+  if (!r) r = dalloc(h, &h->d_fail, batch_cap);
+  if (!r) r = dalloc(h, &h->d_bs, (size_t)batch_cap * h->nblk);
+  if (!r) r = dalloc(h, &h->d_total, batch_cap);
+  if (!r) r = dalloc(h, &h->d_off, batch_cap);
+  if (!r) r = dalloc(h, &h->d_m, batch_cap);
+  if (!r) r = dalloc(h, &h->d_nuniq, batch_cap);
+  if (!r) r = dalloc(h, &h->d_uoff, batch_cap);
+  if (!r) r = dalloc(h, &h->d_rng, (size_t)batch_cap * 4);
+  if (!r) {
+    std::vector<double> ones(batch_cap, 1.0);
+    std::vector<int32_t> zeros(batch_cap, 0);
+    e = cudaMemcpy(h->d_nst, ones.data(), batch_cap * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(h->d_status, zeros.data(), batch_cap * 4, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) r = fail(h, PTSBE_ERR_CUDA, "init copy failed: %s", cudaGetErrorString(e));
+  }
+  if (r) {
+    // keep the handle so the caller can read the error, then destroy it
+    *out = h;
+    return r;
+  }
+  *out = h;
+  return 0;
+}
+
+int ptsbe_destroy(ptsbe_engine* h) {
+  if (!h) return 0;
+  cudaSetDevice(h->dev);
+  void* ptrs[] = {h->states, h->d_sel, h->d_weight, h->d_nst, h->d_status, h->d_fail, h->d_ops, h->d_mats,
+                  h->d_chans, h->d_site_chan, h->d_slot_site, h->d_partials, h->d_bs, h->d_total, h->d_off,
+                  h->d_m, h->d_nuniq, h->d_uoff, h->d_rng, h->d_keys, h->d_tmp, h->d_idx, h->d_runidx,
+                  h->d_runcnt, h->d_chunks};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return 0;
+}
+
+int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const double* mats, int n_mats,
+                       const ptsbe_channel* chans, int n_chans, const int32_t* site_chan, int n_sites,
+                       const ptsbe_pass* passes, int n_passes) {
+  if (!h) return PTSBE_ERR_VALIDATION;
+  CK(h, cudaSetDevice(h->dev));
+  h->loaded = false;
+  if (n_ops < 0 || n_mats < 0 || n_chans < 0 || n_sites < 0 || n_passes < 0)
+    return fail(h, PTSBE_ERR_VALIDATION, "negative table size");
+  if (n_sites > 0 && n_chans == 0) return fail(h, PTSBE_ERR_VALIDATION, "sites without channels");
+  for (int s = 0; s < n_sites; ++s)
+    if (site_chan[s] < 0 || site_chan[s] >= n_chans)
+      return fail(h, PTSBE_ERR_VALIDATION, "site %d references channel %d", s, site_chan[s]);
+  for (int k = 0; k < n_chans; ++k) {
+    if (chans[k].n_outcomes < 1 || chans[k].n_outcomes > 64 || chans[k].mat_base < 0 ||
+        chans[k].mat_base + chans[k].n_outcomes > n_mats)
+      return fail(h, PTSBE_ERR_VALIDATION, "channel %d has an invalid matrix range", k);
+    if (chans[k].general && chans[k].identity_mask)
+      return fail(h, PTSBE_ERR_VALIDATION, "channel %d: identity skipping is for unitary mixtures only", k);
+  }
+  std::vector<PassHost> ph(n_passes);
+  std::vector<DevOp> dops(n_ops);
+  std::vector<int32_t> slot_site;
+  for (int p = 0; p < n_passes; ++p) {
+    const ptsbe_pass& P = passes[p];
+    const uint64_t nmask = (h->n >= 64) ? ~0ull : ((1ull << h->n) - 1);
+    if ((P.qubit_mask & ~nmask) || __builtin_popcountll(P.qubit_mask) != P.tile_bits)
+      return fail(h, PTSBE_ERR_VALIDATION, "pass %d: qubit mask does not match tile_bits", p);
+    if (P.tile_bits < 1 || P.tile_bits > 13)
+      return fail(h, PTSBE_ERR_VALIDATION, "pass %d: tile_bits %d outside [1, 13]", p, P.tile_bits);
+    const int min_low = std::min(h->n, h->dtype == PTSBE_C64 ? 1 : 0);
+    if (P.low_bits < min_low || P.low_bits > P.tile_bits ||
+        (P.qubit_mask & ((1ull << P.low_bits) - 1)) != ((1ull << P.low_bits) - 1))
+      return fail(h, PTSBE_ERR_VALIDATION, "pass %d: low_bits %d not contiguous in the mask", p, P.low_bits);
+    ph[p] = PassHost{P.qubit_mask, P.tile_bits, P.low_bits, 0, 0, 0, 0};
+  }
+  int prev_pass = -1;
+  for (int i = 0; i < n_ops; ++i) {
+    const ptsbe_op& o = ops[i];
+    if (o.pass < 0 || o.pass >= n_passes || o.pass < prev_pass)
+      return fail(h, PTSBE_ERR_VALIDATION, "op %d: pass index %d out of order", i, o.pass);
+    if (o.arity != 1 && o.arity != 2)
+      return fail(h, PTSBE_ERR_VALIDATION, "op %d: arity %d unsupported on device (1 or 2)", i, o.arity);
+    PassHost& P = ph[o.pass];
+    if (o.pass != prev_pass) { P.op_begin = i; P.slot_begin = (int)slot_site.size(); }
+    prev_pass = o.pass;
+    P.n_ops++;
+    auto local = [&](int q) -> int {
+      if (q < 0 || q >= h->n || !((P.qmask >> q) & 1)) return -1;
+      return __builtin_popcountll(P.qmask & ((1ull << q) - 1));
+    };
+    DevOp d;
+    d.kind = o.kind;
+    d.arity = o.arity;
+    d.b0 = local(o.t0);
+    d.b1 = o.arity == 2 ? local(o.t1) : -1;
+    d.ref = o.ref;
+    d.slot = -1;
+    if (d.b0 < 0 || (o.arity == 2 && (d.b1 < 0 || o.t0 == o.t1)))
+      return fail(h, PTSBE_ERR_VALIDATION, "op %d: targets not inside its pass's qubit set", i);
+    if (o.kind == 0) {
+      if (o.ref < 0 || o.ref >= n_mats) return fail(h, PTSBE_ERR_VALIDATION, "op %d: matrix %d", i, o.ref);
+    } else if (o.kind == 1) {
+      if (o.ref < 0 || o.ref >= n_sites) return fail(h, PTSBE_ERR_VALIDATION, "op %d: site %d", i, o.ref);
+      const ptsbe_channel& ch = chans[site_chan[o.ref]];
+      if (ch.arity != o.arity) return fail(h, PTSBE_ERR_VALIDATION, "op %d: channel arity mismatch", i);
+      if (ch.general) {
+        d.slot = P.n_slots++;
+        slot_site.push_back(o.ref);
+      }
+    } else {
+      return fail(h, PTSBE_ERR_VALIDATION, "op %d: unknown kind %d", i, o.kind);
+    }
+    dops[i] = d;
+  }
+  int max_slots = 0;
+  for (auto& P : ph) max_slots = std::max(max_slots, P.n_slots);
+  for (int p = 0; p < n_passes; ++p) {
+    const size_t smem = pass_smem(ph[p].L, ph[p].c, h->amp_bytes);
+    if (smem > 227 * 1024) return fail(h, PTSBE_ERR_VALIDATION, "pass %d needs %zu B shared memory", p, smem);
+  }
+  // device tables
+  if (dalloc(h, &h->d_ops, std::max(n_ops, 1))) return PTSBE_ERR_CUDA;
+  if (n_ops) CK(h, cudaMemcpy(h->d_ops, dops.data(), n_ops * sizeof(DevOp), cudaMemcpyHostToDevice));
+  {
+    const size_t nm = std::max(n_mats, 1);
+    if (h->dtype == PTSBE_C64) {
+      std::vector<float> f(nm * 32, 0.f);
+      for (size_t i = 0; i < (size_t)n_mats * 32; ++i) f[i] = (float)mats[i];
+      float* d = nullptr;
+      if (dalloc(h, &d, f.size())) return PTSBE_ERR_CUDA;
+      if (h->d_mats) cudaFree(h->d_mats);
+      h->d_mats = d;
+      CK(h, cudaMemcpy(d, f.data(), f.size() * 4, cudaMemcpyHostToDevice));
+    } else {
+      double* d = nullptr;
+      if (dalloc(h, &d, nm * 32)) return PTSBE_ERR_CUDA;
+      if (h->d_mats) cudaFree(h->d_mats);
+      h->d_mats = d;
+      if (n_mats) CK(h, cudaMemcpy(d, mats, (size_t)n_mats * 32 * 8, cudaMemcpyHostToDevice));
+    }
+  }
+  std::vector<DevChan> dch(std::max(n_chans, 1));
+  for (int k = 0; k < n_chans; ++k)
+    dch[k] = DevChan{chans[k].n_outcomes, chans[k].mat_base, chans[k].general, chans[k].arity, chans[k].identity_mask};
+  if (dalloc(h, &h->d_chans, dch.size())) return PTSBE_ERR_CUDA;
+  CK(h, cudaMemcpy(h->d_chans, dch.data(), dch.size() * sizeof(DevChan), cudaMemcpyHostToDevice));
+  if (dalloc(h, &h->d_site_chan, std::max(n_sites, 1))) return PTSBE_ERR_CUDA;
+  if (n_sites) CK(h, cudaMemcpy(h->d_site_chan, site_chan, n_sites * 4, cudaMemcpyHostToDevice));
+  if (dalloc(h, &h->d_slot_site, std::max<size_t>(slot_site.size(), 1))) return PTSBE_ERR_CUDA;
+  if (!slot_site.empty())
+    CK(h, cudaMemcpy(h->d_slot_site, slot_site.data(), slot_site.size() * 4, cudaMemcpyHostToDevice));
+  if (dalloc(h, &h->d_sel, (size_t)h->cap * std::max(n_sites, 1))) return PTSBE_ERR_CUDA;
+  size_t need = 1;
+  for (auto& P : ph)
+    if (P.n_slots) need = std::max(need, (size_t)P.n_slots * h->cap * ((size_t)1 << (h->n - P.L)));
+  if (need > h->partial_cap) {
+    if (dalloc(h, &h->d_partials, need)) return PTSBE_ERR_CUDA;
+    h->partial_cap = need;
+  }
+  for (int p = 0; p < n_passes; ++p) {
+    const size_t smem = pass_smem(ph[p].L, ph[p].c, h->amp_bytes);
+    if (smem > 48 * 1024) {
+      if (h->dtype == PTSBE_C64)
+        CK(h, cudaFuncSetAttribute(pass_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      else
+        CK(h, cudaFuncSetAttribute(pass_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    }
+  }
+  h->passes = ph;
+  h->n_sites = n_sites;
+  h->n_mats = n_mats;
+  h->loaded = true;
+  return 0;
+}
+
+int ptsbe_run_batch(ptsbe_engine* h, const uint8_t* sel, int B, double* out_weight, int32_t* out_status,
+                    uint32_t flags) {
+  return run_common(h, sel, B, out_weight, out_status, flags, true);
+}
+
+int ptsbe_apply_program(ptsbe_engine* h, const uint8_t* sel, int B, double* out_weight, int32_t* out_status,
+                        uint32_t flags) {
+  return run_common(h, sel, B, out_weight, out_status, flags, false);
+}
+
+int ptsbe_sample(ptsbe_engine* h, int B, const int64_t* shots, int rng_mode, const uint64_t* rng_state,
+                 const uint64_t* keys, uint64_t* out_idx, uint32_t* out_cnt, int64_t* out_nuniq, uint32_t flags) {
+  if (!h) return PTSBE_ERR_VALIDATION;
+  if (B < 0 || B > h->last_B) return fail(h, PTSBE_ERR_VALIDATION, "batch %d exceeds the %d prepared states", B, h->last_B);
+  if (B == 0) return 0;
+  CK(h, cudaSetDevice(h->dev));
+  return h->dtype == PTSBE_C64
+             ? sample_impl<float>(h, B, shots, rng_mode, rng_state, keys, out_idx, out_cnt, out_nuniq, flags)
+             : sample_impl<double>(h, B, shots, rng_mode, rng_state, keys, out_idx, out_cnt, out_nuniq, flags);
+}
+
+int ptsbe_get_state(ptsbe_engine* h, int b, void* buf, uint32_t flags) {
+  if (!h) return PTSBE_ERR_VALIDATION;
+  if (b < 0 || b >= h->cap) return fail(h, PTSBE_ERR_VALIDATION, "state %d out of range", b);
+  CK(h, cudaSetDevice(h->dev));
+  int r = h->dtype == PTSBE_C64 ? rescale_if_needed<float>(h) : rescale_if_needed<double>(h);
+  if (r) return r;
+  const size_t bytes = ((size_t)1 << h->n) * h->amp_bytes;
+  if (int e = copy_out(h, buf, (char*)h->states + (size_t)b * bytes, bytes, flags)) return e;
+  CK(h, cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int ptsbe_set_state(ptsbe_engine* h, int b, const void* buf, uint32_t flags) {
+  if (!h) return PTSBE_ERR_VALIDATION;
+  if (b < 0 || b >= h->cap) return fail(h, PTSBE_ERR_VALIDATION, "state %d out of range", b);
+  CK(h, cudaSetDevice(h->dev));
+  const size_t bytes = ((size_t)1 << h->n) * h->amp_bytes;
+  if (int e = copy_in(h, (char*)h->states + (size_t)b * bytes, buf, bytes, flags)) return e;
+  const double one = 1.0;
+  const int32_t zero = 0;
+  CK(h, cudaMemcpyAsync(h->d_nst + b, &one, 8, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaMemcpyAsync(h->d_status + b, &zero, 4, cudaMemcpyHostToDevice, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  h->last_B = std::max(h->last_B, b + 1);
+  h->final_general = false;
+  return 0;
+}
+
+int ptsbe_device_memory(int device, uint64_t* free_bytes, uint64_t* total_bytes) {
+  if (cudaSetDevice(device) != cudaSuccess) return PTSBE_ERR_CUDA;
+  size_t f = 0, t = 0;
+  if (cudaMemGetInfo(&f, &t) != cudaSuccess) return PTSBE_ERR_CUDA;
+  if (free_bytes) *free_bytes = f;
+  if (total_bytes) *total_bytes = t;
+  return 0;
+}
+
+int ptsbe_synchronize(ptsbe_engine* h) {
+  if (!h) return PTSBE_ERR_VALIDATION;
+  CK(h, cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+void* ptsbe_stream(ptsbe_engine* h) { return h ? (void*)h->stream : nullptr; }
+
+int ptsbe_profile(ptsbe_engine* h, int enable) {
+  if (!h) return PTSBE_ERR_VALIDATION;
+  h->profiling = enable != 0;
+  h->ev_used = 0;
+  h->pass_ms_total = 0.0;
+  h->pass_launches = 0;
+  return 0;
+}
+
+int ptsbe_profile_read(ptsbe_engine* h, double* total_ms, int64_t* launches) {
+  if (!h) return PTSBE_ERR_VALIDATION;
+  CK(h, cudaStreamSynchronize(h->stream));
+  for (int i = 0; i + 1 < h->ev_used; i += 2) {
+    float ms = 0.f;
+    CK(h, cudaEventElapsedTime(&ms, h->ev[i], h->ev[i + 1]));
+    h->pass_ms_total += ms;
+    h->pass_launches++;
+  }
+  h->ev_used = 0;
+  if (total_ms) *total_ms = h->pass_ms_total;
+  if (launches) *launches = h->pass_launches;
+  return 0;
+}
+
+int ptsbe_info(ptsbe_engine* h, int64_t* out, int n) {
+  if (!h || !out) return PTSBE_ERR_VALIDATION;
+  int max_tile = 0, total_slots = 0;
+  for (auto& P : h->passes) { max_tile = std::max(max_tile, P.L); total_slots += P.n_slots; }
+  const int64_t vals[] = {h->n, h->dtype, h->cap, (int64_t)h->passes.size(), max_tile, h->n_sites,
+                          h->sbits, total_slots, h->launches};
+  for (int i = 0; i < n && i < (int)(sizeof vals / sizeof vals[0]); ++i) out[i] = vals[i];
+  return 0;
+}
+
+int ptsbe_last_error(ptsbe_engine* h, char* buf, size_t len) {
+  if (!buf || len == 0) return PTSBE_ERR_VALIDATION;
+  const std::string& s = h ? h->err : std::string("null handle");
+  std::snprintf(buf, len, "%s", s.c_str());
+  return 0;
+}
+
+int64_t ptsbe_launch_count(ptsbe_engine* h) { return h ? h->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,213 @@
+"""Python handle over one ``libptsbe.so`` engine (one device, one batch of states).
+
+``Engine`` owns a device-resident batch of ``batch_cap`` statevectors of
+2^n amplitudes (complex64 or complex128, qubit q = bit q of the index) and a
+loaded program.  ``run`` prepares B trajectories at once from an outcome table
+(the batched form of ``prepare_state``, reference ``execute.py:74-98``);
+``sample`` draws every trajectory's shots in bulk (``sample_shots``,
+``statevector.py:148-163``) and returns them run-length encoded.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .errors import ValidationError
+from .program import Program, compile_circuit
+
+DTYPES = {"c64": (N.PTSBE_C64, np.complex64), "c128": (N.PTSBE_C128, np.complex128)}
+
+
+def _ptr(a: np.ndarray):
+    return C.c_void_p(a.ctypes.data) if a is not None and a.size else None
+
+
+def device_memory(device: int = 0):
+    lib = N.load_library()
+    free, total = C.c_uint64(), C.c_uint64()
+    N.check(lib, None, lib.ptsbe_device_memory(device, C.byref(free), C.byref(total)), "device memory query")
+    return int(free.value), int(total.value)
+
+
+@dataclass
+class Shots:
+    """CSR shot output of one sample() call: trajectory b owns rows [offsets[b], offsets[b+1])."""
+
+    indices: np.ndarray    # uint64 basis indices, ascending per trajectory
+    counts: np.ndarray     # uint32
+    offsets: np.ndarray    # int64, len B+1
+
+    def counts_dict(self, b: int, n_qubits: int) -> dict:
+        lo, hi = int(self.offsets[b]), int(self.offsets[b + 1])
+        fmt = f"0{n_qubits}b"
+        return {format(int(v), fmt): int(c) for v, c in zip(self.indices[lo:hi], self.counts[lo:hi])}
+
+
+class Engine:
+    def __init__(self, n_qubits: int, dtype: str = "c128", batch_cap: int = 1, device: int = 0):
+        if dtype not in DTYPES:
+            raise ValidationError(f"dtype must be one of {sorted(DTYPES)}, got {dtype!r}")
+        self.lib = N.load_library()
+        self.n = int(n_qubits)
+        self.dtype = dtype
+        self.np_dtype = DTYPES[dtype][1]
+        self.cap = int(batch_cap)
+        self.device = int(device)
+        self.program: Program | None = None
+        h = C.c_void_p()
+        st = self.lib.ptsbe_create(self.device, self.n, DTYPES[dtype][0], self.cap, C.byref(h))
+        self.h = h
+        if st != 0:
+            msg = N.last_error(self.lib, h) if h.value else "invalid arguments"
+            if h.value:
+                self.lib.ptsbe_destroy(h)
+            self.h = C.c_void_p()
+            N.check(self.lib, None, st, f"ptsbe_create(n={n_qubits}, {dtype}, cap={batch_cap}): {msg}")
+
+    # -- lifetime
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.ptsbe_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def _check(self, st, what):
+        N.check(self.lib, self.h, st, what)
+
+    # -- program
+    def load(self, circuit, **plan_kw) -> Program:
+        prog = compile_circuit(circuit, self.dtype, **plan_kw)
+        self.load_program(prog)
+        return prog
+
+    def load_program(self, prog: Program) -> None:
+        if prog.n_qubits != self.n:
+            raise ValidationError(f"program is for {prog.n_qubits} qubits, engine holds {self.n}")
+        order = [(p, i) for p, plan in enumerate(prog.passes) for i in plan.ops]
+        ops = (N.Op * max(len(order), 1))()
+        for j, (p, i) in enumerate(order):
+            so = prog.stream[i]
+            t1 = so.targets[1] if len(so.targets) > 1 else -1
+            ops[j] = N.Op(so.kind, len(so.targets), so.targets[0], t1, so.ref, p)
+        mats = np.ascontiguousarray(prog.mats.reshape(-1, 16)).view(np.float64).reshape(-1)
+        chans = (N.Channel * max(len(prog.chans), 1))()
+        for k, ch in enumerate(prog.chans):
+            chans[k] = N.Channel(ch["n_outcomes"], ch["mat_base"], ch["general"], ch["arity"], ch["identity_mask"])
+        site_chan = np.ascontiguousarray(prog.site_chan, dtype=np.int32)
+        passes = (N.Pass * max(len(prog.passes), 1))()
+        for p, plan in enumerate(prog.passes):
+            passes[p] = N.Pass(plan.mask, len(plan.qubits), plan.low_bits)
+        mats = np.ascontiguousarray(mats)
+        st = self.lib.ptsbe_load_program(self.h, ops, len(order), _ptr(mats), int(prog.mats.shape[0]),
+                                         chans, len(prog.chans), _ptr(site_chan), int(site_chan.size),
+                                         passes, len(prog.passes))
+        self._check(st, "ptsbe_load_program")
+        self.program = prog
+
+    # -- execution
+    def run(self, sel: np.ndarray, apply_only: bool = False):
+        """Prepare len(sel) trajectories; returns (weights float64[B], status int32[B])."""
+        sel = np.ascontiguousarray(sel, dtype=np.uint8)
+        B = sel.shape[0]
+        w = np.empty(B, dtype=np.float64)
+        s = np.empty(B, dtype=np.int32)
+        fn = self.lib.ptsbe_apply_program if apply_only else self.lib.ptsbe_run_batch
+        self._check(fn(self.h, _ptr(sel), B, _ptr(w), _ptr(s), 0), "ptsbe_run_batch")
+        return w, s
+
+    def run_device(self, sel_ptr: int, B: int, w_ptr: int, s_ptr: int, sync: bool = False):
+        """Device-pointer variant (inputs already resident in HBM)."""
+        flags = N.PTSBE_DEVICE_PTRS | (0 if sync else N.PTSBE_NO_SYNC)
+        self._check(self.lib.ptsbe_run_batch(self.h, C.c_void_p(sel_ptr), B, C.c_void_p(w_ptr),
+                                             C.c_void_p(s_ptr), flags), "ptsbe_run_batch")
+
+    def sample(self, shots, rng_mode: int = N.RNG_PCG64, rng_state=None, keys=None) -> Shots:
+        shots = np.ascontiguousarray(shots, dtype=np.int64)
+        B = shots.size
+        total = int(shots.sum()) if B else 0
+        idx = np.empty(max(total, 1), dtype=np.uint64)
+        cnt = np.empty(max(total, 1), dtype=np.uint32)
+        nu = np.zeros(B, dtype=np.int64)
+        rs = None if rng_state is None else np.ascontiguousarray(rng_state, dtype=np.uint64)
+        ks = None if keys is None else np.ascontiguousarray(keys, dtype=np.uint64)
+        st = self.lib.ptsbe_sample(self.h, B, _ptr(shots), rng_mode, _ptr(rs), _ptr(ks),
+                                   _ptr(idx), _ptr(cnt), _ptr(nu), 0)
+        self._check(st, "ptsbe_sample")
+        off = np.zeros(B + 1, dtype=np.int64)
+        np.cumsum(nu, out=off[1:])
+        U = int(off[-1])
+        return Shots(idx[:U], cnt[:U], off)
+
+    def sample_device(self, B: int, shots_ptr: int, rng_mode: int, rng_ptr: int, idx_ptr: int, cnt_ptr: int,
+                      nuniq_ptr: int, sync: bool = False) -> None:
+        """Device-pointer variant of sample(): inputs and CSR outputs stay in HBM."""
+        flags = N.PTSBE_DEVICE_PTRS | (0 if sync else N.PTSBE_NO_SYNC)
+        st = self.lib.ptsbe_sample(self.h, B, C.c_void_p(shots_ptr), rng_mode, C.c_void_p(rng_ptr), None,
+                                   C.c_void_p(idx_ptr), C.c_void_p(cnt_ptr), C.c_void_p(nuniq_ptr), flags)
+        self._check(st, "ptsbe_sample")
+
+    def get_state(self, b: int = 0) -> np.ndarray:
+        out = np.empty(1 << self.n, dtype=self.np_dtype)
+        self._check(self.lib.ptsbe_get_state(self.h, b, _ptr(out), 0), "ptsbe_get_state")
+        return out
+
+    def set_state(self, b: int, amps: np.ndarray) -> None:
+        a = np.ascontiguousarray(amps, dtype=self.np_dtype)
+        if a.size != 1 << self.n:
+            raise ValidationError(f"state has {a.size} amplitudes, expected {1 << self.n}")
+        self._check(self.lib.ptsbe_set_state(self.h, b, _ptr(a), 0), "ptsbe_set_state")
+
+    def synchronize(self):
+        self._check(self.lib.ptsbe_synchronize(self.h), "ptsbe_synchronize")
+
+    @property
+    def stream(self) -> int:
+        return int(self.lib.ptsbe_stream(self.h) or 0)
+
+    @property
+    def launches(self) -> int:
+        return int(self.lib.ptsbe_launch_count(self.h))
+
+    def profile(self, enable: bool = True) -> None:
+        self._check(self.lib.ptsbe_profile(self.h, 1 if enable else 0), "ptsbe_profile")
+
+    def profile_read(self):
+        """(total pass-kernel ms, pass launches) since profile(True)."""
+        ms, n = C.c_double(), C.c_int64()
+        self._check(self.lib.ptsbe_profile_read(self.h, C.byref(ms), C.byref(n)), "ptsbe_profile_read")
+        return float(ms.value), int(n.value)
+
+    def info(self) -> dict:
+        out = np.zeros(9, dtype=np.int64)
+        self._check(self.lib.ptsbe_info(self.h, _ptr(out), out.size), "ptsbe_info")
+        keys = ("n", "dtype", "cap", "n_passes", "tile_bits", "n_sites", "sample_bits", "norm_slots", "launches")
+        return dict(zip(keys, (int(v) for v in out)))
+
+
+def pcg64_state_words(seed_or_rng) -> np.ndarray:
+    """(state_hi, state_lo, inc_hi, inc_lo) of a numpy PCG64 stream, for RNG_PCG64."""
+    if isinstance(seed_or_rng, np.random.Generator):
+        bg = seed_or_rng.bit_generator
+    else:
+        bg = np.random.PCG64(int(seed_or_rng))
+    st = bg.state
+    if st.get("bit_generator") != "PCG64":
+        raise ValidationError("not a PCG64 stream")
+    s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
+    m = (1 << 64) - 1
+    return np.array([s >> 64, s & m, inc >> 64, inc & m], dtype=np.uint64)

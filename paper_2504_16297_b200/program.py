@@ -1,0 +1,224 @@
+"""Host compiler: NoisyCircuit -> device program (op stream, operator table, fused passes).
+
+The reference evolves a trajectory by walking ``circuit.ops`` and, after each
+gate, firing that gate's noise sites in site-id order with outcome
+``chosen.get(site, 0)`` (``execute.py:85-97``) -- one full numpy pass per op
+and per site.  This module lowers the same sequence once per circuit:
+
+* a linear op stream: gate, then its sites (site-id order); a site op carries
+  the site id and its channel, the outcome is read per trajectory on device;
+* an operator table (complex128, 4x4 padded): gate matrices, unitary-mixture
+  ``U_k`` (``noise.py:100-119``) or general ``K_k`` per channel outcome, with a
+  mask of outcomes that are exactly the identity (skipped on device -- the
+  builtin mixtures' ``U_0`` is exactly I, so the skip is bit-exact);
+* a fusion plan: a partition of the stream into passes.  Each pass owns a
+  tile qubit set Q (|Q| = L, always containing qubits 0..c-1 so tile rows are
+  >= 128 B contiguous) and takes every op whose targets lie in Q and whose
+  predecessors on those qubits already ran.  A pass is one HBM read + write
+  of every state in the batch, regardless of how many ops it absorbs.
+
+Planner: greedy in stream order.  Ops whose targets fit in the growing set
+join; an op that does not fit blocks its qubits for the rest of the pass
+(later ops on them depend on it), ops on untouched qubits keep flowing.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .errors import ValidationError
+
+KIND_GATE = 0
+KIND_SITE = 1
+
+DEFAULT_TILE_BITS = {"c64": 12, "c128": 11}
+DEFAULT_LOW_BITS = {"c64": 4, "c128": 3}     # 16 x 8 B / 8 x 16 B = 128-B rows
+
+
+@dataclass
+class StreamOp:
+    kind: int
+    targets: tuple
+    ref: int              # gate: matrix index; site: site id
+    pos: int              # op position in circuit.ops
+
+
+@dataclass
+class PassPlan:
+    qubits: tuple         # sorted tile qubit set
+    low_bits: int         # contiguous run 0..c-1 inside qubits
+    ops: list             # stream indices, execution order
+
+    @property
+    def mask(self) -> int:
+        m = 0
+        for q in self.qubits:
+            m |= 1 << q
+        return m
+
+
+@dataclass
+class Program:
+    n_qubits: int
+    stream: list
+    mats: np.ndarray              # (n_mats, 4, 4) complex128
+    chans: list                   # dicts: n_outcomes, mat_base, general, arity, identity_mask
+    chan_index: dict              # channel_id -> channel row
+    site_chan: np.ndarray         # (S,) int32
+    passes: list = field(default_factory=list)
+    g_ref: int = 0                # reference-equivalent full-state passes: #ops + #sites
+
+    @property
+    def n_sites(self) -> int:
+        return int(self.site_chan.size)
+
+    @property
+    def n_passes(self) -> int:
+        return len(self.passes)
+
+
+class _MatTable:
+    def __init__(self):
+        self.rows = []
+        self.index = {}
+
+    def add(self, m: np.ndarray, dedupe: bool = True) -> int:
+        m = np.asarray(m, dtype=np.complex128)
+        d = m.shape[0]
+        pad = np.zeros((4, 4), dtype=np.complex128)
+        pad[:d, :d] = m
+        key = (d, pad.tobytes())
+        if dedupe and key in self.index:
+            return self.index[key]
+        self.rows.append(pad)
+        self.index[key] = len(self.rows) - 1
+        return len(self.rows) - 1
+
+
+def _is_identity(m: np.ndarray) -> bool:
+    return bool(np.array_equal(m, np.eye(m.shape[0], dtype=np.complex128)))
+
+
+def lower(circuit) -> Program:
+    """Op stream + operator table of a circuit (no fusion yet)."""
+    table = _MatTable()
+    chans, chan_index = [], {}
+    for cid, ch in circuit.channels.items():
+        if ch.arity > 2:
+            raise ValidationError(f"channel '{cid}': arity {ch.arity} unsupported on device (1 or 2)")
+        mix = ch.unitary_mixture()
+        ops = list(mix.unitaries) if mix is not None else list(ch.kraus_ops)
+        if len(ops) > 64:
+            raise ValidationError(f"channel '{cid}' has {len(ops)} outcomes (device limit 64)")
+        base = len(table.rows)
+        ident = 0
+        for k, m in enumerate(ops):
+            table.add(m, dedupe=False)
+            if mix is not None and _is_identity(m):
+                ident |= 1 << k
+        chan_index[cid] = len(chans)
+        chans.append(dict(n_outcomes=len(ops), mat_base=base, general=int(mix is None),
+                          arity=ch.arity, identity_mask=ident))
+    site_chan = np.array([chan_index[s.channel_id] for s in circuit.sites], dtype=np.int32)
+    by_pos = circuit.sites_by_position()
+    stream = []
+    for pos, op in enumerate(circuit.ops):
+        k = len(op.targets)
+        if k > 2:
+            raise ValidationError(f"op {pos} ('{op.name}') acts on {k} qubits; the device engine supports 1 or 2")
+        if not _is_identity(op.matrix):
+            stream.append(StreamOp(KIND_GATE, tuple(op.targets), table.add(op.matrix), pos))
+        for s in by_pos.get(pos, ()):
+            stream.append(StreamOp(KIND_SITE, tuple(s.targets), s.site_id, pos))
+    mats = np.array(table.rows, dtype=np.complex128).reshape(-1, 4, 4)
+    return Program(circuit.n_qubits, stream, mats, chans, chan_index, site_chan,
+                   g_ref=len(circuit.ops) + len(circuit.sites))
+
+
+def plan_passes(n: int, stream: list, tile_bits: int, low_bits: int) -> list:
+    """Greedy qubit-set fusion of the op stream into passes (see module docstring)."""
+    L = min(n, tile_bits)
+    if n <= L:
+        return [PassPlan(tuple(range(n)), n, list(range(len(stream))))] if stream else []
+    c = min(low_bits, L)
+    low = frozenset(range(c))
+    remaining = list(range(len(stream)))
+    plans = []
+    while remaining:
+        qset = set(low)
+        blocked = set()
+        taken, deferred = [], []
+        for i in remaining:
+            t = stream[i].targets
+            if blocked.intersection(t):
+                deferred.append(i)
+                blocked.update(t)
+                continue
+            grown = qset.union(t)
+            if len(grown) <= L:
+                qset = grown
+                taken.append(i)
+            else:
+                deferred.append(i)
+                blocked.update(t)
+        if not taken:     # cannot happen for arity <= 2 and L >= c + 2
+            raise ValidationError("fusion planner made no progress")
+        # pad the set with the lowest free qubits: longer contiguous rows, same traffic
+        q = 0
+        while len(qset) < L:
+            if q not in qset:
+                qset.add(q)
+            q += 1
+        qs = tuple(sorted(qset))
+        run = 0
+        while run < len(qs) and qs[run] == run:
+            run += 1
+        plans.append(PassPlan(qs, run, taken))
+        remaining = deferred
+    return plans
+
+
+def compile_circuit(circuit, dtype: str = "c128", tile_bits: int | None = None,
+                    low_bits: int | None = None) -> Program:
+    prog = lower(circuit)
+    L = tile_bits if tile_bits is not None else DEFAULT_TILE_BITS[dtype]
+    c = low_bits if low_bits is not None else DEFAULT_LOW_BITS[dtype]
+    prog.passes = plan_passes(circuit.n_qubits, prog.stream, L, c)
+    return prog
+
+
+def compile_ops(n: int, items, dtype: str = "c128") -> Program:
+    """Program for an explicit list of (matrix, targets, general) ops -- the inner API.
+
+    Each general op becomes a one-outcome general channel site, so the engine
+    reports its realized norm^2 through the weight (statevector.py:129-145).
+    """
+    table = _MatTable()
+    chans, stream, site_chan = [], [], []
+    for matrix, targets, general in items:
+        targets = tuple(int(t) for t in targets)
+        if len(targets) > 2:
+            raise ValidationError(f"{len(targets)}-qubit operators are unsupported on device (1 or 2)")
+        if general:
+            base = table.add(matrix, dedupe=False)
+            chans.append(dict(n_outcomes=1, mat_base=base, general=1, arity=len(targets), identity_mask=0))
+            sid = len(site_chan)
+            site_chan.append(len(chans) - 1)
+            stream.append(StreamOp(KIND_SITE, targets, sid, 0))
+        else:
+            stream.append(StreamOp(KIND_GATE, targets, table.add(matrix), 0))
+    mats = np.array(table.rows, dtype=np.complex128).reshape(-1, 4, 4)
+    prog = Program(n, stream, mats, chans, {}, np.array(site_chan, dtype=np.int32), g_ref=len(stream))
+    prog.passes = plan_passes(n, stream, DEFAULT_TILE_BITS[dtype], DEFAULT_LOW_BITS[dtype])
+    return prog
+
+
+def selection_matrix(program: Program, specs) -> np.ndarray:
+    """(B, S) uint8 outcome table: sel[b, site] = k for spec b's (site, k) pairs, else 0."""
+    sel = np.zeros((len(specs), max(program.n_sites, 0)), dtype=np.uint8)
+    for b, spec in enumerate(specs):
+        for sid, k in spec.selections:
+            sel[b, sid] = k
+    return sel

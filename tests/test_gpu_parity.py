@@ -1,0 +1,250 @@
+"""CUDA engine vs the reference (golden vectors) and the CPU oracle.
+
+Tolerances (north_star): amplitudes ||psi_dev - psi_ref|| / ||psi_ref|| <= 1e-12
+(complex128) / 1e-5 (complex64); realized weights relative 1e-12 / 1e-5;
+shots in verification mode (device PCG64 replaying the reference's stream)
+exactly equal; Philox-mode histograms pass chi-square at p > 0.01.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2504_16297_b200 as P
+from paper_2504_16297_b200 import _native as N
+from paper_2504_16297_b200.engine import Engine, pcg64_state_words
+from paper_2504_16297_b200.execute import mix_seed
+from paper_2504_16297_b200.program import compile_circuit, selection_matrix
+from conftest import build_case
+from paper_2504_16297_b200 import workloads
+from oracle import engine as O
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["rychain_mixture", "rychain_damped", "teleport_damped", "ghz4_depol", "distill5_custom",
+         "config1", "config2", "brick8", "steane1"]
+TOL = {"c128": 1e-12, "c64": 1e-5}
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.mark.parametrize("dtype", ["c128", "c64"])
+@pytest.mark.parametrize("name", CASES)
+def test_prepared_amplitudes_and_weights(golden, golden_arrays, name, dtype):
+    case = golden["cases"][name]
+    c = build_case(case)
+    preps = case["prepared"]
+    specs = [P.TrajectorySpec(tuple(tuple(p) for p in d["selections"]), 0) for d in preps]
+    with Engine(c.n_qubits, dtype, batch_cap=len(specs)) as eng:
+        prog = eng.load(c)
+        w, st = eng.run(selection_matrix(prog, specs))
+        for b, d in enumerate(preps):
+            if "annihilated" in d:
+                assert st[b] == N.TRAJ_ANNIHILATED
+                continue
+            assert st[b] == N.TRAJ_OK
+            assert w[b] == pytest.approx(d["weight"], rel=TOL[dtype], abs=0)
+            psi = eng.get_state(b)
+            assert rel(psi.astype(np.complex128), golden_arrays[d["amps"]]) <= TOL[dtype]
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_shots_bit_exact_pcg64(golden, golden_arrays, name):
+    """Verification mode: device replays stream_rng(9, i) -> counts identical to the reference."""
+    case = golden["cases"][name]
+    c = build_case(case)
+    preps = [d for d in case["prepared"] if "annihilated" not in d]
+    with Engine(c.n_qubits, "c128", batch_cap=len(preps)) as eng:
+        for b, d in enumerate(preps):
+            eng.set_state(b, golden_arrays[d["amps"]])
+        words = np.concatenate([pcg64_state_words(mix_seed(*d["sample_seed"])) for d in preps])
+        out = eng.sample(np.array([d["sample_m"] for d in preps]), N.RNG_PCG64, rng_state=words)
+        for b, d in enumerate(preps):
+            assert out.counts_dict(b, c.n_qubits) == d["counts"]
+
+
+@pytest.mark.parametrize("name", ["rychain_mixture", "rychain_damped", "teleport_damped", "config1", "steane1"])
+def test_execute_all_records_identical(golden, name, tmp_path):
+    """The drop-in boundary: execute_all's records and manifest equal the reference's."""
+    case = golden["cases"][name]
+    c = build_case(case)
+    core = case["dataset"]["manifest_core"]
+    specs = [P.TrajectorySpec(tuple(tuple(p) for p in t["selections"]), t["shots"], t["joint_prob"], t["tags"])
+             for t in core["trajectories"]]
+    ds = P.execute_all(c, specs, parallelism=3, master_seed=case["dataset"]["master_seed"])
+    ds.validate()
+    assert [[r.trajectory_id, r.bitstring, r.count] for r in ds.records] == case["dataset"]["records"]
+    got = P.manifest_core(ds.manifest)
+    for row_g, row_r in zip(got["trajectories"], core["trajectories"]):
+        wg, wr = row_g.pop("realized_weight"), row_r.pop("realized_weight")
+        assert wg == pytest.approx(wr, rel=1e-12, abs=0)
+    assert got == core
+
+
+def test_philox_histograms_chi_square(golden, golden_arrays):
+    from scipy import stats
+    case = golden["cases"]["config1"]
+    c = build_case(case)
+    preps = [d for d in case["prepared"] if "annihilated" not in d][:4]
+    m = 200_000
+    with Engine(c.n_qubits, "c64", batch_cap=len(preps)) as eng:
+        for b, d in enumerate(preps):
+            eng.set_state(b, golden_arrays[d["amps"]])
+        seeds = np.array([mix_seed(5, b) for b in range(len(preps))], dtype=np.uint64)
+        out = eng.sample(np.full(len(preps), m), N.RNG_PHILOX, rng_state=seeds)
+        for b, d in enumerate(preps):
+            probs = np.abs(golden_arrays[d["amps"]]) ** 2
+            lo, hi = out.offsets[b], out.offsets[b + 1]
+            obs = np.zeros(probs.size)
+            obs[out.indices[lo:hi].astype(np.int64)] = out.counts[lo:hi]
+            assert obs.sum() == m
+            assert np.all(probs[obs > 0] > 0)          # never a zero-probability outcome
+            keep = probs * m >= 5
+            exp = probs[keep] * m
+            o = obs[keep]
+            # fold the rare tail into one bin
+            o = np.append(o, m - o.sum())
+            exp = np.append(exp, m - exp.sum())
+            nz = exp > 0
+            p = stats.chisquare(o[nz], exp[nz] * o[nz].sum() / exp[nz].sum()).pvalue
+            assert p > 0.01
+
+
+def test_bench20_state_and_shots(golden):
+    g = golden["bench20"]
+    c = P.parse_circuit(g["circuit"])
+    with Engine(20, "c128", batch_cap=1) as eng:
+        eng.load(c)
+        w, st = eng.run(np.zeros((1, 0), dtype=np.uint8))
+        psi = eng.get_state(0)
+        probs = np.abs(psi) ** 2
+        assert np.allclose(probs.reshape(-1, 1024).sum(axis=1), g["prob_sum_by_1024"], rtol=1e-11, atol=1e-15)
+        head = np.array([complex(a, b) for a, b in g["amps_head"]])
+        assert np.allclose(psi[:64], head, rtol=1e-11, atol=1e-14)
+        out = eng.sample([1000], N.RNG_PCG64, rng_state=pcg64_state_words(mix_seed(0, 0)))
+        assert out.counts_dict(0, 20) == g["counts_m1000_seed00"]
+
+
+def test_uneven_shots_zero_shots_and_annihilation():
+    c = P.attach_noise(P.parse_circuit("qubits 3\ngate h 0\ngate cx 0 1\ngate x 2\n"),
+                       P.parse_noise_model("rule gate=x qubit=* channel=amplitude_damping(0.5)\n"
+                                           "rule gate=* qubit=* channel=depolarizing(0.2)\n"))
+    specs = [P.TrajectorySpec((), 0), P.TrajectorySpec(((3, 1),), 7), P.TrajectorySpec(((0, 2),), 1),
+             P.TrajectorySpec((), 50_000)]
+    ds = P.execute_all(c, specs, master_seed=4)
+    ds.validate()
+    rows = ds.manifest["trajectories"]
+    assert [r["emitted"] for r in rows] == [0, 7, 1, 50_000]
+    # K1 of damping on |1> is allowed; on |0> (qubit 2 flipped by x -> |1>) check the annihilating case
+    c2 = P.attach_noise(P.parse_circuit("qubits 1\ngate i 0\n"),
+                        P.parse_noise_model("rule gate=i qubit=* channel=amplitude_damping(0.5)\n"))
+    ds2 = P.execute_all(c2, [P.TrajectorySpec((), 50), P.TrajectorySpec(((0, 1),), 50)], master_seed=0)
+    ds2.validate()
+    r = ds2.manifest["trajectories"]
+    assert ds2.manifest["partial"]
+    assert r[0]["status"] == "ok" and r[0]["emitted"] == 50
+    assert r[1]["status"] == "annihilated" and r[1]["emitted"] == 0
+    with pytest.raises(P.AnnihilatedStateError):
+        P.prepare_state(c2, P.TrajectorySpec(((0, 1),), 1))
+
+
+def test_general_channel_weight_known_answer():
+    # ref tests/test_execute.py:59-68: damping(0.36) after h -> weight 0.82
+    c = P.attach_noise(P.parse_circuit("qubits 1\ngate h 0\n"),
+                       P.parse_noise_model("rule gate=h qubit=* channel=amplitude_damping(0.36)\n"))
+    st, w = P.prepare_state(c, P.TrajectorySpec((), 0))
+    assert w == pytest.approx(0.82, rel=1e-12)
+    assert st.probabilities()[1] == pytest.approx(0.5 * 0.64 / 0.82, rel=1e-12)
+
+
+def test_inner_api_matches_reference_semantics():
+    s = P.apply_gate(P.init_zero(2), P.gate_op("x", [0]))
+    s = P.apply_gate(s, P.gate_op("cx", [0, 1]))
+    assert np.allclose(s.probabilities(), [0, 0, 0, 1])
+    damp = P.builtin_channel("amplitude_damping", 0.3)
+    one = P.apply_gate(P.init_zero(1), P.gate_op("x", [0]))
+    out, r = P.apply_kraus_normalized(one, damp.kraus_ops[1], [0])
+    assert r == pytest.approx(0.3, rel=1e-12) and np.allclose(out.amplitudes, [1, 0])
+    assert P.kraus_outcome_probability(P.init_zero(1), damp.kraus_ops[1], [0]) == pytest.approx(0.0)
+    with pytest.raises(P.AnnihilatedStateError):
+        P.apply_kraus_normalized(P.init_zero(1), damp.kraus_ops[1], [0])
+    # stream concatenation (ref tests/test_statevector.py:145-151)
+    st = P.apply_gate(P.init_zero(3), P.gate_op("h", [1]))
+    before = st.amplitudes.copy()
+    split, whole = np.random.default_rng(9), np.random.default_rng(9)
+    merged = P.sample_shots(st, 400, split).merged(P.sample_shots(st, 600, split))
+    assert merged.counts == P.sample_shots(st, 1000, whole).counts
+    assert np.array_equal(st.amplitudes, before)
+    # identical to the oracle's numpy sampler for a random state
+    rng = np.random.default_rng(42)
+    amps = rng.normal(size=256) + 1j * rng.normal(size=256)
+    amps /= np.linalg.norm(amps)
+    dev = P.sample_shots(P.ComplexState(8, amps), 20_000, np.random.default_rng(3)).counts
+    assert dev == O.sample(amps, 20_000, np.random.default_rng(3), 8)
+    with pytest.raises(P.ValidationError, match=">= 1"):
+        P.sample_shots(P.init_zero(1), 0, np.random.default_rng(0))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5])
+def test_tiny_states(n):
+    ops = "".join(f"gate h {q}\n" for q in range(n))
+    c = P.parse_circuit(f"qubits {n}\n{ops}")
+    for dtype in ("c64", "c128"):
+        with Engine(n, dtype, batch_cap=2) as eng:
+            eng.load(c)
+            eng.run(np.zeros((2, 0), dtype=np.uint8))
+            psi = eng.get_state(1)
+            assert np.allclose(psi, np.full(1 << n, 2 ** (-n / 2)), atol=1e-6)
+            out = eng.sample([1000, 3], N.RNG_PHILOX, rng_state=np.array([1, 2], dtype=np.uint64))
+            assert out.counts[: out.offsets[1]].sum() == 1000 and out.counts[out.offsets[1]:].sum() == 3
+    empty = P.parse_circuit(f"qubits {n}\n")
+    st, w = P.prepare_state(empty, P.TrajectorySpec((), 0))
+    assert st.amplitudes[0] == 1 and w == 1.0
+
+
+def test_tile_sizes_agree_at_22_qubits():
+    """Size-independent property: different fusion plans give the same state (c128)."""
+    c = P.parse_circuit(workloads.random_brickwork(22, layers=4, seed=9)[0])
+    states = []
+    for tb in (8, 11, 13):
+        prog = compile_circuit(c, "c128", tile_bits=tb)
+        with Engine(22, "c128", batch_cap=1) as eng:
+            eng.load_program(prog)
+            eng.run(np.zeros((1, 0), dtype=np.uint8))
+            states.append(eng.get_state(0))
+    assert rel(states[0], states[1]) <= 1e-12 and rel(states[2], states[1]) <= 1e-12
+    assert abs(np.linalg.norm(states[1]) - 1) <= 1e-12
+
+
+def test_config3_20q_against_oracle():
+    c = workloads.build(3, P.parse_circuit, P.parse_noise_model, P.attach_noise)
+    specs = P.presample_probabilistic(c, 30, 100, np.random.default_rng(1))[:2]
+    for dtype in ("c128", "c64"):
+        with Engine(20, dtype, batch_cap=2) as eng:
+            prog = eng.load(c)
+            w, st = eng.run(selection_matrix(prog, specs))
+            for b, s in enumerate(specs[:1]):
+                ref, rw = O.prepare(c, s.selections)
+                assert rel(eng.get_state(b).astype(np.complex128), ref) <= TOL[dtype]
+
+
+def test_config4_28q_properties():
+    """Full-size config 4 (28 q, c64): norm, determinism, shot totals, no zero-probability outcomes."""
+    c = workloads.build(4, P.parse_circuit, P.parse_noise_model, P.attach_noise)
+    specs = P.presample_probabilistic(c, 20, 10_000, np.random.default_rng(3))[:2]
+    with Engine(28, "c64", batch_cap=2) as eng:
+        prog = eng.load(c)
+        sel = selection_matrix(prog, specs)
+        w, st = eng.run(sel)
+        assert list(st) == [0, 0] and np.allclose(w, 1.0)
+        words = np.concatenate([pcg64_state_words(mix_seed(1, t)) for t in range(2)])
+        a = eng.sample([10_000, 10_000], N.RNG_PCG64, rng_state=words)
+        eng.run(sel)
+        b = eng.sample([10_000, 10_000], N.RNG_PCG64, rng_state=words)
+        assert np.array_equal(a.indices, b.indices) and np.array_equal(a.counts, b.counts)
+        assert int(a.counts.sum()) == 20_000
+        assert a.indices.max() < (1 << 28)
+        psi = eng.get_state(0)
+        assert abs(float(np.sum(np.abs(psi.astype(np.complex128)) ** 2)) - 1.0) < 1e-4
+        assert np.all(np.abs(psi[a.indices[: a.offsets[1]].astype(np.int64)]) > 0)

@@ -1,0 +1,80 @@
+"""Fusion planner: every plan is a legal reordering of the reference's op loop.
+
+The planned order (pass by pass) is executed with the CPU oracle and compared
+with the reference's sequential order (execute.py:85-97); per pass the targets
+must lie in the pass's qubit set and qubits 0..c-1 must be in it.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2504_16297_b200 as P
+from paper_2504_16297_b200 import workloads as W
+from paper_2504_16297_b200.program import KIND_GATE, compile_circuit, plan_passes, selection_matrix
+from oracle import engine as O
+
+
+def _run_stream(c, prog, order, sel):
+    psi = O.zero_state(c.n_qubits)
+    w = 1.0
+    for i in order:
+        so = prog.stream[i]
+        if so.kind == KIND_GATE:
+            m = prog.mats[so.ref][: 1 << len(so.targets), : 1 << len(so.targets)]
+            psi = O.apply_local(psi, m, so.targets, c.n_qubits)
+            continue
+        ch = prog.chans[int(prog.site_chan[so.ref])]
+        k = int(sel[so.ref])
+        if (ch["identity_mask"] >> k) & 1:
+            continue
+        d = 1 << len(so.targets)
+        m = prog.mats[ch["mat_base"] + k][:d, :d]
+        psi = O.apply_local(psi, m, so.targets, c.n_qubits)
+        if ch["general"]:
+            r = float(np.sum(np.abs(psi) ** 2))
+            psi = psi / np.sqrt(r)
+            w *= r
+    return psi, w
+
+
+@pytest.mark.parametrize("tile_bits,low_bits", [(4, 2), (5, 3), (6, 4)])
+@pytest.mark.parametrize("name", ["brick8", "steane1", "teleport_damped", "distill5_custom"])
+def test_plan_is_legal_reordering(golden, name, tile_bits, low_bits):
+    from conftest import build_case
+    c = build_case(golden["cases"][name])
+    prog = compile_circuit(c, "c128", tile_bits=tile_bits, low_bits=low_bits)
+    order = [i for p in prog.passes for i in p.ops]
+    assert sorted(order) == list(range(len(prog.stream)))
+    for p in prog.passes:
+        assert len(p.qubits) == min(c.n_qubits, tile_bits)
+        assert tuple(range(p.low_bits)) == p.qubits[: p.low_bits]
+        for i in p.ops:
+            assert set(prog.stream[i].targets) <= set(p.qubits)
+    rng = np.random.default_rng(1)
+    specs = P.presample_probabilistic(c, 40, 1, rng)
+    sel = selection_matrix(prog, specs)
+    for b, spec in enumerate(specs[:8]):
+        try:
+            ref_psi, ref_w = O.prepare(c, spec.selections)
+        except O.Annihilated:
+            continue
+        psi, w = _run_stream(c, prog, order, sel[b])
+        assert np.linalg.norm(psi - ref_psi) <= 1e-12
+        assert w == pytest.approx(ref_w, rel=1e-12)
+
+
+def test_plan_counts_for_configs():
+    c = W.build(4, P.parse_circuit, P.parse_noise_model, P.attach_noise)
+    prog = compile_circuit(c, "c64")
+    assert prog.g_ref == len(c.ops) + len(c.sites)
+    assert prog.n_passes < prog.g_ref / 10          # >= 10x fewer HBM passes than the reference
+    small = W.build(1, P.parse_circuit, P.parse_noise_model, P.attach_noise)
+    assert compile_circuit(small, "c128").n_passes == 1   # whole 10 q circuit in one smem pass
+
+
+def test_identity_gates_dropped_and_identity_outcomes_masked():
+    c = P.attach_noise(P.parse_circuit("qubits 2\ngate i 0\ngate h 1\n"),
+                       P.parse_noise_model("rule gate=* qubit=* channel=depolarizing(0.1)\n"))
+    prog = compile_circuit(c, "c128")
+    assert [s.kind for s in prog.stream] == [1, 0, 1]    # 'i' gate removed, both sites kept
+    assert all(ch["identity_mask"] == 1 for ch in prog.chans)
