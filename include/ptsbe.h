@@ -104,7 +104,7 @@ int ptsbe_create(int device, int n_qubits, int dtype, int batch_cap, ptsbe_engin
 int ptsbe_destroy(ptsbe_engine* h);
 
 /* mats: n_mats matrices, each 4x4 complex128 row-major padded (32 doubles,
- * re/im interleaved); a 1-qubit matrix uses the leading 2x2 (entries 0,1,2,3). */
+ * re/im interleaved); a 1-qubit matrix is the leading 2x2 block (entries 0,1,4,5). */
 int ptsbe_load_program(ptsbe_engine* h,
                        const ptsbe_op* ops, int n_ops,
                        const double* mats, int n_mats,

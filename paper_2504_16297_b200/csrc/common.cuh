@@ -10,6 +10,10 @@ template <typename R> struct Cplx;
 template <> struct Cplx<float>  { using V = float2;  using W = float4;  };   // W: one 16-B vector
 template <> struct Cplx<double> { using V = double2; using W = double2; };
 
+template <typename V> __device__ __forceinline__ V make_vec2(double x, double y);
+template <> __device__ __forceinline__ float2 make_vec2<float2>(double x, double y) { return make_float2((float)x, (float)y); }
+template <> __device__ __forceinline__ double2 make_vec2<double2>(double x, double y) { return make_double2(x, y); }
+
 template <typename V>
 __device__ __forceinline__ V cmadd2(V m0, V a, V m1, V b) {
   // m0*a + m1*b

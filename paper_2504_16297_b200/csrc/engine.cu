@@ -23,6 +23,7 @@ struct PassHost {
   int L, c;
   int op_begin, n_ops;
   int slot_begin, n_slots;
+  int phase_begin, n_phases;
 };
 
 struct ptsbe_engine {
@@ -43,6 +44,9 @@ struct ptsbe_engine {
   int n_sites = 0, n_mats = 0;
   std::vector<PassHost> passes;
   DevOp* d_ops = nullptr;
+  DevPhase* d_phases = nullptr;
+  int32_t* d_matkind = nullptr;
+  int n_phases_total = 0;
   void* d_mats = nullptr;
   DevChan* d_chans = nullptr;
   int32_t* d_site_chan = nullptr;
@@ -132,8 +136,8 @@ int copy_out(ptsbe_engine* h, void* dst, const void* src_dev, size_t bytes, uint
   return 0;
 }
 
-size_t pass_smem(int L, int c, size_t amp_bytes) {
-  return ((size_t)1 << L) * amp_bytes + (((size_t)1 << L) >> c) * 8 + 32 * 8;
+size_t pass_smem(const PassHost& P, size_t amp_bytes) {
+  return pass_smem_bytes(P.L, P.c, amp_bytes, P.n_ops, P.n_phases);
 }
 
 template <typename R>
@@ -158,6 +162,9 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero) {
     p.qmask = ph.qmask;
     p.ops = h->d_ops + ph.op_begin;
     p.n_ops = ph.n_ops;
+    p.phases = h->d_phases + ph.phase_begin;
+    p.n_phases = ph.n_phases;
+    p.mat_kind = h->d_matkind;
     p.sel = h->d_sel;
     p.S = h->n_sites;
     p.site_chan = h->d_site_chan;
@@ -170,7 +177,7 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero) {
     p.status = h->d_status;
     p.B = B;
     p.tiles = 1ll << (h->n - ph.L);
-    const size_t smem = pass_smem(ph.L, ph.c, sizeof(typename Cplx<R>::V));
+    const size_t smem = pass_smem(ph, sizeof(typename Cplx<R>::V));
     dim3 grid((unsigned)p.tiles, (unsigned)B);
     if (h->profiling) {
       while ((int)h->ev.size() < h->ev_used + 2) {
@@ -180,7 +187,10 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero) {
       }
       CK(h, cudaEventRecord(h->ev[h->ev_used], h->stream));
     }
-    pass_kernel<R><<<grid, 256, smem, h->stream>>>(p);
+    if (ph.L >= 4)
+      pass_kernel<R><<<grid, std::max(32u, 1u << (ph.L - 4)), smem, h->stream>>>(p);
+    else
+      pass_kernel_small<R><<<grid, 32, 0, h->stream>>>(p);
     CKL(h);
     if (h->profiling) {
       CK(h, cudaEventRecord(h->ev[h->ev_used + 1], h->stream));
@@ -413,6 +423,7 @@ int ptsbe_destroy(ptsbe_engine* h) {
   if (!h) return 0;
   cudaSetDevice(h->dev);
   void* ptrs[] = {h->states, h->d_sel, h->d_weight, h->d_nst, h->d_status, h->d_fail, h->d_ops, h->d_mats,
+                  h->d_phases, h->d_matkind,
                   h->d_chans, h->d_site_chan, h->d_slot_site, h->d_partials, h->d_bs, h->d_total, h->d_off,
                   h->d_m, h->d_nuniq, h->d_uoff, h->d_rng, h->d_keys, h->d_tmp, h->d_idx, h->d_runidx,
                   h->d_runcnt, h->d_chunks};
@@ -422,6 +433,91 @@ int ptsbe_destroy(ptsbe_engine* h) {
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
   return 0;
+}
+
+// Classify a padded 4x4 operator for the specialised register kernels.
+static int32_t classify_matrix(const double* m32, int arity) {
+  auto re = [&](int r, int c) { return m32[2 * (4 * r + c)]; };
+  auto im = [&](int r, int c) { return m32[2 * (4 * r + c) + 1]; };
+  auto zero = [&](int r, int c) { return re(r, c) == 0.0 && im(r, c) == 0.0; };
+  auto one = [&](int r, int c) { return re(r, c) == 1.0 && im(r, c) == 0.0; };
+  if (arity == 1) {
+    if (zero(0, 0) && zero(1, 1)) return MK_ANTI1;
+    if (zero(0, 1) && zero(1, 0)) return one(0, 0) ? MK_PHASE1 : MK_DIAG1;
+    if (im(0, 0) == 0.0 && im(0, 1) == 0.0 && im(1, 0) == 0.0 && im(1, 1) == 0.0) return MK_REAL1;
+    return MK_GEN1;
+  }
+  static const int cx[4] = {0, 1, 3, 2}, sw[4] = {0, 2, 1, 3};
+  bool is_cx = true, is_sw = true, is_diag = true;
+  for (int r = 0; r < 4; ++r)
+    for (int c = 0; c < 4; ++c) {
+      const bool want_cx = cx[r] == c, want_sw = sw[r] == c;
+      is_cx = is_cx && (want_cx ? one(r, c) : zero(r, c));
+      is_sw = is_sw && (want_sw ? one(r, c) : zero(r, c));
+      if (r != c) is_diag = is_diag && zero(r, c);
+    }
+  if (is_cx) return MK_CX2;
+  if (is_sw) return MK_SWAP2;
+  if (is_diag) return MK_DIAG2;
+  return MK_GEN2;
+}
+
+struct HostOp {
+  DevOp d;
+  uint32_t bits;   // tile-bit mask of the targets
+  bool general;
+};
+
+// Group a pass's ops (stream order) into phases of <= 4 tile bits.  Same greedy
+// rule as the host pass planner: an op that does not fit blocks its bits for
+// the rest of the phase; general-channel sites never overtake each other (their
+// realized weights are ratios of consecutive norms in reference order).
+static void plan_phases(std::vector<HostOp>& ops, int L, std::vector<DevOp>& out_ops,
+                        std::vector<DevPhase>& out_phases) {
+  std::vector<int> remaining(ops.size());
+  for (size_t i = 0; i < ops.size(); ++i) remaining[i] = (int)i;
+  const uint32_t full = L >= 32 ? 0xffffffffu : ((1u << L) - 1u);
+  while (!remaining.empty()) {
+    uint32_t S = 0, blocked = 0;
+    bool gen_blocked = false;
+    std::vector<int> taken, deferred;
+    for (int i : remaining) {
+      const HostOp& o = ops[i];
+      if ((o.bits & blocked) || (o.general && gen_blocked)) {
+        deferred.push_back(i);
+        blocked |= o.bits;
+        gen_blocked = gen_blocked || o.general;
+        continue;
+      }
+      const uint32_t U = S | o.bits;
+      if (__builtin_popcount(U) <= 4) {
+        S = U;
+        taken.push_back(i);
+      } else {
+        deferred.push_back(i);
+        blocked |= o.bits;
+        gen_blocked = gen_blocked || o.general;
+      }
+    }
+    for (int q = 0; q < L && __builtin_popcount(S) < 4; ++q) S |= (1u << q) & full;
+    int pb[4], np_ = 0;
+    for (int q = 0; q < L && np_ < 4; ++q)
+      if ((S >> q) & 1) pb[np_++] = q;
+    DevPhase P;
+    P.pbits = (uint32_t)pb[0] | ((uint32_t)pb[1] << 5) | ((uint32_t)pb[2] << 10) | ((uint32_t)pb[3] << 15);
+    P.op_begin = (int32_t)out_ops.size();
+    P.n_ops = (int32_t)taken.size();
+    P.pad = 0;
+    for (int i : taken) {
+      DevOp d = ops[i].d;
+      auto pos = [&](int bit) { for (int k = 0; k < 4; ++k) if (pb[k] == bit) return k; return -1; };
+      d.k0 = pos(d.b0);
+      d.k1 = d.arity == 2 ? pos(d.b1) : -1;
+      out_ops.push_back(d);
+    }
+    out_phases.push_back(P);
+    remaining.swap(deferred);
+  }
 }
 
 int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const double* mats, int n_mats,
@@ -436,77 +532,111 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
   for (int s = 0; s < n_sites; ++s)
     if (site_chan[s] < 0 || site_chan[s] >= n_chans)
       return fail(h, PTSBE_ERR_VALIDATION, "site %d references channel %d", s, site_chan[s]);
+  std::vector<int> mat_arity(std::max(n_mats, 1), 0);
   for (int k = 0; k < n_chans; ++k) {
     if (chans[k].n_outcomes < 1 || chans[k].n_outcomes > 64 || chans[k].mat_base < 0 ||
         chans[k].mat_base + chans[k].n_outcomes > n_mats)
       return fail(h, PTSBE_ERR_VALIDATION, "channel %d has an invalid matrix range", k);
     if (chans[k].general && chans[k].identity_mask)
       return fail(h, PTSBE_ERR_VALIDATION, "channel %d: identity skipping is for unitary mixtures only", k);
+    if (chans[k].arity != 1 && chans[k].arity != 2)
+      return fail(h, PTSBE_ERR_VALIDATION, "channel %d: arity %d unsupported on device (1 or 2)", k, chans[k].arity);
+    for (int o = 0; o < chans[k].n_outcomes; ++o) mat_arity[chans[k].mat_base + o] = chans[k].arity;
   }
   std::vector<PassHost> ph(n_passes);
-  std::vector<DevOp> dops(n_ops);
-  std::vector<int32_t> slot_site;
+  const uint64_t nmask = (h->n >= 64) ? ~0ull : ((1ull << h->n) - 1);
   for (int p = 0; p < n_passes; ++p) {
     const ptsbe_pass& P = passes[p];
-    const uint64_t nmask = (h->n >= 64) ? ~0ull : ((1ull << h->n) - 1);
     if ((P.qubit_mask & ~nmask) || __builtin_popcountll(P.qubit_mask) != P.tile_bits)
       return fail(h, PTSBE_ERR_VALIDATION, "pass %d: qubit mask does not match tile_bits", p);
-    if (P.tile_bits < 1 || P.tile_bits > 13)
-      return fail(h, PTSBE_ERR_VALIDATION, "pass %d: tile_bits %d outside [1, 13]", p, P.tile_bits);
+    const int max_tile = h->dtype == PTSBE_C64 ? 13 : 12;   // 2^(L-4) threads <= launch bound
+    if (P.tile_bits < 1 || P.tile_bits > max_tile || (P.tile_bits < 4 && P.tile_bits != h->n))
+      return fail(h, PTSBE_ERR_VALIDATION, "pass %d: tile_bits %d outside [4, %d]", p, P.tile_bits, max_tile);
     const int min_low = std::min(h->n, h->dtype == PTSBE_C64 ? 1 : 0);
     if (P.low_bits < min_low || P.low_bits > P.tile_bits ||
         (P.qubit_mask & ((1ull << P.low_bits) - 1)) != ((1ull << P.low_bits) - 1))
       return fail(h, PTSBE_ERR_VALIDATION, "pass %d: low_bits %d not contiguous in the mask", p, P.low_bits);
-    ph[p] = PassHost{P.qubit_mask, P.tile_bits, P.low_bits, 0, 0, 0, 0};
+    ph[p] = PassHost{P.qubit_mask, P.tile_bits, P.low_bits, 0, 0, 0, 0, 0, 0};
   }
+  // validate ops, translate targets to tile bits, bucket by pass
+  std::vector<std::vector<HostOp>> per_pass(n_passes);
   int prev_pass = -1;
   for (int i = 0; i < n_ops; ++i) {
     const ptsbe_op& o = ops[i];
     if (o.pass < 0 || o.pass >= n_passes || o.pass < prev_pass)
       return fail(h, PTSBE_ERR_VALIDATION, "op %d: pass index %d out of order", i, o.pass);
+    prev_pass = o.pass;
     if (o.arity != 1 && o.arity != 2)
       return fail(h, PTSBE_ERR_VALIDATION, "op %d: arity %d unsupported on device (1 or 2)", i, o.arity);
-    PassHost& P = ph[o.pass];
-    if (o.pass != prev_pass) { P.op_begin = i; P.slot_begin = (int)slot_site.size(); }
-    prev_pass = o.pass;
-    P.n_ops++;
+    const PassHost& P = ph[o.pass];
     auto local = [&](int q) -> int {
       if (q < 0 || q >= h->n || !((P.qmask >> q) & 1)) return -1;
       return __builtin_popcountll(P.qmask & ((1ull << q) - 1));
     };
-    DevOp d;
-    d.kind = o.kind;
-    d.arity = o.arity;
-    d.b0 = local(o.t0);
-    d.b1 = o.arity == 2 ? local(o.t1) : -1;
-    d.ref = o.ref;
-    d.slot = -1;
-    if (d.b0 < 0 || (o.arity == 2 && (d.b1 < 0 || o.t0 == o.t1)))
+    HostOp ho;
+    ho.d.kind = o.kind;
+    ho.d.arity = o.arity;
+    ho.d.b0 = local(o.t0);
+    ho.d.b1 = o.arity == 2 ? local(o.t1) : -1;
+    ho.d.ref = o.ref;
+    ho.d.slot = -1;
+    ho.d.k0 = ho.d.k1 = -1;
+    ho.general = false;
+    if (ho.d.b0 < 0 || (o.arity == 2 && (ho.d.b1 < 0 || o.t0 == o.t1)))
       return fail(h, PTSBE_ERR_VALIDATION, "op %d: targets not inside its pass's qubit set", i);
+    ho.bits = (1u << ho.d.b0) | (o.arity == 2 ? (1u << ho.d.b1) : 0u);
     if (o.kind == 0) {
       if (o.ref < 0 || o.ref >= n_mats) return fail(h, PTSBE_ERR_VALIDATION, "op %d: matrix %d", i, o.ref);
+      if (mat_arity[o.ref] && mat_arity[o.ref] != o.arity)
+        return fail(h, PTSBE_ERR_VALIDATION, "op %d: matrix %d used with two arities", i, o.ref);
+      mat_arity[o.ref] = o.arity;
     } else if (o.kind == 1) {
       if (o.ref < 0 || o.ref >= n_sites) return fail(h, PTSBE_ERR_VALIDATION, "op %d: site %d", i, o.ref);
       const ptsbe_channel& ch = chans[site_chan[o.ref]];
       if (ch.arity != o.arity) return fail(h, PTSBE_ERR_VALIDATION, "op %d: channel arity mismatch", i);
-      if (ch.general) {
-        d.slot = P.n_slots++;
-        slot_site.push_back(o.ref);
-      }
+      ho.general = ch.general != 0;
     } else {
       return fail(h, PTSBE_ERR_VALIDATION, "op %d: unknown kind %d", i, o.kind);
     }
-    dops[i] = d;
+    per_pass[o.pass].push_back(ho);
   }
-  int max_slots = 0;
-  for (auto& P : ph) max_slots = std::max(max_slots, P.n_slots);
+  // phases + norm slots (slot order = reference order of general sites)
+  std::vector<DevOp> dops;
+  std::vector<DevPhase> dph;
+  std::vector<int32_t> slot_site;
   for (int p = 0; p < n_passes; ++p) {
-    const size_t smem = pass_smem(ph[p].L, ph[p].c, h->amp_bytes);
+    PassHost& P = ph[p];
+    for (HostOp& o : per_pass[p])
+      if (o.general) { o.d.slot = P.n_slots++; slot_site.push_back(o.d.ref); }
+    P.slot_begin = (int)slot_site.size() - P.n_slots;
+    P.op_begin = (int)dops.size();
+    P.phase_begin = (int)dph.size();
+    if (P.L >= 4) {
+      std::vector<DevOp> pops;
+      std::vector<DevPhase> pphs;
+      plan_phases(per_pass[p], P.L, pops, pphs);
+      dops.insert(dops.end(), pops.begin(), pops.end());
+      dph.insert(dph.end(), pphs.begin(), pphs.end());
+      P.n_phases = (int)pphs.size();
+    } else {
+      for (HostOp& o : per_pass[p]) dops.push_back(o.d);
+      P.n_phases = 0;
+    }
+    P.n_ops = (int)dops.size() - P.op_begin;
+  }
+  for (int p = 0; p < n_passes; ++p) {
+    const size_t smem = pass_smem(ph[p], h->amp_bytes);
     if (smem > 227 * 1024) return fail(h, PTSBE_ERR_VALIDATION, "pass %d needs %zu B shared memory", p, smem);
   }
+  std::vector<int32_t> kinds(std::max(n_mats, 1), MK_GEN1);
+  for (int m = 0; m < n_mats; ++m) kinds[m] = classify_matrix(mats + (size_t)m * 32, mat_arity[m] ? mat_arity[m] : 2);
   // device tables
-  if (dalloc(h, &h->d_ops, std::max(n_ops, 1))) return PTSBE_ERR_CUDA;
-  if (n_ops) CK(h, cudaMemcpy(h->d_ops, dops.data(), n_ops * sizeof(DevOp), cudaMemcpyHostToDevice));
+  if (dalloc(h, &h->d_ops, std::max<size_t>(dops.size(), 1))) return PTSBE_ERR_CUDA;
+  if (!dops.empty()) CK(h, cudaMemcpy(h->d_ops, dops.data(), dops.size() * sizeof(DevOp), cudaMemcpyHostToDevice));
+  if (dalloc(h, &h->d_phases, std::max<size_t>(dph.size(), 1))) return PTSBE_ERR_CUDA;
+  if (!dph.empty()) CK(h, cudaMemcpy(h->d_phases, dph.data(), dph.size() * sizeof(DevPhase), cudaMemcpyHostToDevice));
+  if (dalloc(h, &h->d_matkind, kinds.size())) return PTSBE_ERR_CUDA;
+  CK(h, cudaMemcpy(h->d_matkind, kinds.data(), kinds.size() * 4, cudaMemcpyHostToDevice));
   {
     const size_t nm = std::max(n_mats, 1);
     if (h->dtype == PTSBE_C64) {
@@ -543,18 +673,15 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
     if (dalloc(h, &h->d_partials, need)) return PTSBE_ERR_CUDA;
     h->partial_cap = need;
   }
-  for (int p = 0; p < n_passes; ++p) {
-    const size_t smem = pass_smem(ph[p].L, ph[p].c, h->amp_bytes);
-    if (smem > 48 * 1024) {
-      if (h->dtype == PTSBE_C64)
-        CK(h, cudaFuncSetAttribute(pass_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      else
-        CK(h, cudaFuncSetAttribute(pass_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    }
-  }
+  const int max_smem = 227 * 1024;
+  if (h->dtype == PTSBE_C64)
+    CK(h, cudaFuncSetAttribute(pass_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
+  else
+    CK(h, cudaFuncSetAttribute(pass_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
   h->passes = ph;
   h->n_sites = n_sites;
   h->n_mats = n_mats;
+  h->n_phases_total = (int)dph.size();
   h->loaded = true;
   return 0;
 }

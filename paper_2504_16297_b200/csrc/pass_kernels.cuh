@@ -4,31 +4,54 @@
 // costs one full-state numpy pass per gate and per noise site
 // (statevector.py:102-109 / :91-99), by P << (#ops + #sites) HBM passes.
 //
-// One CTA owns one TILE of one trajectory's state: the 2^L amplitudes whose
-// basis indices agree outside the pass's qubit set Q (|Q| = L).  Q always
-// contains qubits 0..c-1, so a tile is 2^(L-c) rows of 2^c contiguous
+// Pass = tile sweep.  One CTA owns one TILE of one trajectory's state: the 2^L
+// amplitudes whose basis indices agree outside the pass's qubit set Q (|Q| = L).
+// Q always contains qubits 0..c-1, so a tile is 2^(L-c) rows of 2^c contiguous
 // amplitudes (>= 128 B), moved with coalesced 16-B streaming loads/stores.
 // Every op of the pass has its targets inside Q, so it acts block-diagonally on
-// tiles: the CTA applies the whole op list in shared memory and writes the tile
-// back once.  Noise sites read the trajectory's outcome from sel[b][site];
-// exact-identity outcomes (U_0 = I of every builtin mixture) are skipped
-// bit-exactly, CTA-uniformly.  Non-unitary Kraus ops (general channels,
-// statevector.py:136-145) are applied unnormalised; the CTA writes its tile's
-// ||.||^2 right after each one (a unitary inside Q preserves every tile's norm),
-// norm_finalize turns the per-tile partials into realized weights, and the
+// tiles; the tile is read from HBM once and written once.
+//
+// Phase = register sweep.  Inside the tile the pass's ops are grouped (by the
+// host, engine.cu) into phases whose targets span at most 4 tile bits.  Each
+// thread owns one 16-amplitude group of a phase in registers and applies every
+// op of the phase there -- with the gate's kind specialised (real, diagonal,
+// phase, anti-diagonal, CX, SWAP, general) and its bit positions compile-time
+// so the register file is indexed statically.  Between phases the tile goes
+// through XOR-swizzled shared memory once.
+//
+// Noise sites read the trajectory's outcome from sel[b][site]; exact-identity
+// outcomes (U_0 = I of every builtin mixture) are skipped bit-exactly and
+// CTA-uniformly.  Non-unitary Kraus ops (general channels, statevector.py:
+// 136-145) are applied unnormalised; right after each one the CTA reduces its
+// tile's ||.||^2 into a per-tile partial (an op inside Q preserves every other
+// tile), norm_finalize turns partials into realized weights, and the
 // 1/sqrt(norm^2) rescale is deferred into the next pass's loads.
 #pragma once
 #include "common.cuh"
 
 namespace ptsbe {
 
+// matrix kinds (engine.cu classifies every matrix of the operator table)
+enum : int32_t {
+  MK_GEN1 = 0, MK_REAL1 = 1, MK_DIAG1 = 2, MK_PHASE1 = 3, MK_ANTI1 = 4,
+  MK_GEN2 = 8, MK_CX2 = 9, MK_SWAP2 = 10, MK_DIAG2 = 11
+};
+
 struct DevOp {
   int32_t kind;    // 0 gate, 1 site
   int32_t arity;   // 1 or 2
-  int32_t b0;      // local (tile) bit of first target (MSB of matrix index)
-  int32_t b1;      // local bit of second target or -1
+  int32_t b0;      // tile bit of first target (MSB of matrix index)
+  int32_t b1;      // tile bit of second target or -1
   int32_t ref;     // gate: matrix index; site: site id
-  int32_t slot;    // site of a general channel: norm slot within the pass, else -1
+  int32_t slot;    // general-channel site: norm slot within the pass, else -1
+  int32_t k0, k1;  // register-bit positions (0..3) of b0/b1 inside the op's phase
+};
+
+struct DevPhase {
+  uint32_t pbits;  // 4 tile bit positions, 5 bits each (ascending)
+  int32_t op_begin;
+  int32_t n_ops;
+  int32_t pad;
 };
 
 struct DevChan {
@@ -45,13 +68,16 @@ struct PassParams {
   int L;                     // tile bits
   int c;                     // contiguous low bits in Q
   uint64_t qmask;            // Q
-  const DevOp* ops;
+  const DevOp* ops;          // this pass's ops, phase-major
   int n_ops;
+  const DevPhase* phases;    // this pass's phases
+  int n_phases;
   const uint8_t* sel;        // [B][S]
   int S;
   const int32_t* site_chan;  // [S]
   const DevChan* chans;
   const void* mats;          // [n_mats][16] V
+  const int32_t* mat_kind;   // [n_mats]
   const double* nst;         // [B] norm^2 of the stored state (used when use_scale)
   int use_scale;
   int gen_zero;              // first pass: synthesize |0...0> instead of loading
@@ -61,8 +87,171 @@ struct PassParams {
   long long tiles;
 };
 
+// ---- shared-memory swizzle: spreads the 32 lanes of a phase access over banks
+template <typename V> __device__ __forceinline__ uint32_t swz(uint32_t i);
+template <> __device__ __forceinline__ uint32_t swz<float2>(uint32_t i) {
+  const uint32_t h = (i >> 4) ^ (i >> 8) ^ ((i >> 8) << 1) ^ (i >> 12);
+  return i ^ (h & 15u);
+}
+template <> __device__ __forceinline__ uint32_t swz<double2>(uint32_t i) {
+  const uint32_t h = (i >> 3) ^ (i >> 6) ^ ((i >> 6) << 1) ^ (i >> 9) ^ (i >> 12);
+  return i ^ (h & 7u);
+}
+
+// ---- register-resident gate kernels on a 16-amplitude group; K* are bit positions
+template <int K, typename V>
+__device__ __forceinline__ void r1_gen(V* a, const V* m) {
+  const V m00 = m[0], m01 = m[1], m10 = m[4], m11 = m[5];
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (!(j & (1 << K))) {
+      const V x = a[j], y = a[j | (1 << K)];
+      a[j] = cmadd2(m00, x, m01, y);
+      a[j | (1 << K)] = cmadd2(m10, x, m11, y);
+    }
+}
+template <int K, typename V>
+__device__ __forceinline__ void r1_real(V* a, const V* m) {
+  const auto m00 = m[0].x, m01 = m[1].x, m10 = m[4].x, m11 = m[5].x;
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (!(j & (1 << K))) {
+      const V x = a[j], y = a[j | (1 << K)];
+      V u, v;
+      u.x = m00 * x.x + m01 * y.x; u.y = m00 * x.y + m01 * y.y;
+      v.x = m10 * x.x + m11 * y.x; v.y = m10 * x.y + m11 * y.y;
+      a[j] = u;
+      a[j | (1 << K)] = v;
+    }
+}
+template <typename V>
+__device__ __forceinline__ V cmul(V d, V x) {
+  V r;
+  r.x = d.x * x.x - d.y * x.y;
+  r.y = d.x * x.y + d.y * x.x;
+  return r;
+}
+template <int K, typename V>
+__device__ __forceinline__ void r1_diag(V* a, const V* m) {
+  const V d0 = m[0], d1 = m[5];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) a[j] = cmul((j & (1 << K)) ? d1 : d0, a[j]);
+}
+template <int K, typename V>
+__device__ __forceinline__ void r1_phase(V* a, const V* m) {   // diag(1, d1)
+  const V d1 = m[5];
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (j & (1 << K)) a[j] = cmul(d1, a[j]);
+}
+template <int K, typename V>
+__device__ __forceinline__ void r1_anti(V* a, const V* m) {    // [[0, m01], [m10, 0]]
+  const V m01 = m[1], m10 = m[4];
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (!(j & (1 << K))) {
+      const V x = a[j], y = a[j | (1 << K)];
+      a[j] = cmul(m01, y);
+      a[j | (1 << K)] = cmul(m10, x);
+    }
+}
+// 2-qubit ops: KH = register bit of the first-listed target (MSB of local index)
+template <int KH, int KL, typename V>
+__device__ __forceinline__ void r2_gen(V* a, const V* m) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (!(j & (1 << KH)) && !(j & (1 << KL))) {
+      const int i1 = j | (1 << KL), i2 = j | (1 << KH), i3 = j | (1 << KH) | (1 << KL);
+      const V v0 = a[j], v1 = a[i1], v2 = a[i2], v3 = a[i3];
+      a[j] = cmadd4(m + 0, v0, v1, v2, v3);
+      a[i1] = cmadd4(m + 4, v0, v1, v2, v3);
+      a[i2] = cmadd4(m + 8, v0, v1, v2, v3);
+      a[i3] = cmadd4(m + 12, v0, v1, v2, v3);
+    }
+}
+template <int KH, int KL, typename V>
+__device__ __forceinline__ void r2_cx(V* a) {    // control = first target (KH), flip KL
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if ((j & (1 << KH)) && !(j & (1 << KL))) {
+      const V t = a[j];
+      a[j] = a[j | (1 << KL)];
+      a[j | (1 << KL)] = t;
+    }
+}
+template <int KH, int KL, typename V>
+__device__ __forceinline__ void r2_swap(V* a) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if ((j & (1 << KH)) && !(j & (1 << KL))) {
+      const int o = (j & ~(1 << KH)) | (1 << KL);
+      const V t = a[j];
+      a[j] = a[o];
+      a[o] = t;
+    }
+}
+template <int KH, int KL, typename V>
+__device__ __forceinline__ void r2_diag(V* a, const V* m) {
+  const V d0 = m[0], d1 = m[5], d2 = m[10], d3 = m[15];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int s = ((j >> KH) & 1) * 2 + ((j >> KL) & 1);
+    a[j] = cmul(s == 0 ? d0 : s == 1 ? d1 : s == 2 ? d2 : d3, a[j]);
+  }
+}
+
+// ---- one switch over (kind, register positions): a single indirect branch per op
+struct CompactOp {
+  int32_t code;    // kind * 16 + k0 * 4 + k1
+  int32_t mat;     // matrix index
+  int32_t slot;    // general-channel norm slot or -1
+  int32_t pad;
+};
+
+template <typename V>
+__device__ __forceinline__ void apply_code(V* a, int code, const V* m) {
+#define C1(KIND, FN, K) case KIND * 16 + K * 4: FN<K>(a, m); break;
+#define C1ALL(KIND, FN) C1(KIND, FN, 0) C1(KIND, FN, 1) C1(KIND, FN, 2) C1(KIND, FN, 3)
+#define C2(KIND, EXPR, H, L) case KIND * 16 + H * 4 + L: EXPR(H, L); break;
+#define C2ALL(KIND, EXPR) C2(KIND, EXPR, 0, 1) C2(KIND, EXPR, 0, 2) C2(KIND, EXPR, 0, 3) C2(KIND, EXPR, 1, 0) \
+  C2(KIND, EXPR, 1, 2) C2(KIND, EXPR, 1, 3) C2(KIND, EXPR, 2, 0) C2(KIND, EXPR, 2, 1) C2(KIND, EXPR, 2, 3)       \
+  C2(KIND, EXPR, 3, 0) C2(KIND, EXPR, 3, 1) C2(KIND, EXPR, 3, 2)
+#define E_GEN(H, L) r2_gen<H, L>(a, m)
+#define E_CX(H, L) r2_cx<H, L>(a)
+#define E_SWAP(H, L) r2_swap<H, L>(a)
+#define E_DIAG(H, L) r2_diag<H, L>(a, m)
+  switch (code) {
+    C1ALL(MK_GEN1, r1_gen)
+    C1ALL(MK_REAL1, r1_real)
+    C1ALL(MK_DIAG1, r1_diag)
+    C1ALL(MK_PHASE1, r1_phase)
+    C1ALL(MK_ANTI1, r1_anti)
+    C2ALL(MK_GEN2, E_GEN)
+    C2ALL(MK_CX2, E_CX)
+    C2ALL(MK_SWAP2, E_SWAP)
+    C2ALL(MK_DIAG2, E_DIAG)
+    default: break;
+  }
+#undef C1
+#undef C1ALL
+#undef C2
+#undef C2ALL
+#undef E_GEN
+#undef E_CX
+#undef E_SWAP
+#undef E_DIAG
+}
+
+// Shared-memory layout of the pass kernel (dynamic):
+//   tile [2^L] V | rowoff [2^(L-c)] u64 | red [32] f64 | cops [n_ops] CompactOp | cph [n_phases] int2
+__host__ __device__ inline size_t pass_smem_bytes(int L, int c, size_t amp_bytes, int n_ops, int n_phases) {
+  return ((size_t)1 << L) * amp_bytes + (((size_t)1 << L) >> c) * 8 + 32 * 8 +
+         (size_t)n_ops * sizeof(CompactOp) + (size_t)n_phases * 8;
+}
+
+// Threads = max(32, 2^(L-4)): each thread owns at most one 16-amplitude group per phase.
 template <typename R>
-__global__ void __launch_bounds__(256) pass_kernel(PassParams p) {
+__global__ void __launch_bounds__(sizeof(R) == 8 ? 256 : 512) pass_kernel(PassParams p) {
   using V = typename Cplx<R>::V;
   using W = typename Cplx<R>::W;
   constexpr int VPW = sizeof(W) / sizeof(V);   // amplitudes per 16-B vector
@@ -75,43 +264,157 @@ __global__ void __launch_bounds__(256) pass_kernel(PassParams p) {
   V* tile = reinterpret_cast<V*>(smem);
   uint64_t* rowoff = reinterpret_cast<uint64_t*>(smem + (size_t)TL * sizeof(V));
   double* red = reinterpret_cast<double*>(rowoff + (TL >> c));
+  CompactOp* cops = reinterpret_cast<CompactOp*>(red + 32);
+  int2* cph = reinterpret_cast<int2*>(cops + p.n_ops);
 
   const uint64_t nmask = (p.n >= 64) ? ~0ull : ((1ull << p.n) - 1ull);
   const uint64_t base = pdep64((uint64_t)blockIdx.x, ~p.qmask & nmask);
   const uint64_t hmask = p.qmask & ~((1ull << c) - 1ull);
   const uint32_t rows = TL >> c;
   for (uint32_t r = threadIdx.x; r < rows; r += blockDim.x) rowoff[r] = pdep64(r, hmask);
+
+  // ---- warp 0: this trajectory's op list, identity outcomes dropped, decoded once
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int out = 0;
+    for (int ph = 0; ph < p.n_phases; ++ph) {
+      const DevPhase P = p.phases[ph];
+      const int start = out;
+      for (int k0 = 0; k0 < P.n_ops; k0 += 32) {
+        const int k = P.op_begin + k0 + lane;
+        bool keep = false;
+        CompactOp co{0, 0, -1, 0};
+        if (k0 + lane < P.n_ops) {
+          const DevOp op = p.ops[k];
+          int mat = op.ref;
+          keep = true;
+          if (op.kind == 1) {
+            const int outcome = p.sel[(size_t)b * p.S + op.ref];
+            const DevChan ch = p.chans[p.site_chan[op.ref]];
+            keep = !((ch.identity_mask >> outcome) & 1ull);
+            mat = ch.mat_base + outcome;
+            if (ch.general) co.slot = op.slot;
+          }
+          co.mat = mat;
+          co.code = p.mat_kind[mat] * 16 + op.k0 * 4 + (op.arity == 2 ? op.k1 : 0);
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        if (keep) cops[out + __popc(bal & ((1u << lane) - 1u))] = co;
+        out += __popc(bal);
+      }
+      if (lane == 0) cph[ph] = make_int2(start, out - start);
+    }
+  }
   __syncthreads();
 
   V* st = reinterpret_cast<V*>(p.states) + ((size_t)b << p.n);
   const int cpr_log = c - (VPW == 2 ? 1 : 0);   // 16-B vectors per row, log2
   const uint32_t nvec = TL / VPW;
 
-  // ---- load (or synthesize) the tile
+  // ---- HBM -> shared (coalesced rows), or synthesize |0..0>
   if (p.gen_zero) {
     for (uint32_t i = threadIdx.x; i < TL; i += blockDim.x) {
       V z; z.x = (base == 0 && i == 0) ? R(1) : R(0); z.y = R(0);
-      tile[i] = z;
+      tile[swz<V>(i)] = z;
     }
   } else {
     const R scale = p.use_scale ? (R)rsqrt(p.nst[b]) : R(1);
+#pragma unroll 4
     for (uint32_t u = threadIdx.x; u < nvec; u += blockDim.x) {
       const uint32_t r = u >> cpr_log;
       const uint32_t j = u & ((1u << cpr_log) - 1u);
       const uint64_t g = base + rowoff[r] + (uint64_t)j * VPW;
-      W w = ld_stream(reinterpret_cast<const W*>(st + g));
-      V* dst = tile + ((r << c) | (j * VPW));
+      const W w = ld_stream(reinterpret_cast<const W*>(st + g));
+      const uint32_t li = (r << c) | (j * VPW);
       if constexpr (VPW == 2) {
-        dst[0] = make_float2(w.x * scale, w.y * scale);
-        dst[1] = make_float2(w.z * scale, w.w * scale);
+        const uint32_t s0 = swz<V>(li);
+        tile[s0] = make_float2(w.x * scale, w.y * scale);
+        tile[s0 ^ swz<V>(1u)] = make_float2(w.z * scale, w.w * scale);   // swz is GF(2)-linear
       } else {
-        dst[0] = make_double2(w.x * scale, w.y * scale);
+        tile[swz<V>(li)] = make_double2(w.x * scale, w.y * scale);
       }
     }
   }
   __syncthreads();
 
-  // ---- apply the pass's op list in shared memory
+  // ---- phases: shared -> registers, apply, registers -> shared
+  const V* mats = reinterpret_cast<const V*>(p.mats);
+  const uint32_t g = threadIdx.x;               // this thread's group
+  const bool active = g < (TL >> 4);            // blockDim may exceed 2^(L-4) for L < 8
+  for (int ph = 0; ph < p.n_phases; ++ph) {
+    const DevPhase P = p.phases[ph];
+    const int p0 = P.pbits & 31, p1 = (P.pbits >> 5) & 31, p2 = (P.pbits >> 10) & 31, p3 = (P.pbits >> 15) & 31;
+    const uint32_t gb = insert0(insert0(insert0(insert0(g, p0), p1), p2), p3);
+    // swz is linear over GF(2) and gb / offsets have disjoint bits: addr_j = swz(gb) ^ swz(off_j)
+    const uint32_t sg = swz<V>(gb);
+    uint32_t so[16];
+    so[0] = 0;
+    so[1] = swz<V>(1u << p0);
+    so[2] = swz<V>(1u << p1);
+    so[4] = swz<V>(1u << p2);
+    so[8] = swz<V>(1u << p3);
+#pragma unroll
+    for (int j = 3; j < 16; ++j)
+      if (j & (j - 1)) so[j] = so[j & (j - 1)] ^ so[j & -j];
+    V a[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) a[j] = active ? tile[sg ^ so[j]] : make_vec2<V>(0, 0);
+    const int2 range = cph[ph];
+    for (int k = range.x; k < range.x + range.y; ++k) {
+      const CompactOp co = cops[k];
+      apply_code(a, co.code, mats + (size_t)co.mat * 16);
+      if (co.slot >= 0) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) s += prob64(a[j]);
+        s = block_sum_f64(s, red);
+        if (threadIdx.x == 0) p.partials[((size_t)co.slot * p.B + b) * p.tiles + blockIdx.x] = s;
+      }
+    }
+    if (active) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) tile[sg ^ so[j]] = a[j];
+    }
+    __syncthreads();
+  }
+
+  // ---- shared -> HBM
+#pragma unroll 4
+  for (uint32_t u = threadIdx.x; u < nvec; u += blockDim.x) {
+    const uint32_t r = u >> cpr_log;
+    const uint32_t j = u & ((1u << cpr_log) - 1u);
+    const uint64_t gi = base + rowoff[r] + (uint64_t)j * VPW;
+    const uint32_t li = (r << c) | (j * VPW);
+    W w;
+    if constexpr (VPW == 2) {
+      const uint32_t s0 = swz<V>(li);
+      const V x = tile[s0], y = tile[s0 ^ swz<V>(1u)];
+      w = make_float4(x.x, x.y, y.x, y.y);
+    } else {
+      w = tile[swz<V>(li)];
+    }
+    st_stream(reinterpret_cast<W*>(st + gi), w);
+  }
+}
+
+// Tiny states (L < 4): one op at a time in shared memory.
+template <typename R>
+__global__ void __launch_bounds__(32) pass_kernel_small(PassParams p) {
+  using V = typename Cplx<R>::V;
+  __shared__ V tile[16];
+  __shared__ double red[32];
+  const int b = blockIdx.y;
+  if (p.status[b] != 0) return;
+  const uint32_t TL = 1u << p.L;                 // == 2^n, one tile
+  V* st = reinterpret_cast<V*>(p.states) + ((size_t)b << p.n);
+  const R scale = (!p.gen_zero && p.use_scale) ? (R)rsqrt(p.nst[b]) : R(1);
+  for (uint32_t i = threadIdx.x; i < TL; i += blockDim.x) {
+    V v;
+    if (p.gen_zero) { v.x = i == 0 ? R(1) : R(0); v.y = R(0); }
+    else { v = st[i]; v.x *= scale; v.y *= scale; }
+    tile[i] = v;
+  }
+  __syncthreads();
   const V* mats = reinterpret_cast<const V*>(p.mats);
   for (int k = 0; k < p.n_ops; ++k) {
     const DevOp op = p.ops[k];
@@ -120,61 +423,36 @@ __global__ void __launch_bounds__(256) pass_kernel(PassParams p) {
     if (op.kind == 1) {
       const int outcome = p.sel[(size_t)b * p.S + op.ref];
       const DevChan ch = p.chans[p.site_chan[op.ref]];
-      if ((ch.identity_mask >> outcome) & 1ull) continue;   // CTA-uniform skip
+      if ((ch.identity_mask >> outcome) & 1ull) continue;
       mat = ch.mat_base + outcome;
       general = ch.general != 0;
     }
     const V* m = mats + (size_t)mat * 16;
-    if (op.arity == 1) {
-      const V m00 = m[0], m01 = m[1], m10 = m[2], m11 = m[3];
-      const int bit = op.b0;
-      const uint32_t step = 1u << bit;
-      for (uint32_t q = threadIdx.x; q < (TL >> 1); q += blockDim.x) {
-        const uint32_t i0 = insert0(q, bit), i1 = i0 | step;
-        const V a0 = tile[i0], a1 = tile[i1];
-        tile[i0] = cmadd2(m00, a0, m01, a1);
-        tile[i1] = cmadd2(m10, a0, m11, a1);
-      }
-    } else {
-      V mm[16];
-#pragma unroll
-      for (int e = 0; e < 16; ++e) mm[e] = m[e];
-      const int hb = op.b0, lb = op.b1;   // hb: MSB of local index
-      const int lo = min(hb, lb), hi = max(hb, lb);
-      const uint32_t sh = 1u << hb, sl = 1u << lb;
-      for (uint32_t q = threadIdx.x; q < (TL >> 2); q += blockDim.x) {
-        const uint32_t i0 = insert0(insert0(q, lo), hi);
-        const V v0 = tile[i0], v1 = tile[i0 | sl], v2 = tile[i0 | sh], v3 = tile[i0 | sh | sl];
-        tile[i0]           = cmadd4(mm + 0,  v0, v1, v2, v3);
-        tile[i0 | sl]      = cmadd4(mm + 4,  v0, v1, v2, v3);
-        tile[i0 | sh]      = cmadd4(mm + 8,  v0, v1, v2, v3);
-        tile[i0 | sh | sl] = cmadd4(mm + 12, v0, v1, v2, v3);
+    V out = make_vec2<V>(0, 0);
+    const uint32_t i = threadIdx.x;
+    if (i < TL) {
+      if (op.arity == 1) {
+        const int bit = (i >> op.b0) & 1;
+        const V x0 = tile[i & ~(1u << op.b0)], x1 = tile[i | (1u << op.b0)];
+        out = cmadd2(m[bit * 4 + 0], x0, m[bit * 4 + 1], x1);
+      } else {
+        const int r = ((i >> op.b0) & 1) * 2 + ((i >> op.b1) & 1);
+        const uint32_t z = i & ~(1u << op.b0) & ~(1u << op.b1);
+        const V v0 = tile[z], v1 = tile[z | (1u << op.b1)], v2 = tile[z | (1u << op.b0)],
+                v3 = tile[z | (1u << op.b0) | (1u << op.b1)];
+        out = cmadd4(m + 4 * r, v0, v1, v2, v3);
       }
     }
     __syncthreads();
+    if (i < TL) tile[i] = out;
+    __syncthreads();
     if (general) {
-      double s = 0.0;
-      for (uint32_t i = threadIdx.x; i < TL; i += blockDim.x) s += prob64(tile[i]);
+      double s = (i < TL) ? prob64(tile[i]) : 0.0;
       s = block_sum_f64(s, red);
-      if (threadIdx.x == 0)
-        p.partials[((size_t)op.slot * p.B + b) * p.tiles + blockIdx.x] = s;
+      if (threadIdx.x == 0) p.partials[((size_t)op.slot * p.B + b) * p.tiles + blockIdx.x] = s;
     }
   }
-
-  // ---- store
-  for (uint32_t u = threadIdx.x; u < nvec; u += blockDim.x) {
-    const uint32_t r = u >> cpr_log;
-    const uint32_t j = u & ((1u << cpr_log) - 1u);
-    const uint64_t g = base + rowoff[r] + (uint64_t)j * VPW;
-    const V* src = tile + ((r << c) | (j * VPW));
-    W w;
-    if constexpr (VPW == 2) {
-      w = make_float4(src[0].x, src[0].y, src[1].x, src[1].y);
-    } else {
-      w = src[0];
-    }
-    st_stream(reinterpret_cast<W*>(st + g), w);
-  }
+  for (uint32_t i = threadIdx.x; i < TL; i += blockDim.x) st[i] = tile[i];
 }
 
 // Per trajectory: fold the pass's per-tile partial norms (fixed order ->
@@ -201,11 +479,11 @@ __global__ void __launch_bounds__(256) norm_finalize(const double* partials, int
     const double nj = red[0];
     __syncthreads();
     const double realized = nj / prev;
-    if (realized <= 1e-14) {
+    if (!(realized > 1e-14)) {        // also catches 0/0
       if (threadIdx.x == 0) {
         status[b] = 2;
         fail_site[b] = slot_site[j];
-        weight[b] = realized;     // host reports the offending norm^2
+        weight[b] = realized == realized ? realized : 0.0;   // host reports the offending norm^2
       }
       return;
     }
@@ -236,7 +514,7 @@ __global__ void batch_reset(double* weight, double* nst, int32_t* status, int32_
   if (b < B) { weight[b] = 1.0; nst[b] = 1.0; status[b] = 0; fail_site[b] = -1; }
 }
 
-// Multiply state b by s[b] (used to normalise before download / after set).
+// Multiply state b by 1/sqrt(nst[b]) (normalise before download).
 template <typename R>
 __global__ void scale_states(void* states, int n, int B, const double* nst, int invert_sqrt) {
   using V = typename Cplx<R>::V;

@@ -20,6 +20,9 @@ and per site.  This module lowers the same sequence once per circuit:
 Planner: greedy in stream order.  Ops whose targets fit in the growing set
 join; an op that does not fit blocks its qubits for the rest of the pass
 (later ops on them depend on it), ops on untouched qubits keep flowing.
+Sites of general (renormalising) channels never overtake one another: their
+realized weights are ratios of consecutive norms in the reference's order
+(statevector.py:136-145), so that order is part of the semantics.
 """
 
 from __future__ import annotations
@@ -43,6 +46,7 @@ class StreamOp:
     targets: tuple
     ref: int              # gate: matrix index; site: site id
     pos: int              # op position in circuit.ops
+    general: bool = False # site of a non-unitary channel (renormalising)
 
 
 @dataclass
@@ -131,7 +135,8 @@ def lower(circuit) -> Program:
         if not _is_identity(op.matrix):
             stream.append(StreamOp(KIND_GATE, tuple(op.targets), table.add(op.matrix), pos))
         for s in by_pos.get(pos, ()):
-            stream.append(StreamOp(KIND_SITE, tuple(s.targets), s.site_id, pos))
+            general = bool(chans[chan_index[s.channel_id]]["general"])
+            stream.append(StreamOp(KIND_SITE, tuple(s.targets), s.site_id, pos, general))
     mats = np.array(table.rows, dtype=np.complex128).reshape(-1, 4, 4)
     return Program(circuit.n_qubits, stream, mats, chans, chan_index, site_chan,
                    g_ref=len(circuit.ops) + len(circuit.sites))
@@ -149,12 +154,15 @@ def plan_passes(n: int, stream: list, tile_bits: int, low_bits: int) -> list:
     while remaining:
         qset = set(low)
         blocked = set()
+        gen_blocked = False
         taken, deferred = [], []
         for i in remaining:
-            t = stream[i].targets
-            if blocked.intersection(t):
+            so = stream[i]
+            t = so.targets
+            if blocked.intersection(t) or (so.general and gen_blocked):
                 deferred.append(i)
                 blocked.update(t)
+                gen_blocked = gen_blocked or so.general
                 continue
             grown = qset.union(t)
             if len(grown) <= L:
@@ -163,6 +171,7 @@ def plan_passes(n: int, stream: list, tile_bits: int, low_bits: int) -> list:
             else:
                 deferred.append(i)
                 blocked.update(t)
+                gen_blocked = gen_blocked or so.general
         if not taken:     # cannot happen for arity <= 2 and L >= c + 2
             raise ValidationError("fusion planner made no progress")
         # pad the set with the lowest free qubits: longer contiguous rows, same traffic
@@ -206,7 +215,7 @@ def compile_ops(n: int, items, dtype: str = "c128") -> Program:
             chans.append(dict(n_outcomes=1, mat_base=base, general=1, arity=len(targets), identity_mask=0))
             sid = len(site_chan)
             site_chan.append(len(chans) - 1)
-            stream.append(StreamOp(KIND_SITE, targets, sid, 0))
+            stream.append(StreamOp(KIND_SITE, targets, sid, 0, True))
         else:
             stream.append(StreamOp(KIND_GATE, targets, table.add(matrix), 0))
     mats = np.array(table.rows, dtype=np.complex128).reshape(-1, 4, 4)

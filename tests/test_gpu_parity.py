@@ -207,7 +207,7 @@ def test_tile_sizes_agree_at_22_qubits():
     """Size-independent property: different fusion plans give the same state (c128)."""
     c = P.parse_circuit(workloads.random_brickwork(22, layers=4, seed=9)[0])
     states = []
-    for tb in (8, 11, 13):
+    for tb in (8, 10, 12):
         prog = compile_circuit(c, "c128", tile_bits=tb)
         with Engine(22, "c128", batch_cap=1) as eng:
             eng.load_program(prog)
