@@ -34,7 +34,17 @@ def up_to_date() -> bool:
     return all(p.stat().st_mtime <= t for p in DEPS if p.exists())
 
 
+def write_prelude_inc() -> None:
+    """Embed gen_prelude.cuh as a C++ raw string for NVRTC (codegen.h)."""
+    text = (CSRC / "gen_prelude.cuh").read_text()
+    inc = CSRC / "gen_prelude.inc"
+    body = 'static const char* kGenPrelude = R"PTSBE_PRELUDE(' + text + ')PTSBE_PRELUDE";\n'
+    if not inc.exists() or inc.read_text() != body:
+        inc.write_text(body)
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
+    write_prelude_inc()
     if not force and up_to_date():
         return OUT
     cmd = [nvcc(), *NVCC_FLAGS, "-o", str(OUT), *map(str, SOURCES)]

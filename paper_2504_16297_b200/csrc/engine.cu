@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -15,6 +16,7 @@
 #include "../../include/ptsbe.h"
 #include "pass_kernels.cuh"
 #include "sample_kernels.cuh"
+#include "codegen.h"
 
 using namespace ptsbe;
 
@@ -27,7 +29,7 @@ struct PassHost {
 };
 
 struct ptsbe_engine {
-  int dev = 0, n = 0, dtype = 0, cap = 0;
+  int dev = 0, n = 0, dtype = 0, cap = 0, num_sms = 148;
   size_t amp_bytes = 8;
   cudaStream_t stream = nullptr;
   void* states = nullptr;
@@ -47,6 +49,10 @@ struct ptsbe_engine {
   DevPhase* d_phases = nullptr;
   int32_t* d_matkind = nullptr;
   int n_phases_total = 0;
+  // circuit-specialised kernels (codegen.h); generic pass_kernel when off
+  bool gen_active = false;
+  std::string gen_note;
+  gen::Module gen_mod;
   void* d_mats = nullptr;
   DevChan* d_chans = nullptr;
   int32_t* d_site_chan = nullptr;
@@ -187,10 +193,31 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero) {
       }
       CK(h, cudaEventRecord(h->ev[h->ev_used], h->stream));
     }
-    if (ph.L >= 4)
-      pass_kernel<R><<<grid, std::max(32u, 1u << (ph.L - 4)), smem, h->stream>>>(p);
-    else
+    if (h->gen_active) {
+      const unsigned threads = std::max(32u, 1u << (ph.L - 4));
+      const size_t gsm = gen::smem_bytes(ph.L, ph.c, sizeof(typename Cplx<R>::V));
+      CUfunction f = h->gen_mod.fns[pi];
+      int per_sm = 0;
+      if (gen::api().occupancy(&per_sm, f, (int)threads, gsm) != CUDA_SUCCESS) per_sm = 1;
+      const long long total = (long long)B * p.tiles;
+      const long long want = (long long)std::max(per_sm, 1) * h->num_sms;
+      const unsigned nblk = (unsigned)std::max<long long>(1, std::min(total, want));
+      void* args[] = {&p};
+      if (gen::api().launch(f, nblk, 1, 1, threads, 1, 1, (unsigned)gsm, (CUstream)h->stream, args, nullptr) !=
+          CUDA_SUCCESS)
+        return fail(h, PTSBE_ERR_CUDA, "cuLaunchKernel of generated pass %zu failed", pi);
+    } else if (ph.L >= 4) {
+      // persistent grid: as many CTAs as fit on the GPU, walking all (trajectory, tile) pairs
+      const unsigned threads = std::max(32u, 1u << (ph.L - 4));
+      int per_sm = 0;
+      CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pass_kernel<R>, threads, smem));
+      const long long total = (long long)B * p.tiles;
+      const long long want = (long long)std::max(per_sm, 1) * h->num_sms;
+      const unsigned nblk = (unsigned)std::max<long long>(1, std::min(total, want));
+      pass_kernel<R><<<nblk, threads, smem, h->stream>>>(p);
+    } else {
       pass_kernel_small<R><<<grid, 32, 0, h->stream>>>(p);
+    }
     CKL(h);
     if (h->profiling) {
       CK(h, cudaEventRecord(h->ev[h->ev_used + 1], h->stream));
@@ -384,6 +411,7 @@ int ptsbe_create(int device, int n_qubits, int dtype, int batch_cap, ptsbe_engin
   int r = 0;
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (e != cudaSuccess) {
     r = fail(h, PTSBE_ERR_CUDA, "device %d unavailable: %s", device, cudaGetErrorString(e));
   }
@@ -678,6 +706,43 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
     CK(h, cudaFuncSetAttribute(pass_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
   else
     CK(h, cudaFuncSetAttribute(pass_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
+  // circuit-specialised kernels: PTSBE_CODEGEN=1 forces, =0 disables, default for n >= 16
+  h->gen_active = false;
+  h->gen_note.clear();
+  {
+    const char* env = std::getenv("PTSBE_CODEGEN");
+    const int mode = env ? std::atoi(env) : -1;
+    bool want = mode == 1 || (mode < 0 && h->n >= 16);
+    for (auto& P : ph) want = want && P.L >= 4;
+    if (want && n_passes > 0) {
+      gen::GenProgram G;
+      G.c64 = h->dtype == PTSBE_C64;
+      G.mats = mats;
+      G.kinds = kinds.data();
+      G.chans = chans;
+      G.site_chan = site_chan;
+      for (int p = 0; p < n_passes; ++p) {
+        gen::GenPass gp;
+        gp.L = ph[p].L;
+        gp.c = ph[p].c;
+        gp.phases.assign(dph.begin() + ph[p].phase_begin, dph.begin() + ph[p].phase_begin + ph[p].n_phases);
+        for (auto& D : gp.phases) D.op_begin -= 0;
+        gp.ops.assign(dops.begin() + ph[p].op_begin, dops.begin() + ph[p].op_begin + ph[p].n_ops);
+        G.passes.push_back(gp);
+      }
+      const std::string src = gen::generate(G);
+      if (const char* dump = std::getenv("PTSBE_CODEGEN_DUMP")) {
+        if (FILE* f = std::fopen(dump, "w")) { std::fputs(src.c_str(), f); std::fclose(f); }
+      }
+      std::string err;
+      if (gen::compile(src, n_passes, h->dev, h->gen_mod, err)) {
+        h->gen_active = true;
+      } else {
+        h->gen_note = err;
+        if (mode == 1) return fail(h, PTSBE_ERR_CUDA, "codegen: %s", err.c_str());
+      }
+    }
+  }
   h->passes = ph;
   h->n_sites = n_sites;
   h->n_mats = n_mats;
@@ -781,7 +846,7 @@ int ptsbe_info(ptsbe_engine* h, int64_t* out, int n) {
   int max_tile = 0, total_slots = 0;
   for (auto& P : h->passes) { max_tile = std::max(max_tile, P.L); total_slots += P.n_slots; }
   const int64_t vals[] = {h->n, h->dtype, h->cap, (int64_t)h->passes.size(), max_tile, h->n_sites,
-                          h->sbits, total_slots, h->launches};
+                          h->sbits, total_slots, h->launches, h->gen_active ? 1 : 0, h->n_phases_total};
   for (int i = 0; i < n && i < (int)(sizeof vals / sizeof vals[0]); ++i) out[i] = vals[i];
   return 0;
 }

@@ -1,0 +1,305 @@
+// gen_prelude.cuh -- device prelude of the circuit-specialised pass kernels.
+//
+// At ptsbe_load_program time engine.cu emits, for every fused pass, a phase
+// body in which every gate is a straight-line call with compile-time register
+// positions and literal matrix entries (cx / swap become pure register
+// renaming), and every noise site is a CTA-uniform test of the trajectory's
+// outcome.  NVRTC compiles prelude + bodies for sm_100a; the persistent,
+// cp.async double-buffered tile loop below is shared by all passes.
+//
+// This file is embedded verbatim as a string (gen_prelude.inc, produced by
+// build.py) -- it is NOT compiled by nvcc directly.  Keep PassParams identical
+// to pass_kernels.cuh (engine.cu static_asserts the layout).
+typedef unsigned int uint32_t;
+typedef int int32_t;
+typedef unsigned long long uint64_t;
+typedef unsigned char uint8_t;
+typedef long long int64_t;
+
+namespace ptg {
+
+struct DevOp { int32_t kind, arity, b0, b1, ref, slot, k0, k1; };
+struct DevPhase { uint32_t pbits; int32_t op_begin, n_ops, pad; };
+struct DevChan { int32_t n_outcomes, mat_base, general, arity; uint64_t identity_mask; };
+struct PassParams {
+  void* states; int n; int L; int c; uint64_t qmask;
+  const DevOp* ops; int n_ops; const DevPhase* phases; int n_phases;
+  const uint8_t* sel; int S; const int32_t* site_chan; const DevChan* chans;
+  const void* mats; const int32_t* mat_kind; const double* nst; int use_scale; int gen_zero;
+  double* partials; const int32_t* status; int B; long long tiles;
+};
+
+template <typename R> struct Cplx;
+template <> struct Cplx<float> { typedef float2 V; typedef float4 W; };
+template <> struct Cplx<double> { typedef double2 V; typedef double2 W; };
+
+__device__ __forceinline__ float2 mk(float2*, double x, double y) { return make_float2((float)x, (float)y); }
+__device__ __forceinline__ double2 mk(double2*, double x, double y) { return make_double2(x, y); }
+
+template <typename V> __device__ __forceinline__ V cmul(V d, V x) {
+  V r; r.x = d.x * x.x - d.y * x.y; r.y = d.x * x.y + d.y * x.x; return r;
+}
+template <typename V> __device__ __forceinline__ V cmadd2(V m0, V a, V m1, V b) {
+  V r;
+  r.x = m0.x * a.x - m0.y * a.y + m1.x * b.x - m1.y * b.y;
+  r.y = m0.x * a.y + m0.y * a.x + m1.x * b.y + m1.y * b.x;
+  return r;
+}
+template <typename V> __device__ __forceinline__ V cmadd4(V m0, V m1, V m2, V m3, V a, V b, V c, V d) {
+  V r;
+  r.x = m0.x * a.x - m0.y * a.y + m1.x * b.x - m1.y * b.y + m2.x * c.x - m2.y * c.y + m3.x * d.x - m3.y * d.y;
+  r.y = m0.x * a.y + m0.y * a.x + m1.x * b.y + m1.y * b.x + m2.x * c.y + m2.y * c.x + m3.x * d.y + m3.y * d.x;
+  return r;
+}
+__device__ __forceinline__ double prob64(float2 a) {
+  const double x = a.x, y = a.y;
+  return __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y));
+}
+__device__ __forceinline__ double prob64(double2 a) {
+  return __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y));
+}
+
+// ---- gate kernels on a 16-amplitude register group; K* compile-time bit positions
+template <int K, typename V> __device__ __forceinline__ void g1(V* a, V m00, V m01, V m10, V m11) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (!(j & (1 << K))) {
+      const V x = a[j], y = a[j | (1 << K)];
+      a[j] = cmadd2(m00, x, m01, y);
+      a[j | (1 << K)] = cmadd2(m10, x, m11, y);
+    }
+}
+template <int K, typename V, typename R> __device__ __forceinline__ void g1r(V* a, R m00, R m01, R m10, R m11) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (!(j & (1 << K))) {
+      const V x = a[j], y = a[j | (1 << K)];
+      V u, v;
+      u.x = m00 * x.x + m01 * y.x; u.y = m00 * x.y + m01 * y.y;
+      v.x = m10 * x.x + m11 * y.x; v.y = m10 * x.y + m11 * y.y;
+      a[j] = u; a[j | (1 << K)] = v;
+    }
+}
+template <int K, typename V> __device__ __forceinline__ void g1d(V* a, V d0, V d1) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) a[j] = cmul((j & (1 << K)) ? d1 : d0, a[j]);
+}
+template <int K, typename V> __device__ __forceinline__ void g1p(V* a, V d1) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (j & (1 << K)) a[j] = cmul(d1, a[j]);
+}
+template <int K, typename V> __device__ __forceinline__ void g1a(V* a, V m01, V m10) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (!(j & (1 << K))) {
+      const V x = a[j], y = a[j | (1 << K)];
+      a[j] = cmul(m01, y); a[j | (1 << K)] = cmul(m10, x);
+    }
+}
+template <int K, typename V> __device__ __forceinline__ void g1x(V* a) {   // X: swap, no arithmetic
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (!(j & (1 << K))) { const V t = a[j]; a[j] = a[j | (1 << K)]; a[j | (1 << K)] = t; }
+}
+template <int KH, int KL, typename V> __device__ __forceinline__ void g2(V* a, const V* m) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (!(j & (1 << KH)) && !(j & (1 << KL))) {
+      const int i1 = j | (1 << KL), i2 = j | (1 << KH), i3 = j | (1 << KH) | (1 << KL);
+      const V v0 = a[j], v1 = a[i1], v2 = a[i2], v3 = a[i3];
+      a[j] = cmadd4(m[0], m[1], m[2], m[3], v0, v1, v2, v3);
+      a[i1] = cmadd4(m[4], m[5], m[6], m[7], v0, v1, v2, v3);
+      a[i2] = cmadd4(m[8], m[9], m[10], m[11], v0, v1, v2, v3);
+      a[i3] = cmadd4(m[12], m[13], m[14], m[15], v0, v1, v2, v3);
+    }
+}
+template <int KH, int KL, typename V> __device__ __forceinline__ void g2cx(V* a) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if ((j & (1 << KH)) && !(j & (1 << KL))) { const V t = a[j]; a[j] = a[j | (1 << KL)]; a[j | (1 << KL)] = t; }
+}
+template <int KH, int KL, typename V> __device__ __forceinline__ void g2sw(V* a) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if ((j & (1 << KH)) && !(j & (1 << KL))) {
+      const int o = (j & ~(1 << KH)) | (1 << KL);
+      const V t = a[j]; a[j] = a[o]; a[o] = t;
+    }
+}
+template <int KH, int KL, typename V> __device__ __forceinline__ void g2d(V* a, V d0, V d1, V d2, V d3) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int s = ((j >> KH) & 1) * 2 + ((j >> KL) & 1);
+    a[j] = cmul(s == 0 ? d0 : s == 1 ? d1 : s == 2 ? d2 : d3, a[j]);
+  }
+}
+
+// ---- addressing
+__device__ __forceinline__ uint32_t swz(float2*, uint32_t i) {   // never flips bit 0
+  const uint32_t h = (i >> 3) ^ (i >> 7) ^ ((i >> 7) << 1) ^ (i >> 11);
+  return i ^ (h & 14u);
+}
+__device__ __forceinline__ uint32_t swz(double2*, uint32_t i) {
+  const uint32_t h = (i >> 3) ^ (i >> 6) ^ ((i >> 6) << 1) ^ (i >> 9) ^ (i >> 12);
+  return i ^ (h & 7u);
+}
+__device__ __forceinline__ uint64_t pdep64(uint64_t src, uint64_t mask) {
+  uint64_t out = 0;
+  while (mask) {
+    const uint64_t low = mask & (~mask + 1);
+    if (src & 1) out |= low;
+    src >>= 1;
+    mask ^= low;
+  }
+  return out;
+}
+__device__ __forceinline__ uint32_t ins0(uint32_t p, int bit) {
+  const uint32_t lo = p & ((1u << bit) - 1u);
+  return ((p ^ lo) << 1) | lo;
+}
+__device__ __forceinline__ void cp_async16(void* smem_ptr, const void* gptr) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_ptr);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gptr) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void st_stream(float4* p, float4 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v); }
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (threadIdx.x == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    for (int i = 0; i < nw; ++i) r += red[i];
+  }
+  __syncthreads();
+  return r;
+}
+
+// ---- phase register load / store (16 amplitudes at sg ^ so[j]; so[] literal)
+template <typename V, int P0>
+__device__ __forceinline__ void ld16(V* a, const V* cur, uint32_t sg, const uint32_t* so, bool active, double scale) {
+  if (!active) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) a[j] = mk((V*)0, 0.0, 0.0);
+    return;
+  }
+  if (sizeof(V) == 8 && P0 == 0) {      // bit 0 in the phase: adjacent pairs, 16-B accesses
+#pragma unroll
+    for (int j = 0; j < 16; j += 2) {
+      const float4 w = *reinterpret_cast<const float4*>(cur + (sg ^ so[j]));
+      a[j] = mk((V*)0, w.x, w.y);
+      a[j + 1] = mk((V*)0, w.z, w.w);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) a[j] = cur[sg ^ so[j]];
+  }
+  if (scale != 1.0) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) { a[j].x *= scale; a[j].y *= scale; }
+  }
+}
+template <typename V, int P0>
+__device__ __forceinline__ void st16(const V* a, V* cur, uint32_t sg, const uint32_t* so, bool active) {
+  if (!active) return;
+  if (sizeof(V) == 8 && P0 == 0) {
+#pragma unroll
+    for (int j = 0; j < 16; j += 2) {
+      float4 w; w.x = a[j].x; w.y = a[j].y; w.z = a[j + 1].x; w.w = a[j + 1].y;
+      *reinterpret_cast<float4*>(cur + (sg ^ so[j])) = w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) cur[sg ^ so[j]] = a[j];
+  }
+}
+template <typename V>
+__device__ __forceinline__ void zero16(V* a, uint64_t base, uint32_t gb, const uint32_t* off, bool active) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) a[j] = mk((V*)0, (active && base == 0 && (gb | off[j]) == 0) ? 1.0 : 0.0, 0.0);
+}
+
+// Persistent, double-buffered tile loop shared by every generated pass kernel.
+// body(cur, b, sel_row, tile, base, scale, red) runs the pass's phases on one tile.
+template <typename R, int L, int C, class Body>
+__device__ __forceinline__ void run_pass(const PassParams& p, Body body) {
+  typedef typename Cplx<R>::V V;
+  typedef typename Cplx<R>::W W;
+  const int VPW = sizeof(W) / sizeof(V);
+  const uint32_t TL = 1u << L;
+  extern __shared__ __align__(16) unsigned char smem[];
+  V* buf0 = reinterpret_cast<V*>(smem);
+  V* buf1 = buf0 + TL;
+  uint64_t* rowoff = reinterpret_cast<uint64_t*>(buf1 + TL);
+  double* red = reinterpret_cast<double*>(rowoff + (TL >> C));
+  const uint64_t nmask = (p.n >= 64) ? ~0ull : ((1ull << p.n) - 1ull);
+  const uint64_t comp = ~p.qmask & nmask;
+  const uint64_t hmask = p.qmask & ~((1ull << C) - 1ull);
+  for (uint32_t r = threadIdx.x; r < (TL >> C); r += blockDim.x) rowoff[r] = pdep64(r, hmask);
+  __syncthreads();
+  const int cpr_log = C - (VPW == 2 ? 1 : 0);
+  const uint32_t nvec = TL / VPW;
+  const long long total = (long long)p.B * p.tiles;
+  long long t = blockIdx.x;
+  int lb = -1;
+  uint64_t lbase = 0;
+  if (t < total) {
+    const int bb = (int)(t / p.tiles);
+    if (!p.gen_zero && p.status[bb] == 0) {
+      const uint64_t base = pdep64((uint64_t)(t - (long long)bb * p.tiles), comp);
+      const V* src = reinterpret_cast<const V*>(p.states) + ((size_t)bb << p.n) + base;
+#pragma unroll 4
+      for (uint32_t u = threadIdx.x; u < nvec; u += blockDim.x) {
+        const uint32_t r = u >> cpr_log, j = u & ((1u << cpr_log) - 1u);
+        cp_async16(buf0 + swz((V*)0, (r << C) | (j * VPW)), src + rowoff[r] + (uint64_t)j * VPW);
+      }
+    }
+  }
+  cp_async_commit();
+  for (int it = 0; t < total; t += gridDim.x, ++it) {
+    V* cur = (it & 1) ? buf1 : buf0;
+    V* nxt = (it & 1) ? buf0 : buf1;
+    const long long tn = t + gridDim.x;
+    if (tn < total) {
+      const int bb = (int)(tn / p.tiles);
+      if (!p.gen_zero && p.status[bb] == 0) {
+        const uint64_t base = pdep64((uint64_t)(tn - (long long)bb * p.tiles), comp);
+        const V* src = reinterpret_cast<const V*>(p.states) + ((size_t)bb << p.n) + base;
+#pragma unroll 4
+        for (uint32_t u = threadIdx.x; u < nvec; u += blockDim.x) {
+          const uint32_t r = u >> cpr_log, j = u & ((1u << cpr_log) - 1u);
+          cp_async16(nxt + swz((V*)0, (r << C) | (j * VPW)), src + rowoff[r] + (uint64_t)j * VPW);
+        }
+      }
+    }
+    cp_async_commit();
+    cp_async_wait1();
+    __syncthreads();
+    const int b = (int)(t / p.tiles);
+    const long long tile = t - (long long)b * p.tiles;
+    if (p.status[b] != 0) continue;
+    if (b != lb) { lb = b; }
+    const uint64_t base = pdep64((uint64_t)tile, comp);
+    (void)lbase;
+    const double scale = (p.use_scale && !p.gen_zero) ? rsqrt(p.nst[b]) : 1.0;
+    body(cur, b, p.sel + (size_t)b * p.S, tile, base, scale, red);
+    V* st = reinterpret_cast<V*>(p.states) + ((size_t)b << p.n) + base;
+#pragma unroll 4
+    for (uint32_t u = threadIdx.x; u < nvec; u += blockDim.x) {
+      const uint32_t r = u >> cpr_log, j = u & ((1u << cpr_log) - 1u);
+      const W w = *reinterpret_cast<const W*>(cur + swz((V*)0, (r << C) | (j * VPW)));
+      st_stream(reinterpret_cast<W*>(st + rowoff[r] + (uint64_t)j * VPW), w);
+    }
+    __syncthreads();
+  }
+  cp_async_wait0();
+}
+
+}  // namespace ptg

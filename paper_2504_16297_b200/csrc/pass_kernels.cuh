@@ -90,8 +90,9 @@ struct PassParams {
 // ---- shared-memory swizzle: spreads the 32 lanes of a phase access over banks
 template <typename V> __device__ __forceinline__ uint32_t swz(uint32_t i);
 template <> __device__ __forceinline__ uint32_t swz<float2>(uint32_t i) {
-  const uint32_t h = (i >> 4) ^ (i >> 8) ^ ((i >> 8) << 1) ^ (i >> 12);
-  return i ^ (h & 15u);
+  // never flips bit 0: adjacent amplitude pairs stay one aligned 16-B vector
+  const uint32_t h = (i >> 3) ^ (i >> 7) ^ ((i >> 7) << 1) ^ (i >> 11);
+  return i ^ (h & 14u);
 }
 template <> __device__ __forceinline__ uint32_t swz<double2>(uint32_t i) {
   const uint32_t h = (i >> 3) ^ (i >> 6) ^ ((i >> 6) << 1) ^ (i >> 9) ^ (i >> 12);
@@ -243,13 +244,25 @@ __device__ __forceinline__ void apply_code(V* a, int code, const V* m) {
 }
 
 // Shared-memory layout of the pass kernel (dynamic):
-//   tile [2^L] V | rowoff [2^(L-c)] u64 | red [32] f64 | cops [n_ops] CompactOp | cph [n_phases] int2
+//   buf[2][2^L] V | rowoff [2^(L-c)] u64 | red [32] f64 | cops [n_ops] CompactOp | cph [n_phases] int2
 __host__ __device__ inline size_t pass_smem_bytes(int L, int c, size_t amp_bytes, int n_ops, int n_phases) {
-  return ((size_t)1 << L) * amp_bytes + (((size_t)1 << L) >> c) * 8 + 32 * 8 +
+  return 2 * ((size_t)1 << L) * amp_bytes + (((size_t)1 << L) >> c) * 8 + 32 * 8 +
          (size_t)n_ops * sizeof(CompactOp) + (size_t)n_phases * 8;
 }
 
-// Threads = max(32, 2^(L-4)): each thread owns at most one 16-amplitude group per phase.
+__device__ __forceinline__ void cp_async16(void* smem_ptr, const void* gptr) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_ptr);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gptr) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// Persistent, double-buffered pass kernel.  The grid walks the flattened
+// (trajectory, tile) space; while a CTA runs the phases of tile i out of one
+// shared buffer, cp.async streams tile i+gridDim into the other, so HBM
+// traffic overlaps the register work.  Threads = max(32, 2^(L-4)): each thread
+// owns at most one 16-amplitude group per phase.
 template <typename R>
 __global__ void __launch_bounds__(sizeof(R) == 8 ? 256 : 512) pass_kernel(PassParams p) {
   using V = typename Cplx<R>::V;
@@ -257,144 +270,176 @@ __global__ void __launch_bounds__(sizeof(R) == 8 ? 256 : 512) pass_kernel(PassPa
   constexpr int VPW = sizeof(W) / sizeof(V);   // amplitudes per 16-B vector
   extern __shared__ __align__(16) unsigned char smem[];
 
-  const int b = blockIdx.y;
-  if (p.status[b] != 0) return;                 // annihilated trajectories stop evolving
   const int L = p.L, c = p.c;
   const uint32_t TL = 1u << L;
-  V* tile = reinterpret_cast<V*>(smem);
-  uint64_t* rowoff = reinterpret_cast<uint64_t*>(smem + (size_t)TL * sizeof(V));
+  V* buf0 = reinterpret_cast<V*>(smem);
+  V* buf1 = buf0 + TL;
+  uint64_t* rowoff = reinterpret_cast<uint64_t*>(buf1 + TL);
   double* red = reinterpret_cast<double*>(rowoff + (TL >> c));
   CompactOp* cops = reinterpret_cast<CompactOp*>(red + 32);
   int2* cph = reinterpret_cast<int2*>(cops + p.n_ops);
 
   const uint64_t nmask = (p.n >= 64) ? ~0ull : ((1ull << p.n) - 1ull);
-  const uint64_t base = pdep64((uint64_t)blockIdx.x, ~p.qmask & nmask);
+  const uint64_t comp = ~p.qmask & nmask;
   const uint64_t hmask = p.qmask & ~((1ull << c) - 1ull);
   const uint32_t rows = TL >> c;
   for (uint32_t r = threadIdx.x; r < rows; r += blockDim.x) rowoff[r] = pdep64(r, hmask);
-
-  // ---- warp 0: this trajectory's op list, identity outcomes dropped, decoded once
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    int out = 0;
-    for (int ph = 0; ph < p.n_phases; ++ph) {
-      const DevPhase P = p.phases[ph];
-      const int start = out;
-      for (int k0 = 0; k0 < P.n_ops; k0 += 32) {
-        const int k = P.op_begin + k0 + lane;
-        bool keep = false;
-        CompactOp co{0, 0, -1, 0};
-        if (k0 + lane < P.n_ops) {
-          const DevOp op = p.ops[k];
-          int mat = op.ref;
-          keep = true;
-          if (op.kind == 1) {
-            const int outcome = p.sel[(size_t)b * p.S + op.ref];
-            const DevChan ch = p.chans[p.site_chan[op.ref]];
-            keep = !((ch.identity_mask >> outcome) & 1ull);
-            mat = ch.mat_base + outcome;
-            if (ch.general) co.slot = op.slot;
-          }
-          co.mat = mat;
-          co.code = p.mat_kind[mat] * 16 + op.k0 * 4 + (op.arity == 2 ? op.k1 : 0);
-        }
-        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-        if (keep) cops[out + __popc(bal & ((1u << lane) - 1u))] = co;
-        out += __popc(bal);
-      }
-      if (lane == 0) cph[ph] = make_int2(start, out - start);
-    }
-  }
   __syncthreads();
 
-  V* st = reinterpret_cast<V*>(p.states) + ((size_t)b << p.n);
   const int cpr_log = c - (VPW == 2 ? 1 : 0);   // 16-B vectors per row, log2
   const uint32_t nvec = TL / VPW;
+  const long long total = (long long)p.B * p.tiles;
 
-  // ---- HBM -> shared (coalesced rows), or synthesize |0..0>
-  if (p.gen_zero) {
-    for (uint32_t i = threadIdx.x; i < TL; i += blockDim.x) {
-      V z; z.x = (base == 0 && i == 0) ? R(1) : R(0); z.y = R(0);
-      tile[swz<V>(i)] = z;
-    }
-  } else {
-    const R scale = p.use_scale ? (R)rsqrt(p.nst[b]) : R(1);
+  auto issue_load = [&](long long tt, V* dst) {
+    const int bb = (int)(tt / p.tiles);
+    if (p.gen_zero || p.status[bb] != 0) return;
+    const uint64_t base = pdep64((uint64_t)(tt - (long long)bb * p.tiles), comp);
+    const V* src = reinterpret_cast<const V*>(p.states) + ((size_t)bb << p.n) + base;
 #pragma unroll 4
     for (uint32_t u = threadIdx.x; u < nvec; u += blockDim.x) {
       const uint32_t r = u >> cpr_log;
       const uint32_t j = u & ((1u << cpr_log) - 1u);
-      const uint64_t g = base + rowoff[r] + (uint64_t)j * VPW;
-      const W w = ld_stream(reinterpret_cast<const W*>(st + g));
-      const uint32_t li = (r << c) | (j * VPW);
-      if constexpr (VPW == 2) {
-        const uint32_t s0 = swz<V>(li);
-        tile[s0] = make_float2(w.x * scale, w.y * scale);
-        tile[s0 ^ swz<V>(1u)] = make_float2(w.z * scale, w.w * scale);   // swz is GF(2)-linear
-      } else {
-        tile[swz<V>(li)] = make_double2(w.x * scale, w.y * scale);
-      }
+      cp_async16(dst + swz<V>((r << c) | (j * VPW)), src + rowoff[r] + (uint64_t)j * VPW);
     }
-  }
-  __syncthreads();
+  };
 
-  // ---- phases: shared -> registers, apply, registers -> shared
+  long long t = blockIdx.x;
+  if (t < total) issue_load(t, buf0);
+  cp_async_commit();
   const V* mats = reinterpret_cast<const V*>(p.mats);
   const uint32_t g = threadIdx.x;               // this thread's group
   const bool active = g < (TL >> 4);            // blockDim may exceed 2^(L-4) for L < 8
-  for (int ph = 0; ph < p.n_phases; ++ph) {
-    const DevPhase P = p.phases[ph];
-    const int p0 = P.pbits & 31, p1 = (P.pbits >> 5) & 31, p2 = (P.pbits >> 10) & 31, p3 = (P.pbits >> 15) & 31;
-    const uint32_t gb = insert0(insert0(insert0(insert0(g, p0), p1), p2), p3);
-    // swz is linear over GF(2) and gb / offsets have disjoint bits: addr_j = swz(gb) ^ swz(off_j)
-    const uint32_t sg = swz<V>(gb);
-    uint32_t so[16];
-    so[0] = 0;
-    so[1] = swz<V>(1u << p0);
-    so[2] = swz<V>(1u << p1);
-    so[4] = swz<V>(1u << p2);
-    so[8] = swz<V>(1u << p3);
-#pragma unroll
-    for (int j = 3; j < 16; ++j)
-      if (j & (j - 1)) so[j] = so[j & (j - 1)] ^ so[j & -j];
-    V a[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) a[j] = active ? tile[sg ^ so[j]] : make_vec2<V>(0, 0);
-    const int2 range = cph[ph];
-    for (int k = range.x; k < range.x + range.y; ++k) {
-      const CompactOp co = cops[k];
-      apply_code(a, co.code, mats + (size_t)co.mat * 16);
-      if (co.slot >= 0) {
-        double s = 0.0;
-#pragma unroll
-        for (int j = 0; j < 16; ++j) s += prob64(a[j]);
-        s = block_sum_f64(s, red);
-        if (threadIdx.x == 0) p.partials[((size_t)co.slot * p.B + b) * p.tiles + blockIdx.x] = s;
+  int cur_b = -1;
+  for (int it = 0; t < total; t += gridDim.x, ++it) {
+    V* cur = (it & 1) ? buf1 : buf0;
+    V* nxt = (it & 1) ? buf0 : buf1;
+    if (t + gridDim.x < total) issue_load(t + gridDim.x, nxt);
+    cp_async_commit();
+    cp_async_wait<1>();                         // this thread's copies of `cur` landed
+    __syncthreads();                            // ... and everyone else's
+    const int b = (int)(t / p.tiles);
+    const long long tile = t - (long long)b * p.tiles;
+    if (p.status[b] != 0) continue;             // annihilated: stop evolving (CTA-uniform)
+    if (b != cur_b) {
+      // warp 0: this trajectory's op list, identity outcomes dropped, decoded once
+      if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        int out = 0;
+        for (int ph = 0; ph < p.n_phases; ++ph) {
+          const DevPhase P = p.phases[ph];
+          const int start = out;
+          for (int k0 = 0; k0 < P.n_ops; k0 += 32) {
+            const int k = P.op_begin + k0 + lane;
+            bool keep = false;
+            CompactOp co{0, 0, -1, 0};
+            if (k0 + lane < P.n_ops) {
+              const DevOp op = p.ops[k];
+              int mat = op.ref;
+              keep = true;
+              if (op.kind == 1) {
+                const int outcome = p.sel[(size_t)b * p.S + op.ref];
+                const DevChan ch = p.chans[p.site_chan[op.ref]];
+                keep = !((ch.identity_mask >> outcome) & 1ull);
+                mat = ch.mat_base + outcome;
+                if (ch.general) co.slot = op.slot;
+              }
+              co.mat = mat;
+              co.code = p.mat_kind[mat] * 16 + op.k0 * 4 + (op.arity == 2 ? op.k1 : 0);
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+            if (keep) cops[out + __popc(bal & ((1u << lane) - 1u))] = co;
+            out += __popc(bal);
+          }
+          if (lane == 0) cph[ph] = make_int2(start, out - start);
+        }
       }
+      __syncthreads();
+      cur_b = b;
     }
-    if (active) {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) tile[sg ^ so[j]] = a[j];
-    }
-    __syncthreads();
-  }
+    const uint64_t base = pdep64((uint64_t)tile, comp);
+    const R scale = (p.use_scale && !p.gen_zero) ? (R)rsqrt(p.nst[b]) : R(1);
 
-  // ---- shared -> HBM
-#pragma unroll 4
-  for (uint32_t u = threadIdx.x; u < nvec; u += blockDim.x) {
-    const uint32_t r = u >> cpr_log;
-    const uint32_t j = u & ((1u << cpr_log) - 1u);
-    const uint64_t gi = base + rowoff[r] + (uint64_t)j * VPW;
-    const uint32_t li = (r << c) | (j * VPW);
-    W w;
-    if constexpr (VPW == 2) {
-      const uint32_t s0 = swz<V>(li);
-      const V x = tile[s0], y = tile[s0 ^ swz<V>(1u)];
-      w = make_float4(x.x, x.y, y.x, y.y);
-    } else {
-      w = tile[swz<V>(li)];
+    // ---- phases: shared -> registers, apply, registers -> shared
+    for (int ph = 0; ph < p.n_phases; ++ph) {
+      const DevPhase P = p.phases[ph];
+      const int p0 = P.pbits & 31, p1 = (P.pbits >> 5) & 31, p2 = (P.pbits >> 10) & 31, p3 = (P.pbits >> 15) & 31;
+      const uint32_t gb = insert0(insert0(insert0(insert0(g, p0), p1), p2), p3);
+      // swz is linear over GF(2) and gb / offsets have disjoint bits: addr_j = swz(gb) ^ swz(off_j)
+      const uint32_t sg = swz<V>(gb);
+      uint32_t so[16];
+      so[0] = 0;
+      so[1] = swz<V>(1u << p0);
+      so[2] = swz<V>(1u << p1);
+      so[4] = swz<V>(1u << p2);
+      so[8] = swz<V>(1u << p3);
+#pragma unroll
+      for (int j = 3; j < 16; ++j)
+        if (j & (j - 1)) so[j] = so[j & (j - 1)] ^ so[j & -j];
+      V a[16];
+      if (ph == 0 && p.gen_zero) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const bool one = base == 0 && active && (gb | ((j & 1) << p0) | (((j >> 1) & 1) << p1) |
+                                                     (((j >> 2) & 1) << p2) | (((j >> 3) & 1) << p3)) == 0;
+          a[j] = make_vec2<V>(one ? 1.0 : 0.0, 0.0);
+        }
+      } else if (active) {
+        if (VPW == 2 && p0 == 0) {            // bit 0 in the phase: adjacent pairs, 16-B accesses
+#pragma unroll
+          for (int j = 0; j < 16; j += 2) {
+            const float4 w = *reinterpret_cast<const float4*>(cur + (sg ^ so[j]));
+            a[j] = make_vec2<V>(w.x, w.y);
+            a[j + 1] = make_vec2<V>(w.z, w.w);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) a[j] = cur[sg ^ so[j]];
+        }
+        if (ph == 0 && p.use_scale) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) { a[j].x *= scale; a[j].y *= scale; }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) a[j] = make_vec2<V>(0, 0);
+      }
+      const int2 range = cph[ph];
+      for (int k = range.x; k < range.x + range.y; ++k) {
+        const CompactOp co = cops[k];
+        apply_code(a, co.code, mats + (size_t)co.mat * 16);
+        if (co.slot >= 0) {
+          double s = 0.0;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) s += prob64(a[j]);
+          s = block_sum_f64(s, red);
+          if (threadIdx.x == 0) p.partials[((size_t)co.slot * p.B + b) * p.tiles + tile] = s;
+        }
+      }
+      if (active) {
+        if (VPW == 2 && p0 == 0) {
+#pragma unroll
+          for (int j = 0; j < 16; j += 2)
+            *reinterpret_cast<float4*>(cur + (sg ^ so[j])) = make_float4(a[j].x, a[j].y, a[j + 1].x, a[j + 1].y);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) cur[sg ^ so[j]] = a[j];
+        }
+      }
+      __syncthreads();
     }
-    st_stream(reinterpret_cast<W*>(st + gi), w);
+
+    // ---- shared -> HBM
+    V* st = reinterpret_cast<V*>(p.states) + ((size_t)b << p.n) + base;
+#pragma unroll 4
+    for (uint32_t u = threadIdx.x; u < nvec; u += blockDim.x) {
+      const uint32_t r = u >> cpr_log;
+      const uint32_t j = u & ((1u << cpr_log) - 1u);
+      const W w = *reinterpret_cast<const W*>(cur + swz<V>((r << c) | (j * VPW)));
+      st_stream(reinterpret_cast<W*>(st + rowoff[r] + (uint64_t)j * VPW), w);
+    }
+    __syncthreads();                            // `cur` is refilled two iterations from now
   }
+  cp_async_wait<0>();
 }
 
 // Tiny states (L < 4): one op at a time in shared memory.

@@ -193,9 +193,10 @@ class Engine:
         return float(ms.value), int(n.value)
 
     def info(self) -> dict:
-        out = np.zeros(9, dtype=np.int64)
+        out = np.zeros(11, dtype=np.int64)
         self._check(self.lib.ptsbe_info(self.h, _ptr(out), out.size), "ptsbe_info")
-        keys = ("n", "dtype", "cap", "n_passes", "tile_bits", "n_sites", "sample_bits", "norm_slots", "launches")
+        keys = ("n", "dtype", "cap", "n_passes", "tile_bits", "n_sites", "sample_bits", "norm_slots", "launches",
+                "codegen", "n_phases")
         return dict(zip(keys, (int(v) for v in out)))
 
 
