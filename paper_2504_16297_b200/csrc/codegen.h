@@ -156,12 +156,14 @@ struct Emitter {
 
 struct GenPass {
   int L, c;
+  uint64_t qmask;
   std::vector<DevPhase> phases;
   std::vector<DevOp> ops;   // phase-major, k0/k1 filled
 };
 
 struct GenProgram {
   bool c64;
+  int n;
   const double* mats;       // n_mats x 32 doubles
   const int32_t* kinds;     // n_mats
   const ptsbe_channel* chans;
@@ -171,6 +173,24 @@ struct GenProgram {
 
 inline std::string kernel_name(int pass) { return "ptsbe_pass_" + std::to_string(pass); }
 
+// Lambda scattering the low bits of x onto the set bits of `mask` (PDEP as shift/mask runs).
+inline std::string scatter_fn(uint64_t mask, const char* arg_type) {
+  std::ostringstream o;
+  o << "[](" << arg_type << " x_) -> uint64_t { return 0ull";
+  int src = 0;
+  for (int q = 0; q < 64;) {
+    if (!((mask >> q) & 1)) { ++q; continue; }
+    int len = 0;
+    while (q + len < 64 && ((mask >> (q + len)) & 1)) ++len;
+    const uint64_t m = len >= 64 ? ~0ull : ((1ull << len) - 1);
+    o << " | ((((uint64_t)x_ >> " << src << ") & 0x" << std::hex << m << std::dec << "ull) << " << q << ")";
+    src += len;
+    q += len;
+  }
+  o << "; }";
+  return o.str();
+}
+
 inline std::string generate(const GenProgram& P) {
   Emitter e(P.c64);
   std::ostringstream& o = e.o;
@@ -178,11 +198,16 @@ inline std::string generate(const GenProgram& P) {
   for (size_t pi = 0; pi < P.passes.size(); ++pi) {
     const GenPass& gp = P.passes[pi];
     const int threads = std::max(32, 1 << (gp.L - 4));
-    o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ") " << kernel_name((int)pi)
-      << "(const ptg::PassParams p) {\n"
+    const uint64_t nmask = P.n >= 64 ? ~0ull : ((1ull << P.n) - 1);
+    const uint64_t comp = ~gp.qmask & nmask;
+    const uint64_t hmask = gp.qmask & ~((1ull << gp.c) - 1);
+    o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << (threads <= 256 ? 2 : 1) << ") "
+      << kernel_name((int)pi) << "(const ptg::PassParams p) {\n"
       << "  typedef " << e.V << " V;\n"
-      << "  ptg::run_pass<" << e.R << ", " << gp.L << ", " << gp.c
-      << ">(p, [&](V* cur, int b, const uint8_t* sel, long long tile, uint64_t base, double scale, double* red) {\n"
+      << "  ptg::run_pass<" << e.R << ", " << gp.L << ", " << gp.c << ", " << (P.n - gp.L) << ">(p,\n"
+      << "    " << scatter_fn(comp, "uint64_t") << ",\n"
+      << "    " << scatter_fn(hmask, "uint32_t") << ",\n"
+      << "    [&](V* cur, int b, const uint8_t* sel, long long tile, uint64_t base, double scale, double* red) {\n"
       << "    const uint32_t g = threadIdx.x;\n"
       << "    const bool active = g < " << (1u << (gp.L - 4)) << "u;\n"
       << "    V a[16];\n";
@@ -295,8 +320,8 @@ inline bool compile(const std::string& src, int n_passes, int dev, Module& out, 
   return true;
 }
 
-inline size_t smem_bytes(int L, int c, size_t amp_bytes) {
-  return 2 * ((size_t)1 << L) * amp_bytes + (((size_t)1 << L) >> c) * 8 + 32 * 8;
+inline size_t smem_bytes(int L, int /*c*/, size_t amp_bytes) {
+  return 2 * ((size_t)1 << L) * amp_bytes + 32 * 8;
 }
 
 }  // namespace gen

@@ -717,6 +717,7 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
     if (want && n_passes > 0) {
       gen::GenProgram G;
       G.c64 = h->dtype == PTSBE_C64;
+      G.n = h->n;
       G.mats = mats;
       G.kinds = kinds.data();
       G.chans = chans;
@@ -725,6 +726,7 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
         gen::GenPass gp;
         gp.L = ph[p].L;
         gp.c = ph[p].c;
+        gp.qmask = ph[p].qmask;
         gp.phases.assign(dph.begin() + ph[p].phase_begin, dph.begin() + ph[p].phase_begin + ph[p].n_phases);
         for (auto& D : gp.phases) D.op_begin -= 0;
         gp.ops.assign(dops.begin() + ph[p].op_begin, dops.begin() + ph[p].op_begin + ph[p].n_ops);

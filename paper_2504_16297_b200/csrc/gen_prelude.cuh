@@ -227,75 +227,82 @@ __device__ __forceinline__ void zero16(V* a, uint64_t base, uint32_t gb, const u
 }
 
 // Persistent, double-buffered tile loop shared by every generated pass kernel.
+// Compile-time: R, tile bits L, contiguous low bits C, TLOG = n - L.
+// tile_base(tile) / row_off(r) scatter bits onto the pass's fixed qubit masks
+// (generated per pass as shift/mask runs).  Each thread's 16-B vectors sit at
+// rows r0 + k*RSTEP with a fixed in-row offset, so their shared and global
+// offsets are a per-thread base plus compile-time constants (swz and the row
+// scatter are linear on disjoint bits).
 // body(cur, b, sel_row, tile, base, scale, red) runs the pass's phases on one tile.
-template <typename R, int L, int C, class Body>
-__device__ __forceinline__ void run_pass(const PassParams& p, Body body) {
+template <typename R, int L, int C, int TLOG, class TileBase, class RowOff, class Body>
+__device__ __forceinline__ void run_pass(const PassParams& p, TileBase tile_base, RowOff row_off, Body body) {
   typedef typename Cplx<R>::V V;
   typedef typename Cplx<R>::W W;
-  const int VPW = sizeof(W) / sizeof(V);
-  const uint32_t TL = 1u << L;
+  constexpr int VPW = sizeof(W) / sizeof(V);
+  constexpr uint32_t TL = 1u << L;
+  constexpr int THREADS = (L - 4) >= 5 ? (1 << (L - 4)) : 32;
+  constexpr int CPR_LOG = C - (VPW == 2 ? 1 : 0);          // 16-B vectors per row, log2
+  constexpr uint32_t NVEC = TL / VPW;
+  constexpr bool FAST = THREADS >= (1 << CPR_LOG) && (NVEC % THREADS) == 0;
+  constexpr int ITER = FAST ? (int)(NVEC / THREADS) : 1;
+  constexpr int RSTEP = FAST ? (THREADS >> CPR_LOG) : 1;   // row stride between a thread's vectors
   extern __shared__ __align__(16) unsigned char smem[];
   V* buf0 = reinterpret_cast<V*>(smem);
   V* buf1 = buf0 + TL;
-  uint64_t* rowoff = reinterpret_cast<uint64_t*>(buf1 + TL);
-  double* red = reinterpret_cast<double*>(rowoff + (TL >> C));
-  const uint64_t nmask = (p.n >= 64) ? ~0ull : ((1ull << p.n) - 1ull);
-  const uint64_t comp = ~p.qmask & nmask;
-  const uint64_t hmask = p.qmask & ~((1ull << C) - 1ull);
-  for (uint32_t r = threadIdx.x; r < (TL >> C); r += blockDim.x) rowoff[r] = pdep64(r, hmask);
-  __syncthreads();
-  const int cpr_log = C - (VPW == 2 ? 1 : 0);
-  const uint32_t nvec = TL / VPW;
-  const long long total = (long long)p.B * p.tiles;
-  long long t = blockIdx.x;
-  int lb = -1;
-  uint64_t lbase = 0;
-  if (t < total) {
-    const int bb = (int)(t / p.tiles);
-    if (!p.gen_zero && p.status[bb] == 0) {
-      const uint64_t base = pdep64((uint64_t)(t - (long long)bb * p.tiles), comp);
-      const V* src = reinterpret_cast<const V*>(p.states) + ((size_t)bb << p.n) + base;
-#pragma unroll 4
-      for (uint32_t u = threadIdx.x; u < nvec; u += blockDim.x) {
-        const uint32_t r = u >> cpr_log, j = u & ((1u << cpr_log) - 1u);
-        cp_async16(buf0 + swz((V*)0, (r << C) | (j * VPW)), src + rowoff[r] + (uint64_t)j * VPW);
+  double* red = reinterpret_cast<double*>(buf1 + TL);
+  const uint32_t tid = threadIdx.x;
+  const uint32_t j0 = tid & ((1u << CPR_LOG) - 1u);
+  const uint32_t r0 = tid >> CPR_LOG;
+  const uint32_t s0 = swz((V*)0, (r0 << C) | (j0 * VPW));
+  const uint64_t g0 = row_off(r0) + (uint64_t)j0 * VPW;
+  const long long total = (long long)p.B << TLOG;
+
+  auto load_tile = [&](long long tt, V* dst) {
+    const int bb = (int)(tt >> TLOG);
+    if (p.gen_zero || p.status[bb] != 0) return;
+    const V* src = reinterpret_cast<const V*>(p.states) + ((size_t)bb << p.n) +
+                   tile_base((uint64_t)(tt & ((1ll << TLOG) - 1)));
+    if (FAST) {
+#pragma unroll
+      for (int k = 0; k < ITER; ++k)
+        cp_async16(dst + (s0 ^ swz((V*)0, (uint32_t)(k * RSTEP) << C)), src + g0 + row_off((uint32_t)(k * RSTEP)));
+    } else {
+      for (uint32_t u = tid; u < NVEC; u += blockDim.x) {
+        const uint32_t r = u >> CPR_LOG, j = u & ((1u << CPR_LOG) - 1u);
+        cp_async16(dst + swz((V*)0, (r << C) | (j * VPW)), src + row_off(r) + (uint64_t)j * VPW);
       }
     }
-  }
+  };
+
+  long long t = blockIdx.x;
+  if (t < total) load_tile(t, buf0);
   cp_async_commit();
   for (int it = 0; t < total; t += gridDim.x, ++it) {
     V* cur = (it & 1) ? buf1 : buf0;
     V* nxt = (it & 1) ? buf0 : buf1;
-    const long long tn = t + gridDim.x;
-    if (tn < total) {
-      const int bb = (int)(tn / p.tiles);
-      if (!p.gen_zero && p.status[bb] == 0) {
-        const uint64_t base = pdep64((uint64_t)(tn - (long long)bb * p.tiles), comp);
-        const V* src = reinterpret_cast<const V*>(p.states) + ((size_t)bb << p.n) + base;
-#pragma unroll 4
-        for (uint32_t u = threadIdx.x; u < nvec; u += blockDim.x) {
-          const uint32_t r = u >> cpr_log, j = u & ((1u << cpr_log) - 1u);
-          cp_async16(nxt + swz((V*)0, (r << C) | (j * VPW)), src + rowoff[r] + (uint64_t)j * VPW);
-        }
-      }
-    }
+    if (t + gridDim.x < total) load_tile(t + gridDim.x, nxt);
     cp_async_commit();
     cp_async_wait1();
     __syncthreads();
-    const int b = (int)(t / p.tiles);
-    const long long tile = t - (long long)b * p.tiles;
+    const int b = (int)(t >> TLOG);
+    const long long tile = t & ((1ll << TLOG) - 1);
     if (p.status[b] != 0) continue;
-    if (b != lb) { lb = b; }
-    const uint64_t base = pdep64((uint64_t)tile, comp);
-    (void)lbase;
+    const uint64_t base = tile_base((uint64_t)tile);
     const double scale = (p.use_scale && !p.gen_zero) ? rsqrt(p.nst[b]) : 1.0;
     body(cur, b, p.sel + (size_t)b * p.S, tile, base, scale, red);
     V* st = reinterpret_cast<V*>(p.states) + ((size_t)b << p.n) + base;
-#pragma unroll 4
-    for (uint32_t u = threadIdx.x; u < nvec; u += blockDim.x) {
-      const uint32_t r = u >> cpr_log, j = u & ((1u << cpr_log) - 1u);
-      const W w = *reinterpret_cast<const W*>(cur + swz((V*)0, (r << C) | (j * VPW)));
-      st_stream(reinterpret_cast<W*>(st + rowoff[r] + (uint64_t)j * VPW), w);
+    if (FAST) {
+#pragma unroll
+      for (int k = 0; k < ITER; ++k) {
+        const W w = *reinterpret_cast<const W*>(cur + (s0 ^ swz((V*)0, (uint32_t)(k * RSTEP) << C)));
+        st_stream(reinterpret_cast<W*>(st + g0 + row_off((uint32_t)(k * RSTEP))), w);
+      }
+    } else {
+      for (uint32_t u = tid; u < NVEC; u += blockDim.x) {
+        const uint32_t r = u >> CPR_LOG, j = u & ((1u << CPR_LOG) - 1u);
+        const W w = *reinterpret_cast<const W*>(cur + swz((V*)0, (r << C) | (j * VPW)));
+        st_stream(reinterpret_cast<W*>(st + row_off(r) + (uint64_t)j * VPW), w);
+      }
     }
     __syncthreads();
   }
