@@ -137,6 +137,23 @@ int ptsbe_set_state(ptsbe_engine* h, int b, const void* buf, uint32_t flags);
 int ptsbe_apply_program(ptsbe_engine* h, const uint8_t* sel, int B,
                         double* out_weight, int32_t* out_status, uint32_t flags);
 
+/* Physical layout: logical qubit q is stored at physical bit perm[q] (NULL =
+ * identity).  Program ops and pass masks are given in physical qubits; shots,
+ * get_state and set_state stay in logical order (indices are mapped back and
+ * re-sorted on device). */
+int ptsbe_set_layout(ptsbe_engine* h, const int32_t* perm);
+
+/* Fusion planner (host only; no GPU or handle needed).  Op i acts on the
+ * LOGICAL qubits in target_masks[i]; general[i] != 0 marks renormalising
+ * sites (never reordered among themselves).  perm_io: in = starting layout,
+ * out = layout after `search_iters` steps of local search minimising the pass
+ * count.  Writes out_pass[i] (pass of op i, ops keep stream order within a
+ * pass) and out_masks[p] (PHYSICAL tile qubit set of pass p).  Returns the
+ * number of passes, or a negative status. */
+int ptsbe_plan(int n_qubits, int n_ops, const uint64_t* target_masks, const uint8_t* general,
+               int tile_bits, int low_bits, int search_iters, uint64_t seed,
+               int32_t* perm_io, int32_t* out_pass, uint64_t* out_masks, int max_passes);
+
 /* Misc */
 int ptsbe_device_memory(int device, uint64_t* free_bytes, uint64_t* total_bytes);
 int ptsbe_synchronize(ptsbe_engine* h);

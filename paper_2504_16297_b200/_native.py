@@ -67,6 +67,9 @@ SIGNATURES = {
     "ptsbe_get_state": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_uint32]),
     "ptsbe_set_state": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_uint32]),
     "ptsbe_device_memory": (C.c_int, [C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "ptsbe_set_layout": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "ptsbe_plan": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_uint64,
+                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
     "ptsbe_synchronize": (C.c_int, [C.c_void_p]),
     "ptsbe_stream": (C.c_void_p, [C.c_void_p]),
     "ptsbe_info": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),

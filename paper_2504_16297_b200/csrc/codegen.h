@@ -238,32 +238,43 @@ inline std::string generate(const GenProgram& P) {
       } else {
         o << "      ptg::ld16<V, " << pb[0] << ">(a, cur, sg, so, active, 1.0);\n";
       }
+      // CTA-uniform: does this trajectory take any non-default outcome in this phase?
+      std::ostringstream err;
+      for (int k = D.op_begin; k < D.op_begin + D.n_ops; ++k)
+        if (gp.ops[k].kind == 1) err << (err.tellp() > 0 ? " | " : "") << "sel[" << gp.ops[k].ref << "]";
+      const bool has_sites = err.tellp() > 0;
+      if (has_sites) o << "      if ((" << err.str() << ") == 0) {\n";
+      // fast path: every site at its default outcome -> straight-line gates only
       for (int k = D.op_begin; k < D.op_begin + D.n_ops; ++k) {
         const DevOp& op = gp.ops[k];
         const int k1 = op.arity == 2 ? op.k1 : 0;
-        o << "      ";
         if (op.kind == 0) {
+          o << "      ";
           e.op(P.kinds[op.ref], op.k0, k1, P.mats + (size_t)op.ref * 32);
           continue;
         }
         const ptsbe_channel& ch = P.chans[P.site_chan[op.ref]];
-        o << "{ const int o_ = sel[" << op.ref << "];\n";
-        bool first = true;
-        for (int oc = 0; oc < ch.n_outcomes; ++oc) {
-          if ((ch.identity_mask >> oc) & 1ull) continue;
-          const int mat = ch.mat_base + oc;
-          o << "        " << (first ? "if" : "else if") << " (o_ == " << oc << ") ";
-          e.op(P.kinds[mat], op.k0, k1, P.mats + (size_t)mat * 32);
-          first = false;
+        if (!(ch.identity_mask & 1ull)) {   // outcome 0 is not the identity (e.g. damping K0)
+          o << "      ";
+          e.op(P.kinds[ch.mat_base], op.k0, k1, P.mats + (size_t)ch.mat_base * 32);
         }
         if (ch.general) {
-          o << "        double s_ = 0.0;\n"
+          o << "      { double s_ = 0.0;\n"
             << "#pragma unroll\n"
             << "        for (int j = 0; j < 16; ++j) s_ += ptg::prob64(a[j]);\n"
             << "        s_ = ptg::block_sum(s_, red);\n"
-            << "        if (threadIdx.x == 0) p.partials[((size_t)" << op.slot << " * p.B + b) * p.tiles + tile] = s_;\n";
+            << "        if (threadIdx.x == 0) p.partials[((size_t)" << op.slot
+            << " * p.B + b) * p.tiles + tile] = s_; }\n";
         }
-        o << "      }\n";
+      }
+      if (has_sites) {
+        // rare path: run the phase through the run-time interpreter on shared memory
+        o << "      } else {\n"
+          << "        ptg::st16<V, " << pb[0] << ">(a, cur, sg, so, active);\n"
+          << "        const uint32_t sb_[4] = {so[1], so[2], so[4], so[8]};\n"
+          << "        ptg::interp_phase<V>(cur, sg, sb_, p, " << ph << ", sel, b, tile, red, active);\n"
+          << "        ptg::ld16<V, " << pb[0] << ">(a, cur, sg, so, active, 1.0);\n"
+          << "      }\n";
       }
       o << "      ptg::st16<V, " << pb[0] << ">(a, cur, sg, so, active);\n"
         << "      __syncthreads();\n"

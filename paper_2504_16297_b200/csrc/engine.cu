@@ -17,6 +17,7 @@
 #include "pass_kernels.cuh"
 #include "sample_kernels.cuh"
 #include "codegen.h"
+#include "planner.h"
 
 using namespace ptsbe;
 
@@ -78,6 +79,10 @@ struct ptsbe_engine {
   size_t chunk_cap = 0;
   uint64_t* d_chunks = nullptr;
   long long launches = 0;
+  // physical layout: logical qubit q stored at physical bit perm[q] (identity unless permuted)
+  bool permuted = false;
+  BitPerm layout{};
+  std::vector<uint8_t> logical;   // per state: 1 = stored in logical order (canonicalised)
   // optional per-launch timing of the pass kernels (CUDA events on h->stream)
   bool profiling = false;
   std::vector<cudaEvent_t> ev;
@@ -236,6 +241,29 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero) {
   return 0;
 }
 
+// Re-store state b in logical (to_logical) or physical order.
+int relayout(ptsbe_engine* h, int b, bool to_logical) {
+  if (!h->permuted || (h->logical[b] != 0) == to_logical) return 0;
+  const size_t bytes = ((size_t)1 << h->n) * h->amp_bytes;
+  char* st = (char*)h->states + (size_t)b * bytes;
+  void* scratch = nullptr;
+  CK(h, cudaMallocAsync(&scratch, bytes, h->stream));
+  BitPerm P = h->layout;            // physical -> logical
+  if (!to_logical) {                 // logical -> physical
+    for (int q = 0; q < h->n; ++q) P.src[h->layout.src[q]] = (int8_t)q;
+  }
+  const unsigned g = (unsigned)std::min<size_t>(((size_t)1 << h->n) / 256 + 1, 8192);
+  if (h->dtype == PTSBE_C64)
+    permute_state<float2><<<g, 256, 0, h->stream>>>((const float2*)st, (float2*)scratch, h->n, P);
+  else
+    permute_state<double2><<<g, 256, 0, h->stream>>>((const double2*)st, (double2*)scratch, h->n, P);
+  CKL(h);
+  CK(h, cudaMemcpyAsync(st, scratch, bytes, cudaMemcpyDeviceToDevice, h->stream));
+  CK(h, cudaFreeAsync(scratch, h->stream));
+  h->logical[b] = to_logical ? 1 : 0;
+  return 0;
+}
+
 template <typename R>
 int rescale_if_needed(ptsbe_engine* h) {
   if (!h->final_general || h->last_B == 0) return 0;
@@ -261,6 +289,10 @@ int run_common(ptsbe_engine* h, const uint8_t* sel, int B, double* out_weight, i
   }
   batch_reset<<<(B + 255) / 256, 256, 0, h->stream>>>(h->d_weight, h->d_nst, h->d_status, h->d_fail, B);
   CKL(h);
+  if (h->permuted && !from_zero)
+    for (int b = 0; b < B; ++b)
+      if (int r = relayout(h, b, false)) return r;
+  for (int b = 0; b < B; ++b) h->logical[b] = 0;
   h->last_B = B;
   int r = h->dtype == PTSBE_C64 ? launch_passes<float>(h, B, from_zero) : launch_passes<double>(h, B, from_zero);
   if (r) return r;
@@ -331,6 +363,20 @@ int sample_impl(ptsbe_engine* h, int B, const int64_t* shots, int rng_mode, cons
   sp.off = h->d_off;
   sp.m = h->d_m;
 
+  // Exact RNG modes replay the reference's CDF, which runs in LOGICAL index
+  // order: canonicalise permuted states first.  Philox mode samples the physical
+  // layout and maps indices back (cheaper); once any state is logical, all are.
+  bool unperm = false;
+  if (h->permuted && total > 0) {
+    bool any_logical = false;
+    for (int b = 0; b < B; ++b) any_logical = any_logical || h->logical[b];
+    if (rng_mode != PTSBE_RNG_PHILOX || any_logical) {
+      for (int b = 0; b < B; ++b)
+        if (int r = relayout(h, b, true)) return r;
+    } else {
+      unperm = true;
+    }
+  }
   if (total > 0) {
     dim3 g1((unsigned)((h->nblk + 7) / 8), (unsigned)B);
     sample_blocksum<R><<<g1, 256, 0, h->stream>>>(sp);
@@ -358,6 +404,13 @@ int sample_impl(ptsbe_engine* h, int B, const int64_t* shots, int rng_mode, cons
     }
     sample_resolve<R><<<gw, 256, 0, h->stream>>>(sp, h->d_chunks, n_chunks, h->d_keys, h->d_idx);
     CKL(h);
+    if (unperm) {   // physical -> logical bitstrings, then ascending order again
+      unpermute_indices<<<std::min<long long>((total + 255) / 256, 4096), 256, 0, h->stream>>>(h->d_idx, total,
+                                                                                                 h->layout);
+      CKL(h);
+      seg_radix_sort<<<B, 1024, 0, h->stream>>>(h->d_idx, h->d_tmp, h->d_off, h->d_m, h->d_status, h->n);
+      CKL(h);
+    }
   }
   sample_rle<<<B, 1024, 0, h->stream>>>(h->d_idx, h->d_off, h->d_m, h->d_status, h->d_runidx, h->d_runcnt,
                                         h->d_nuniq);
@@ -407,6 +460,9 @@ int ptsbe_create(int device, int n_qubits, int dtype, int batch_cap, ptsbe_engin
   h->cap = batch_cap;
   h->amp_bytes = dtype == PTSBE_C64 ? 8 : 16;
   h->sbits = std::min(n_qubits, 9);
+  h->layout.n = n_qubits;
+  for (int q = 0; q < n_qubits && q < 64; ++q) h->layout.src[q] = (int8_t)q;
+  h->logical.assign(batch_cap, 0);
   h->nblk = 1ll << (n_qubits - h->sbits);
   int r = 0;
   cudaError_t e = cudaSetDevice(device);
@@ -781,7 +837,21 @@ int ptsbe_get_state(ptsbe_engine* h, int b, void* buf, uint32_t flags) {
   int r = h->dtype == PTSBE_C64 ? rescale_if_needed<float>(h) : rescale_if_needed<double>(h);
   if (r) return r;
   const size_t bytes = ((size_t)1 << h->n) * h->amp_bytes;
-  if (int e = copy_out(h, buf, (char*)h->states + (size_t)b * bytes, bytes, flags)) return e;
+  const char* src = (char*)h->states + (size_t)b * bytes;
+  void* scratch = nullptr;
+  if (h->permuted && !h->logical[b]) {   // logical order for the caller
+    CK(h, cudaMallocAsync(&scratch, bytes, h->stream));
+    const unsigned g = (unsigned)std::min<size_t>(((size_t)1 << h->n) / 256 + 1, 8192);
+    if (h->dtype == PTSBE_C64)
+      permute_state<float2><<<g, 256, 0, h->stream>>>((const float2*)src, (float2*)scratch, h->n, h->layout);
+    else
+      permute_state<double2><<<g, 256, 0, h->stream>>>((const double2*)src, (double2*)scratch, h->n, h->layout);
+    CKL(h);
+    src = (const char*)scratch;
+  }
+  int e = copy_out(h, buf, src, bytes, flags);
+  if (scratch) cudaFreeAsync(scratch, h->stream);
+  if (e) return e;
   CK(h, cudaStreamSynchronize(h->stream));
   return 0;
 }
@@ -791,7 +861,25 @@ int ptsbe_set_state(ptsbe_engine* h, int b, const void* buf, uint32_t flags) {
   if (b < 0 || b >= h->cap) return fail(h, PTSBE_ERR_VALIDATION, "state %d out of range", b);
   CK(h, cudaSetDevice(h->dev));
   const size_t bytes = ((size_t)1 << h->n) * h->amp_bytes;
-  if (int e = copy_in(h, (char*)h->states + (size_t)b * bytes, buf, bytes, flags)) return e;
+  char* dst = (char*)h->states + (size_t)b * bytes;
+  h->logical[b] = 0;
+  if (h->permuted) {   // caller gives logical order; store physical
+    void* scratch = nullptr;
+    CK(h, cudaMallocAsync(&scratch, bytes, h->stream));
+    if (int e = copy_in(h, scratch, buf, bytes, flags)) return e;
+    BitPerm fwd;     // physical bit perm[q] <- logical bit q
+    fwd.n = h->n;
+    for (int q = 0; q < h->n; ++q) fwd.src[h->layout.src[q]] = (int8_t)q;
+    const unsigned g = (unsigned)std::min<size_t>(((size_t)1 << h->n) / 256 + 1, 8192);
+    if (h->dtype == PTSBE_C64)
+      permute_state<float2><<<g, 256, 0, h->stream>>>((const float2*)scratch, (float2*)dst, h->n, fwd);
+    else
+      permute_state<double2><<<g, 256, 0, h->stream>>>((const double2*)scratch, (double2*)dst, h->n, fwd);
+    CKL(h);
+    cudaFreeAsync(scratch, h->stream);
+  } else if (int e = copy_in(h, dst, buf, bytes, flags)) {
+    return e;
+  }
   const double one = 1.0;
   const int32_t zero = 0;
   CK(h, cudaMemcpyAsync(h->d_nst + b, &one, 8, cudaMemcpyHostToDevice, h->stream));
@@ -800,6 +888,47 @@ int ptsbe_set_state(ptsbe_engine* h, int b, const void* buf, uint32_t flags) {
   h->last_B = std::max(h->last_B, b + 1);
   h->final_general = false;
   return 0;
+}
+
+int ptsbe_set_layout(ptsbe_engine* h, const int32_t* perm) {
+  if (!h) return PTSBE_ERR_VALIDATION;
+  h->permuted = false;
+  h->layout.n = h->n;
+  for (int q = 0; q < h->n; ++q) h->layout.src[q] = (int8_t)q;
+  std::fill(h->logical.begin(), h->logical.end(), 0);
+  if (!perm) return 0;
+  uint64_t seen = 0;
+  for (int q = 0; q < h->n; ++q) {
+    if (perm[q] < 0 || perm[q] >= h->n || ((seen >> perm[q]) & 1))
+      return fail(h, PTSBE_ERR_VALIDATION, "layout is not a permutation of %d qubits", h->n);
+    seen |= 1ull << perm[q];
+    h->layout.src[q] = (int8_t)perm[q];
+    h->permuted = h->permuted || perm[q] != q;
+  }
+  return 0;
+}
+
+int ptsbe_plan(int n_qubits, int n_ops, const uint64_t* target_masks, const uint8_t* general, int tile_bits,
+               int low_bits, int search_iters, uint64_t seed, int32_t* perm_io, int32_t* out_pass,
+               uint64_t* out_masks, int max_passes) {
+  if (n_qubits < 1 || n_qubits > 63 || n_ops < 0 || tile_bits < 1 || low_bits < 0 || !perm_io)
+    return -PTSBE_ERR_VALIDATION;
+  std::vector<plan::Op> ops(n_ops);
+  for (int i = 0; i < n_ops; ++i) ops[i] = plan::Op{target_masks[i], general && general[i] != 0};
+  std::vector<int> perm(perm_io, perm_io + n_qubits);
+  const int L = std::min(tile_bits, n_qubits), c = std::min(low_bits, L);
+  plan::search(n_qubits, ops, perm, L, c, search_iters, seed);
+  std::vector<int> pass;
+  std::vector<uint64_t> masks;
+  const int P = plan::greedy(n_qubits, ops, perm, L, c, &pass, &masks);
+  if (P < 0) return -PTSBE_ERR_VALIDATION;
+  if (P > max_passes) return -PTSBE_ERR_VALIDATION;
+  for (int q = 0; q < n_qubits; ++q) perm_io[q] = perm[q];
+  if (out_pass)
+    for (int i = 0; i < n_ops; ++i) out_pass[i] = pass[i];
+  if (out_masks)
+    for (int p = 0; p < P; ++p) out_masks[p] = masks[p];
+  return P;
 }
 
 int ptsbe_device_memory(int device, uint64_t* free_bytes, uint64_t* total_bytes) {

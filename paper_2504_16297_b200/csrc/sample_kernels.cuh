@@ -370,6 +370,34 @@ __global__ void __launch_bounds__(1024) sample_rle(const uint64_t* idx, const in
   if (threadIdx.x == 0) nuniq[b] = runs;
 }
 
+// Physical layout -> logical bitstrings.  The state may be stored with logical
+// qubit q at physical bit perm[q] (planner.h layout search); shots come out of
+// the CDF in physical order and are mapped back here, then re-sorted.
+struct BitPerm {
+  int8_t src[64];   // logical bit q <- physical bit src[q]
+  int n;
+};
+
+__device__ __forceinline__ uint64_t permute_bits(uint64_t x, const BitPerm& P) {
+  uint64_t out = 0;
+  for (int q = 0; q < P.n; ++q) out |= ((x >> P.src[q]) & 1ull) << q;
+  return out;
+}
+
+__global__ void unpermute_indices(uint64_t* idx, long long total, BitPerm P) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x)
+    idx[i] = permute_bits(idx[i], P);
+}
+
+// out[logical(i)] = in[i] for one state (parity download / upload of permuted layouts).
+template <typename V>
+__global__ void permute_state(const V* in, V* out, int n, BitPerm P) {
+  const size_t N = 1ull << n;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < N; i += (size_t)gridDim.x * blockDim.x)
+    out[permute_bits(i, P)] = in[i];
+}
+
 // Gather each trajectory's runs into one contiguous CSR stream.
 __global__ void compact_runs(const uint64_t* run_idx, const uint32_t* run_cnt, const int64_t* off,
                              const int64_t* nuniq, const int64_t* uoff, uint64_t* out_idx, uint32_t* out_cnt) {

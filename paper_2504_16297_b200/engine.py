@@ -99,11 +99,13 @@ class Engine:
         if prog.n_qubits != self.n:
             raise ValidationError(f"program is for {prog.n_qubits} qubits, engine holds {self.n}")
         order = [(p, i) for p, plan in enumerate(prog.passes) for i in plan.ops]
+        perm = list(range(self.n)) if prog.perm is None else list(prog.perm)
         ops = (N.Op * max(len(order), 1))()
         for j, (p, i) in enumerate(order):
             so = prog.stream[i]
-            t1 = so.targets[1] if len(so.targets) > 1 else -1
-            ops[j] = N.Op(so.kind, len(so.targets), so.targets[0], t1, so.ref, p)
+            t0 = perm[so.targets[0]]
+            t1 = perm[so.targets[1]] if len(so.targets) > 1 else -1
+            ops[j] = N.Op(so.kind, len(so.targets), t0, t1, so.ref, p)
         mats = np.ascontiguousarray(prog.mats.reshape(-1, 16)).view(np.float64).reshape(-1)
         chans = (N.Channel * max(len(prog.chans), 1))()
         for k, ch in enumerate(prog.chans):
@@ -117,6 +119,8 @@ class Engine:
                                          chans, len(prog.chans), _ptr(site_chan), int(site_chan.size),
                                          passes, len(prog.passes))
         self._check(st, "ptsbe_load_program")
+        lay = np.array(perm, dtype=np.int32)
+        self._check(self.lib.ptsbe_set_layout(self.h, C.c_void_p(lay.ctypes.data)), "ptsbe_set_layout")
         self.program = prog
 
     # -- execution

@@ -73,6 +73,7 @@ class Program:
     site_chan: np.ndarray         # (S,) int32
     passes: list = field(default_factory=list)
     g_ref: int = 0                # reference-equivalent full-state passes: #ops + #sites
+    perm: list = None             # logical qubit -> physical bit (None = identity)
 
     @property
     def n_sites(self) -> int:
@@ -189,12 +190,54 @@ def plan_passes(n: int, stream: list, tile_bits: int, low_bits: int) -> list:
     return plans
 
 
+def plan_native(n: int, stream: list, tile_bits: int, low_bits: int, search_iters: int = 0,
+                seed: int = 0, perm=None):
+    """Same greedy rule in libptsbe (planner.h) plus a local search over the
+    physical qubit layout; returns (perm logical->physical, passes in physical qubits)."""
+    import ctypes as C
+
+    from . import _native as N
+    lib = N.load_library()
+    m = len(stream)
+    masks = np.zeros(max(m, 1), dtype=np.uint64)
+    general = np.zeros(max(m, 1), dtype=np.uint8)
+    for i, so in enumerate(stream):
+        for q in so.targets:
+            masks[i] |= np.uint64(1 << q)
+        general[i] = 1 if so.general else 0
+    p = np.arange(n, dtype=np.int32) if perm is None else np.array(perm, dtype=np.int32)
+    out_pass = np.zeros(max(m, 1), dtype=np.int32)
+    out_masks = np.zeros(max(m, 1) + 1, dtype=np.uint64)
+    ptr = lambda a: C.c_void_p(a.ctypes.data)  # noqa: E731
+    P = lib.ptsbe_plan(n, m, ptr(masks), ptr(general), tile_bits, low_bits, search_iters, seed,
+                       ptr(p), ptr(out_pass), ptr(out_masks), out_masks.size)
+    if P < 0:
+        raise ValidationError("fusion planner failed")
+    plans = []
+    for k in range(P):
+        mask = int(out_masks[k])
+        qs = tuple(q for q in range(n) if (mask >> q) & 1)
+        run = 0
+        while run < len(qs) and qs[run] == run:
+            run += 1
+        plans.append(PassPlan(qs, run, [i for i in range(m) if out_pass[i] == k]))
+    return [int(x) for x in p], plans
+
+
+def default_search_iters(n: int, tile_bits: int) -> int:
+    return 3000 if n > tile_bits else 0
+
+
 def compile_circuit(circuit, dtype: str = "c128", tile_bits: int | None = None,
-                    low_bits: int | None = None) -> Program:
+                    low_bits: int | None = None, search_iters: int | None = None, seed: int = 0) -> Program:
+    """Lower + plan.  Circuits wider than a tile get a physical qubit layout chosen
+    by local search to minimise HBM passes (shots and states stay logical)."""
     prog = lower(circuit)
     L = tile_bits if tile_bits is not None else DEFAULT_TILE_BITS[dtype]
     c = low_bits if low_bits is not None else DEFAULT_LOW_BITS[dtype]
-    prog.passes = plan_passes(circuit.n_qubits, prog.stream, L, c)
+    n = circuit.n_qubits
+    iters = default_search_iters(n, L) if search_iters is None else search_iters
+    prog.perm, prog.passes = plan_native(n, prog.stream, L, c, iters, seed)
     return prog
 
 

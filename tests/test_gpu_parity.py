@@ -248,3 +248,36 @@ def test_config4_28q_properties():
         psi = eng.get_state(0)
         assert abs(float(np.sum(np.abs(psi.astype(np.complex128)) ** 2)) - 1.0) < 1e-4
         assert np.all(np.abs(psi[a.indices[: a.offsets[1]].astype(np.int64)]) > 0)
+
+
+def test_permuted_layout_sampling_modes():
+    """Config 2 (17 q, c128) is planned with a permuted physical layout: PCG64 shots must still
+    equal the reference sampler on the logical state, Philox shots must follow |psi|^2."""
+    from scipy import stats
+    c = workloads.build(2, P.parse_circuit, P.parse_noise_model, P.attach_noise)
+    specs = P.enumerate_cutoff(c, 1e-5, 4000)[:3]
+    with Engine(17, "c128", batch_cap=3) as eng:
+        prog = eng.load(c)
+        assert prog.perm != list(range(17))
+        sel = selection_matrix(prog, specs)
+        eng.run(sel)
+        seeds = np.array([mix_seed(7, t) for t in range(3)], dtype=np.uint64)
+        ph = eng.sample([s.shots for s in specs], N.RNG_PHILOX, rng_state=seeds)
+        words = np.concatenate([pcg64_state_words(mix_seed(7, t)) for t in range(3)])
+        ex = eng.sample([s.shots for s in specs], N.RNG_PCG64, rng_state=words)
+        for b, s in enumerate(specs):
+            ref, _ = O.prepare(c, s.selections)
+            assert rel(eng.get_state(b), ref) <= 1e-12
+            rng = np.random.Generator(np.random.PCG64(mix_seed(7, b)))
+            assert ex.counts_dict(b, 17) == O.sample(ref, s.shots, rng, 17)
+            lo, hi = ph.offsets[b], ph.offsets[b + 1]
+            idx = ph.indices[lo:hi].astype(np.int64)
+            assert np.all(np.diff(idx) > 0) and int(ph.counts[lo:hi].sum()) == s.shots
+            probs = np.abs(ref) ** 2
+            assert np.all(probs[idx] > 0)
+            top = np.argsort(probs)[::-1][:8]
+            obs = np.array([ph.counts[lo:hi][idx == t].sum() for t in top], dtype=float)
+            exp = probs[top] * s.shots
+            obs = np.append(obs, s.shots - obs.sum())
+            exp = np.append(exp, s.shots - exp.sum())
+            assert stats.chisquare(obs, exp).pvalue > 0.01

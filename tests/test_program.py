@@ -45,11 +45,13 @@ def test_plan_is_legal_reordering(golden, name, tile_bits, low_bits):
     prog = compile_circuit(c, "c128", tile_bits=tile_bits, low_bits=low_bits)
     order = [i for p in prog.passes for i in p.ops]
     assert sorted(order) == list(range(len(prog.stream)))
+    perm = prog.perm
+    assert sorted(perm) == list(range(c.n_qubits))
     for p in prog.passes:
         assert len(p.qubits) == min(c.n_qubits, tile_bits)
         assert tuple(range(p.low_bits)) == p.qubits[: p.low_bits]
         for i in p.ops:
-            assert set(prog.stream[i].targets) <= set(p.qubits)
+            assert {perm[q] for q in prog.stream[i].targets} <= set(p.qubits)
     rng = np.random.default_rng(1)
     specs = P.presample_probabilistic(c, 40, 1, rng)
     sel = selection_matrix(prog, specs)
@@ -61,6 +63,32 @@ def test_plan_is_legal_reordering(golden, name, tile_bits, low_bits):
         psi, w = _run_stream(c, prog, order, sel[b])
         assert np.linalg.norm(psi - ref_psi) <= 1e-12
         assert w == pytest.approx(ref_w, rel=1e-12)
+
+
+@pytest.mark.parametrize("name", ["brick8", "steane1", "config2"])
+def test_native_planner_matches_python_planner(golden, name):
+    from conftest import build_case
+    from paper_2504_16297_b200.program import lower, plan_native
+    c = build_case(golden["cases"][name])
+    prog = lower(c)
+    for L, lowb in [(5, 3), (6, 4), (12, 4)]:
+        py = plan_passes(c.n_qubits, prog.stream, L, lowb)
+        perm, nat = plan_native(c.n_qubits, prog.stream, L, lowb, search_iters=0)
+        assert perm == list(range(c.n_qubits))
+        assert [(p.qubits, p.low_bits, p.ops) for p in py] == [(p.qubits, p.low_bits, p.ops) for p in nat]
+
+
+def test_layout_search_reduces_passes_config4():
+    from paper_2504_16297_b200.program import lower, plan_native
+    c = W.build(4, P.parse_circuit, P.parse_noise_model, P.attach_noise)
+    prog = lower(c)
+    _, base = plan_native(28, prog.stream, 12, 4, search_iters=0)
+    perm, best = plan_native(28, prog.stream, 12, 4, search_iters=3000)
+    assert len(best) <= len(base) * 0.6
+    # every op's physical targets inside its pass; the reordering is legal (same rule as Python)
+    for p in best:
+        for i in p.ops:
+            assert {perm[q] for q in prog.stream[i].targets} <= set(p.qubits)
 
 
 def test_plan_counts_for_configs():
