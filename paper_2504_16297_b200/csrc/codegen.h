@@ -17,6 +17,7 @@
 #include <cuda.h>
 #include <dlfcn.h>
 
+#include <cmath>
 #include <cstdio>
 #include <map>
 #include <mutex>
@@ -104,52 +105,85 @@ inline uint32_t swz_host(bool c64, uint32_t i) {
   return i ^ (h & 7u);
 }
 
+// Complex scalar helpers for the host-side factor bookkeeping.
+struct Cx { double re, im; };
+inline Cx cxmul(Cx a, Cx b) { return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
+inline Cx cxdiv(Cx a, Cx b) {
+  const double d = b.re * b.re + b.im * b.im;
+  return {(a.re * b.re + a.im * b.im) / d, (a.im * b.re - a.re * b.im) / d};
+}
+inline double cxabs(Cx a) { return std::sqrt(a.re * a.re + a.im * a.im); }
+
 struct Emitter {
   std::ostringstream o;
   bool c64;
   std::string V, R;
   explicit Emitter(bool c64_) : c64(c64_), V(c64_ ? "float2" : "double2"), R(c64_ ? "float" : "double") {}
 
-  std::string cx(const double* m, int r, int c) {   // complex entry literal
-    return "ptg::mk((" + V + "*)0, " + hexd(m[2 * (4 * r + c)]) + ", " + hexd(m[2 * (4 * r + c) + 1]) + ")";
-  }
-  std::string rl(const double* m, int r, int c) { return "(" + R + ")" + hexd(m[2 * (4 * r + c)]); }
+  std::string lit(double re, double im) { return "ptg::mk((" + V + "*)0, " + hexd(re) + ", " + hexd(im) + ")"; }
+  std::string cx(const double* m, int r, int c) { return lit(m[2 * (4 * r + c)], m[2 * (4 * r + c) + 1]); }
+  std::string rl(double v) { return "(" + R + ")" + hexd(v); }
+  static Cx at(const double* m, int r, int c) { return {m[2 * (4 * r + c)], m[2 * (4 * r + c) + 1]}; }
 
-  void op(int kind, int k0, int k1, const double* m) {
+  // Phase-only multiply of the amplitudes whose bit K is 1 (literal ±1, ±i specialised).
+  void phase(int k, Cx d) {
+    if (d.re == 1.0 && d.im == 0.0) return;
+    if (d.im == 0.0 && d.re == -1.0) { o << "ptg::g1neg<" << k << ">(a);\n"; return; }
+    if (d.re == 0.0 && d.im == 1.0) { o << "ptg::g1pi<" << k << ">(a, false);\n"; return; }
+    if (d.re == 0.0 && d.im == -1.0) { o << "ptg::g1pi<" << k << ">(a, true);\n"; return; }
+    o << "ptg::g1p<" << k << ">(a, " << lit(d.re, d.im) << ");\n";
+  }
+
+  // Emit one gate.  With `scaled`, a factor f is pulled out of the matrix
+  // (M = f * M', M' applied) and returned; otherwise f = 1.
+  Cx op(int kind, int k0, int k1, const double* m, bool scaled) {
     switch (kind) {
-      case 1:  // MK_REAL1
-        o << "ptg::g1r<" << k0 << ">(a, " << rl(m, 0, 0) << ", " << rl(m, 0, 1) << ", " << rl(m, 1, 0) << ", "
-          << rl(m, 1, 1) << ");\n";
-        break;
-      case 2:  // MK_DIAG1
+      case 1: {  // MK_REAL1
+        double a = m[0], b = m[2], c = m[8], d = m[10];
+        double f = 1.0;
+        if (scaled) { f = std::fabs(a) >= std::fabs(b) ? a : b; a /= f; b /= f; c /= f; d /= f; }
+        o << "ptg::g1r<" << k0 << ">(a, " << rl(a) << ", " << rl(b) << ", " << rl(c) << ", " << rl(d) << ");\n";
+        return {f, 0.0};
+      }
+      case 2: {  // MK_DIAG1
+        const Cx d0 = at(m, 0, 0), d1 = at(m, 1, 1);
+        if (scaled && cxabs(d0) > 0.0) {
+          phase(k0, cxdiv(d1, d0));
+          return d0;
+        }
         o << "ptg::g1d<" << k0 << ">(a, " << cx(m, 0, 0) << ", " << cx(m, 1, 1) << ");\n";
-        break;
+        return {1.0, 0.0};
+      }
       case 3:  // MK_PHASE1
-        o << "ptg::g1p<" << k0 << ">(a, " << cx(m, 1, 1) << ");\n";
-        break;
+        phase(k0, at(m, 1, 1));
+        return {1.0, 0.0};
       case 4: {  // MK_ANTI1
         const bool x = m[2] == 1.0 && m[3] == 0.0 && m[8] == 1.0 && m[9] == 0.0;
         if (x) o << "ptg::g1x<" << k0 << ">(a);\n";
         else o << "ptg::g1a<" << k0 << ">(a, " << cx(m, 0, 1) << ", " << cx(m, 1, 0) << ");\n";
-        break;
+        return {1.0, 0.0};
       }
       case 8: {  // MK_GEN2
         o << "{ const " << V << " m_[16] = {";
         for (int r = 0; r < 4; ++r)
           for (int c = 0; c < 4; ++c) o << cx(m, r, c) << (r * 4 + c < 15 ? ", " : "");
         o << "}; ptg::g2<" << k0 << ", " << k1 << ">(a, m_); }\n";
-        break;
+        return {1.0, 0.0};
       }
-      case 9: o << "ptg::g2cx<" << k0 << ", " << k1 << ">(a);\n"; break;
-      case 10: o << "ptg::g2sw<" << k0 << ", " << k1 << ">(a);\n"; break;
-      case 11:
-        o << "ptg::g2d<" << k0 << ", " << k1 << ">(a, " << cx(m, 0, 0) << ", " << cx(m, 1, 1) << ", " << cx(m, 2, 2)
-          << ", " << cx(m, 3, 3) << ");\n";
-        break;
+      case 9: o << "ptg::g2cx<" << k0 << ", " << k1 << ">(a);\n"; return {1.0, 0.0};
+      case 10: o << "ptg::g2sw<" << k0 << ", " << k1 << ">(a);\n"; return {1.0, 0.0};
+      case 11: {  // MK_DIAG2: multiply only the entries that are not exactly 1
+        for (int s = 0; s < 4; ++s) {
+          const Cx d = at(m, s, s);
+          if (d.re == 1.0 && d.im == 0.0) continue;
+          o << "ptg::g2dsel<" << k0 << ", " << k1 << ", " << s << ">(a, " << lit(d.re, d.im) << ");\n";
+        }
+        return {1.0, 0.0};
+      }
       default:  // MK_GEN1
         o << "ptg::g1<" << k0 << ">(a, " << cx(m, 0, 0) << ", " << cx(m, 0, 1) << ", " << cx(m, 1, 0) << ", "
           << cx(m, 1, 1) << ");\n";
-        break;
+        return {1.0, 0.0};
     }
   }
 };
@@ -191,25 +225,43 @@ inline std::string scatter_fn(uint64_t mask, const char* arg_type) {
   return o.str();
 }
 
+// Factor bookkeeping (fast path): each scaled gate applies M/f; per phase the
+// product F_ph is what the rare interpreter path must divide out, per pass the
+// magnitude |F| is multiplied back before the tile is stored, and the phase
+// arg(F) of every pass is folded into the initial |0...0> amplitude G, so the
+// stored state equals the true state after every pass.  Passes holding
+// renormalising (general) sites are never scaled: their per-site norms must
+// be measured in the true frame.
 inline std::string generate(const GenProgram& P) {
   Emitter e(P.c64);
   std::ostringstream& o = e.o;
-  o << kGenPrelude << "\n";
+  std::ostringstream body;
+  Cx G{1.0, 0.0};
+  std::vector<std::string> kernels;
   for (size_t pi = 0; pi < P.passes.size(); ++pi) {
     const GenPass& gp = P.passes[pi];
+    bool has_general = false;
+    for (const DevOp& op : gp.ops)
+      if (op.kind == 1 && P.chans[P.site_chan[op.ref]].general) has_general = true;
+    const bool scaled = !has_general;
     const int threads = std::max(32, 1 << (gp.L - 4));
+    const bool all_active = threads == (1 << (gp.L - 4));
     const uint64_t nmask = P.n >= 64 ? ~0ull : ((1ull << P.n) - 1);
     const uint64_t comp = ~gp.qmask & nmask;
     const uint64_t hmask = gp.qmask & ~((1ull << gp.c) - 1);
-    o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << (threads <= 256 ? 2 : 1) << ") "
+    Emitter ke(P.c64);   // kernel text; G is only known after every pass is emitted
+    std::ostringstream& k = ke.o;
+    Cx F{1.0, 0.0};
+    k << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << (threads <= 256 ? 2 : 1) << ") "
       << kernel_name((int)pi) << "(const ptg::PassParams p) {\n"
-      << "  typedef " << e.V << " V;\n"
-      << "  ptg::run_pass<" << e.R << ", " << gp.L << ", " << gp.c << ", " << (P.n - gp.L) << ">(p,\n"
+      << "  typedef " << ke.V << " V;\n"
+      << "  ptg::run_pass<" << ke.R << ", " << gp.L << ", " << gp.c << ", " << (P.n - gp.L) << ">(p,\n"
       << "    " << scatter_fn(comp, "uint64_t") << ",\n"
       << "    " << scatter_fn(hmask, "uint32_t") << ",\n"
       << "    [&](V* cur, int b, const uint8_t* sel, long long tile, uint64_t base, double scale, double* red) {\n"
       << "    const uint32_t g = threadIdx.x;\n"
-      << "    const bool active = g < " << (1u << (gp.L - 4)) << "u;\n"
+      << "    const bool active = " << (all_active ? std::string("true") : "g < " + std::to_string(1u << (gp.L - 4)) + "u")
+      << ";\n"
       << "    V a[16];\n";
     for (size_t ph = 0; ph < gp.phases.size(); ++ph) {
       const DevPhase& D = gp.phases[ph];
@@ -218,48 +270,49 @@ inline std::string generate(const GenProgram& P) {
       uint32_t off[16], so[16];
       for (int j = 0; j < 16; ++j) {
         off[j] = 0;
-        for (int k = 0; k < 4; ++k)
-          if ((j >> k) & 1) off[j] |= 1u << pb[k];
+        for (int q = 0; q < 4; ++q)
+          if ((j >> q) & 1) off[j] |= 1u << pb[q];
         so[j] = swz_host(P.c64, off[j]);
       }
-      o << "    { // phase " << ph << "\n"
+      k << "    { // phase " << ph << "\n"
         << "      const uint32_t gb = ptg::ins0(ptg::ins0(ptg::ins0(ptg::ins0(g, " << pb[0] << "), " << pb[1] << "), "
         << pb[2] << "), " << pb[3] << ");\n"
         << "      const uint32_t sg = ptg::swz((V*)0, gb);\n"
         << "      const uint32_t so[16] = {";
-      for (int j = 0; j < 16; ++j) o << so[j] << "u" << (j < 15 ? ", " : "");
-      o << "};\n";
+      for (int j = 0; j < 16; ++j) k << so[j] << "u" << (j < 15 ? ", " : "");
+      k << "};\n";
       if (ph == 0) {
-        o << "      const uint32_t off[16] = {";
-        for (int j = 0; j < 16; ++j) o << off[j] << "u" << (j < 15 ? ", " : "");
-        o << "};\n"
-          << "      if (p.gen_zero) ptg::zero16(a, base, gb, off, active);\n"
+        k << "      const uint32_t off[16] = {";
+        for (int j = 0; j < 16; ++j) k << off[j] << "u" << (j < 15 ? ", " : "");
+        k << "};\n"
+          << "      if (p.gen_zero) ptg::zero16(a, base, gb, off, active, GZERO_RE, GZERO_IM);\n"
           << "      else ptg::ld16<V, " << pb[0] << ">(a, cur, sg, so, active, scale);\n";
+        if (pi == 0)   // a loaded (not synthesized) input also needs the global phase G
+          k << "      if (!p.gen_zero) ptg::cscale16(a, ptg::mk((V*)0, GZERO_RE, GZERO_IM));\n";
       } else {
-        o << "      ptg::ld16<V, " << pb[0] << ">(a, cur, sg, so, active, 1.0);\n";
+        k << "      ptg::ld16<V, " << pb[0] << ">(a, cur, sg, so, active, 1.0);\n";
       }
-      // CTA-uniform: does this trajectory take any non-default outcome in this phase?
       std::ostringstream err;
-      for (int k = D.op_begin; k < D.op_begin + D.n_ops; ++k)
-        if (gp.ops[k].kind == 1) err << (err.tellp() > 0 ? " | " : "") << "sel[" << gp.ops[k].ref << "]";
+      for (int q = D.op_begin; q < D.op_begin + D.n_ops; ++q)
+        if (gp.ops[q].kind == 1) err << (err.tellp() > 0 ? " | " : "") << "sel[" << gp.ops[q].ref << "]";
       const bool has_sites = err.tellp() > 0;
-      if (has_sites) o << "      if ((" << err.str() << ") == 0) {\n";
-      // fast path: every site at its default outcome -> straight-line gates only
-      for (int k = D.op_begin; k < D.op_begin + D.n_ops; ++k) {
-        const DevOp& op = gp.ops[k];
+      if (has_sites) k << "      if ((" << err.str() << ") == 0) {\n";
+      Cx Fph{1.0, 0.0};
+      for (int q = D.op_begin; q < D.op_begin + D.n_ops; ++q) {
+        const DevOp& op = gp.ops[q];
         const int k1 = op.arity == 2 ? op.k1 : 0;
         if (op.kind == 0) {
-          o << "      ";
-          e.op(P.kinds[op.ref], op.k0, k1, P.mats + (size_t)op.ref * 32);
+          k << "      ";
+          Fph = cxmul(Fph, ke.op(P.kinds[op.ref], op.k0, k1, P.mats + (size_t)op.ref * 32, scaled));
           continue;
         }
         const ptsbe_channel& ch = P.chans[P.site_chan[op.ref]];
         if (!(ch.identity_mask & 1ull)) {   // outcome 0 is not the identity (e.g. damping K0)
-          o << "      ";
-          e.op(P.kinds[ch.mat_base], op.k0, k1, P.mats + (size_t)ch.mat_base * 32);
+          k << "      ";
+          ke.op(P.kinds[ch.mat_base], op.k0, k1, P.mats + (size_t)ch.mat_base * 32, false);
         }
         if (ch.general) {
-          o << "      { double s_ = 0.0;\n"
+          k << "      { double s_ = 0.0;\n"
             << "#pragma unroll\n"
             << "        for (int j = 0; j < 16; ++j) s_ += ptg::prob64(a[j]);\n"
             << "        s_ = ptg::block_sum(s_, red);\n"
@@ -268,20 +321,33 @@ inline std::string generate(const GenProgram& P) {
         }
       }
       if (has_sites) {
-        // rare path: run the phase through the run-time interpreter on shared memory
-        o << "      } else {\n"
+        const Cx inv = cxdiv(Cx{1.0, 0.0}, Fph);
+        k << "      } else {\n"
           << "        ptg::st16<V, " << pb[0] << ">(a, cur, sg, so, active);\n"
           << "        const uint32_t sb_[4] = {so[1], so[2], so[4], so[8]};\n"
           << "        ptg::interp_phase<V>(cur, sg, sb_, p, " << ph << ", sel, b, tile, red, active);\n"
-          << "        ptg::ld16<V, " << pb[0] << ">(a, cur, sg, so, active, 1.0);\n"
-          << "      }\n";
+          << "        ptg::ld16<V, " << pb[0] << ">(a, cur, sg, so, active, 1.0);\n";
+        if (!(inv.re == 1.0 && inv.im == 0.0))   // match the fast path's frame
+          k << "        ptg::cscale16(a, " << ke.lit(inv.re, inv.im) << ");\n";
+        k << "      }\n";
       }
-      o << "      ptg::st16<V, " << pb[0] << ">(a, cur, sg, so, active);\n"
+      F = cxmul(F, Fph);
+      if (ph + 1 == gp.phases.size()) {
+        const double mag = cxabs(F);
+        if (mag != 1.0) k << "      ptg::rscale16(a, " << hexd(mag) << ");\n";
+      }
+      k << "      ptg::st16<V, " << pb[0] << ">(a, cur, sg, so, active);\n"
         << "      __syncthreads();\n"
         << "    }\n";
     }
-    o << "  });\n}\n";
+    k << "  });\n}\n";
+    const double mag = cxabs(F);
+    G = cxmul(G, Cx{F.re / mag, F.im / mag});
+    kernels.push_back(k.str());
   }
+  o << kGenPrelude << "\n"
+    << "#define GZERO_RE " << hexd(G.re) << "\n#define GZERO_IM " << hexd(G.im) << "\n";
+  for (auto& kt : kernels) o << kt;
   return o.str();
 }
 

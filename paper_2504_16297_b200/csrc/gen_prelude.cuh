@@ -135,6 +135,35 @@ template <int KH, int KL, typename V> __device__ __forceinline__ void g2d(V* a, 
   }
 }
 
+template <int K, typename V> __device__ __forceinline__ void g1neg(V* a) {    // diag(1, -1)
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (j & (1 << K)) { a[j].x = -a[j].x; a[j].y = -a[j].y; }
+}
+template <int K, typename V> __device__ __forceinline__ void g1pi(V* a, bool neg) {   // diag(1, ±i)
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (j & (1 << K)) {
+      const V x = a[j];
+      if (neg) { a[j].x = x.y; a[j].y = -x.x; } else { a[j].x = -x.y; a[j].y = x.x; }
+    }
+}
+template <int KH, int KL, int S, typename V> __device__ __forceinline__ void g2dsel(V* a, V d) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (((j >> KH) & 1) * 2 + ((j >> KL) & 1) == S) a[j] = cmul(d, a[j]);
+}
+template <typename V> __device__ __forceinline__ void cscale16(V* a, V d) {
+#pragma unroll
+  for (int j = 0; j < 16; ++j) a[j] = cmul(d, a[j]);
+}
+template <typename V> __device__ __forceinline__ void rscale16(V* a, double s) {
+  typedef decltype(a[0].x) R;
+  const R sc = (R)s;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) { a[j].x *= sc; a[j].y *= sc; }
+}
+
 // ---- interpreter for the rare phases in which a trajectory has a non-default
 // outcome.  The thread's 16-amplitude group is parked in shared memory (its
 // own slots only, so no barrier is needed between ops) and every op of the
@@ -292,9 +321,14 @@ __device__ __forceinline__ void st16(const V* a, V* cur, uint32_t sg, const uint
   }
 }
 template <typename V>
-__device__ __forceinline__ void zero16(V* a, uint64_t base, uint32_t gb, const uint32_t* off, bool active) {
+__device__ __forceinline__ void zero16(V* a, uint64_t base, uint32_t gb, const uint32_t* off, bool active,
+                                       double g_re = 1.0, double g_im = 0.0) {
+  // |0...0> times the program's accumulated global phase G (see codegen.h)
 #pragma unroll
-  for (int j = 0; j < 16; ++j) a[j] = mk((V*)0, (active && base == 0 && (gb | off[j]) == 0) ? 1.0 : 0.0, 0.0);
+  for (int j = 0; j < 16; ++j) {
+    const bool one = active && base == 0 && (gb | off[j]) == 0;
+    a[j] = mk((V*)0, one ? g_re : 0.0, one ? g_im : 0.0);
+  }
 }
 
 // Persistent, double-buffered tile loop shared by every generated pass kernel.
