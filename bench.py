@@ -190,7 +190,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=CONFIG)
-    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
     ap.add_argument("--seed", type=int, default=2024)
     ap.add_argument("--no-cpu", action="store_true")
@@ -274,7 +274,7 @@ def main():
         e1.record(stream)
         barrier()
     launches = eng.launches - l0
-    pass_ms, pass_n = eng.profile_read()
+    pass_ms, pass_n, pass_bytes = eng.profile_read()
     eng.profile(False)
     ms = max_over_ranks(e0.elapsed_time(e1))
     total_traj = K * B * world
@@ -304,7 +304,9 @@ def main():
         return
     hbm, peak_kind = peaks()
     amp = 8 if args.dtype == "c64" else 16
-    bytes_per_launch = 2 * B * (1 << c.n_qubits) * amp
+    # algorithmic bytes: one read + one write of every state each pass launch processes
+    # (2 * E * 2^n * s; E = trajectories + shared trunk in the launch), summed by the engine
+    bytes_per_launch = pass_bytes / max(pass_n, 1)
     avg_launch_ms = pass_ms / max(pass_n, 1)
     achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,

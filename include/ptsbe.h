@@ -165,6 +165,9 @@ int ptsbe_last_error(ptsbe_engine* h, char* buf, size_t len);
  * returns the accumulated kernel milliseconds and launch count. */
 int ptsbe_profile(ptsbe_engine* h, int enable);
 int ptsbe_profile_read(ptsbe_engine* h, double* total_ms, int64_t* launches);
+/* Algorithmic bytes (one read + one write of every state a launch processes)
+ * of the pass launches profiled since ptsbe_profile(h, 1). */
+double ptsbe_profile_bytes(ptsbe_engine* h);
 /* Kernel launches issued by this handle since creation (for bench gpu_launches). */
 int64_t ptsbe_launch_count(ptsbe_engine* h);
 

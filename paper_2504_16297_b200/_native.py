@@ -77,6 +77,7 @@ SIGNATURES = {
     "ptsbe_launch_count": (C.c_int64, [C.c_void_p]),
     "ptsbe_profile": (C.c_int, [C.c_void_p, C.c_int]),
     "ptsbe_profile_read": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+    "ptsbe_profile_bytes": (C.c_double, [C.c_void_p]),
 }
 
 _lib = None

@@ -7,8 +7,10 @@
 // calls with compile-time register positions and literal matrix entries
 // (hex-float, so c128 stays bit-identical to the operator table and c64 gets
 // exactly the host's float rounding); cx / swap / x compile to register
-// renaming.  Noise sites stay data-driven: one CTA-uniform test of the
-// trajectory's outcome per site.
+// renaming.  Noise sites stay data-driven: per phase, one CTA-uniform bit says
+// whether the trajectory takes any non-default outcome there; if so the phase
+// runs through a run-time interpreter (rare), otherwise through the
+// straight-line fast path.
 //
 // NVRTC and the driver API are reached without link-time dependencies
 // (dlopen + cudaGetDriverEntryPoint), so libptsbe.so still loads on hosts
@@ -85,11 +87,6 @@ inline Api& api() {
 }
 
 // ---------------------------------------------------------------- source generation
-struct OpMat {            // one concrete operator: kind + 4x4 complex (row-major, padded)
-  int kind;
-  const double* m;        // 32 doubles
-};
-
 inline std::string hexd(double v) {
   char b[64];
   std::snprintf(b, sizeof b, "%a", v);
@@ -127,7 +124,7 @@ struct Emitter {
 
   // Phase-only multiply of the amplitudes whose bit K is 1 (literal ±1, ±i specialised).
   void phase(int k, Cx d) {
-    if (d.re == 1.0 && d.im == 0.0) return;
+    if (d.re == 1.0 && d.im == 0.0) { o << "\n"; return; }
     if (d.im == 0.0 && d.re == -1.0) { o << "ptg::g1neg<" << k << ">(a);\n"; return; }
     if (d.re == 0.0 && d.im == 1.0) { o << "ptg::g1pi<" << k << ">(a, false);\n"; return; }
     if (d.re == 0.0 && d.im == -1.0) { o << "ptg::g1pi<" << k << ">(a, true);\n"; return; }
@@ -173,10 +170,11 @@ struct Emitter {
       case 9: o << "ptg::g2cx<" << k0 << ", " << k1 << ">(a);\n"; return {1.0, 0.0};
       case 10: o << "ptg::g2sw<" << k0 << ", " << k1 << ">(a);\n"; return {1.0, 0.0};
       case 11: {  // MK_DIAG2: multiply only the entries that are not exactly 1
+        o << "\n";
         for (int s = 0; s < 4; ++s) {
           const Cx d = at(m, s, s);
           if (d.re == 1.0 && d.im == 0.0) continue;
-          o << "ptg::g2dsel<" << k0 << ", " << k1 << ", " << s << ">(a, " << lit(d.re, d.im) << ");\n";
+          o << "      ptg::g2dsel<" << k0 << ", " << k1 << ", " << s << ">(a, " << lit(d.re, d.im) << ");\n";
         }
         return {1.0, 0.0};
       }
@@ -191,13 +189,14 @@ struct Emitter {
 struct GenPass {
   int L, c;
   uint64_t qmask;
-  std::vector<DevPhase> phases;
-  std::vector<DevOp> ops;   // phase-major, k0/k1 filled
+  std::vector<DevPhase> phases;   // pbits: GB positions, 5 bits each
+  std::vector<DevOp> ops;         // phase-major, k0/k1 filled
 };
 
 struct GenProgram {
   bool c64;
   int n;
+  int gb;                   // register bits per phase (4 or 5)
   const double* mats;       // n_mats x 32 doubles
   const int32_t* kinds;     // n_mats
   const ptsbe_channel* chans;
@@ -206,6 +205,8 @@ struct GenProgram {
 };
 
 inline std::string kernel_name(int pass) { return "ptsbe_pass_" + std::to_string(pass); }
+
+inline int threads_for(int L, int gb) { return std::max(32, 1 << (L - gb)); }
 
 // Lambda scattering the low bits of x onto the set bits of `mask` (PDEP as shift/mask runs).
 inline std::string scatter_fn(uint64_t mask, const char* arg_type) {
@@ -225,6 +226,23 @@ inline std::string scatter_fn(uint64_t mask, const char* arg_type) {
   return o.str();
 }
 
+// Per-trajectory bitmask, evaluated once per CTA when the trajectory changes:
+// bit ph set iff some site of phase ph takes a non-default outcome (phases past
+// 63 share bit 63, which then sends all of them down the exact slow path).
+inline std::string err_mask_fn(const GenPass& gp) {
+  std::ostringstream o;
+  o << "[](const uint8_t* sel) -> uint64_t { uint64_t m_ = 0;";
+  for (size_t ph = 0; ph < gp.phases.size(); ++ph) {
+    const DevPhase& D = gp.phases[ph];
+    std::ostringstream e;
+    for (int q = D.op_begin; q < D.op_begin + D.n_ops; ++q)
+      if (gp.ops[q].kind == 1) e << (e.tellp() > 0 ? " | " : "") << "sel[" << gp.ops[q].ref << "]";
+    if (e.tellp() > 0) o << " m_ |= (uint64_t)((" << e.str() << ") != 0) << " << std::min<size_t>(ph, 63) << ";";
+  }
+  o << " return m_; }";
+  return o.str();
+}
+
 // Factor bookkeeping (fast path): each scaled gate applies M/f; per phase the
 // product F_ph is what the rare interpreter path must divide out, per pass the
 // magnitude |F| is multiplied back before the tile is stored, and the phase
@@ -233,9 +251,8 @@ inline std::string scatter_fn(uint64_t mask, const char* arg_type) {
 // renormalising (general) sites are never scaled: their per-site norms must
 // be measured in the true frame.
 inline std::string generate(const GenProgram& P) {
-  Emitter e(P.c64);
-  std::ostringstream& o = e.o;
-  std::ostringstream body;
+  const int GB = P.gb, N = 1 << GB;
+  std::ostringstream o;
   Cx G{1.0, 0.0};
   std::vector<std::string> kernels;
   for (size_t pi = 0; pi < P.passes.size(); ++pi) {
@@ -244,59 +261,61 @@ inline std::string generate(const GenProgram& P) {
     for (const DevOp& op : gp.ops)
       if (op.kind == 1 && P.chans[P.site_chan[op.ref]].general) has_general = true;
     const bool scaled = !has_general;
-    const int threads = std::max(32, 1 << (gp.L - 4));
-    const bool all_active = threads == (1 << (gp.L - 4));
+    const int threads = threads_for(gp.L, GB);
+    const bool all_active = threads == (1 << (gp.L - GB));
+    const int min_blocks = threads <= 128 ? 3 : (threads <= 256 ? 2 : 1);
     const uint64_t nmask = P.n >= 64 ? ~0ull : ((1ull << P.n) - 1);
     const uint64_t comp = ~gp.qmask & nmask;
     const uint64_t hmask = gp.qmask & ~((1ull << gp.c) - 1);
-    Emitter ke(P.c64);   // kernel text; G is only known after every pass is emitted
+    Emitter ke(P.c64);
     std::ostringstream& k = ke.o;
     Cx F{1.0, 0.0};
-    k << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << (threads <= 256 ? 2 : 1) << ") "
+    k << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << min_blocks << ") "
       << kernel_name((int)pi) << "(const ptg::PassParams p) {\n"
       << "  typedef " << ke.V << " V;\n"
-      << "  ptg::run_pass<" << ke.R << ", " << gp.L << ", " << gp.c << ", " << (P.n - gp.L) << ">(p,\n"
+      << "  ptg::run_pass<" << ke.R << ", " << gp.L << ", " << gp.c << ", " << (P.n - gp.L) << ", " << threads
+      << ">(p,\n"
       << "    " << scatter_fn(comp, "uint64_t") << ",\n"
       << "    " << scatter_fn(hmask, "uint32_t") << ",\n"
-      << "    [&](V* cur, int b, const uint8_t* sel, long long tile, uint64_t base, double scale, double* red) {\n"
+      << "    " << err_mask_fn(gp) << ",\n"
+      << "    [&](V* cur, int b, const uint8_t* sel, long long tile, uint64_t base, double scale, double* red,\n"
+      << "        uint64_t emask) {\n"
       << "    const uint32_t g = threadIdx.x;\n"
-      << "    const bool active = " << (all_active ? std::string("true") : "g < " + std::to_string(1u << (gp.L - 4)) + "u")
-      << ";\n"
-      << "    V a[16];\n";
+      << "    const bool active = "
+      << (all_active ? std::string("true") : "g < " + std::to_string(1u << (gp.L - GB)) + "u") << ";\n"
+      << "    V a[" << N << "];\n";
     for (size_t ph = 0; ph < gp.phases.size(); ++ph) {
       const DevPhase& D = gp.phases[ph];
-      const int pb[4] = {(int)(D.pbits & 31), (int)((D.pbits >> 5) & 31), (int)((D.pbits >> 10) & 31),
-                         (int)((D.pbits >> 15) & 31)};
-      uint32_t off[16], so[16];
-      for (int j = 0; j < 16; ++j) {
+      int pb[5];
+      for (int q = 0; q < GB; ++q) pb[q] = (int)((D.pbits >> (5 * q)) & 31);
+      std::vector<uint32_t> off(N), so(N);
+      for (int j = 0; j < N; ++j) {
         off[j] = 0;
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < GB; ++q)
           if ((j >> q) & 1) off[j] |= 1u << pb[q];
         so[j] = swz_host(P.c64, off[j]);
       }
-      k << "    { // phase " << ph << "\n"
-        << "      const uint32_t gb = ptg::ins0(ptg::ins0(ptg::ins0(ptg::ins0(g, " << pb[0] << "), " << pb[1] << "), "
-        << pb[2] << "), " << pb[3] << ");\n"
-        << "      const uint32_t sg = ptg::swz((V*)0, gb);\n"
-        << "      const uint32_t so[16] = {";
-      for (int j = 0; j < 16; ++j) k << so[j] << "u" << (j < 15 ? ", " : "");
+      k << "    { // phase " << ph << "\n      const uint32_t gb = ";
+      for (int q = 0; q < GB; ++q) k << "ptg::ins0(";
+      k << "g";
+      for (int q = 0; q < GB; ++q) k << ", " << pb[q] << ")";
+      k << ";\n      const uint32_t sg = ptg::swz((V*)0, gb);\n      const uint32_t so[" << N << "] = {";
+      for (int j = 0; j < N; ++j) k << so[j] << "u" << (j + 1 < N ? ", " : "");
       k << "};\n";
       if (ph == 0) {
-        k << "      const uint32_t off[16] = {";
-        for (int j = 0; j < 16; ++j) k << off[j] << "u" << (j < 15 ? ", " : "");
+        k << "      const uint32_t off[" << N << "] = {";
+        for (int j = 0; j < N; ++j) k << off[j] << "u" << (j + 1 < N ? ", " : "");
         k << "};\n"
-          << "      if (p.gen_zero) ptg::zero16(a, base, gb, off, active, GZERO_RE, GZERO_IM);\n"
-          << "      else ptg::ld16<V, " << pb[0] << ">(a, cur, sg, so, active, scale);\n";
+          << "      if (p.gen_zero) ptg::zerog(a, base, gb, off, active, GZERO_RE, GZERO_IM);\n"
+          << "      else ptg::ldg<V, " << N << ", " << pb[0] << ">(a, cur, sg, so, active, scale);\n";
         if (pi == 0)   // a loaded (not synthesized) input also needs the global phase G
-          k << "      if (!p.gen_zero) ptg::cscale16(a, ptg::mk((V*)0, GZERO_RE, GZERO_IM));\n";
+          k << "      if (!p.gen_zero) ptg::cscale(a, ptg::mk((V*)0, GZERO_RE, GZERO_IM));\n";
       } else {
-        k << "      ptg::ld16<V, " << pb[0] << ">(a, cur, sg, so, active, 1.0);\n";
+        k << "      ptg::ldg<V, " << N << ", " << pb[0] << ">(a, cur, sg, so, active, 1.0);\n";
       }
-      std::ostringstream err;
-      for (int q = D.op_begin; q < D.op_begin + D.n_ops; ++q)
-        if (gp.ops[q].kind == 1) err << (err.tellp() > 0 ? " | " : "") << "sel[" << gp.ops[q].ref << "]";
-      const bool has_sites = err.tellp() > 0;
-      if (has_sites) k << "      if ((" << err.str() << ") == 0) {\n";
+      bool has_sites = false;
+      for (int q = D.op_begin; q < D.op_begin + D.n_ops; ++q) has_sites = has_sites || gp.ops[q].kind == 1;
+      if (has_sites) k << "      if (!((emask >> " << std::min<size_t>(ph, 63) << ") & 1ull)) {\n";
       Cx Fph{1.0, 0.0};
       for (int q = D.op_begin; q < D.op_begin + D.n_ops; ++q) {
         const DevOp& op = gp.ops[q];
@@ -314,7 +333,7 @@ inline std::string generate(const GenProgram& P) {
         if (ch.general) {
           k << "      { double s_ = 0.0;\n"
             << "#pragma unroll\n"
-            << "        for (int j = 0; j < 16; ++j) s_ += ptg::prob64(a[j]);\n"
+            << "        for (int j = 0; j < " << N << "; ++j) s_ += ptg::prob64(a[j]);\n"
             << "        s_ = ptg::block_sum(s_, red);\n"
             << "        if (threadIdx.x == 0) p.partials[((size_t)" << op.slot
             << " * p.B + b) * p.tiles + tile] = s_; }\n";
@@ -323,20 +342,22 @@ inline std::string generate(const GenProgram& P) {
       if (has_sites) {
         const Cx inv = cxdiv(Cx{1.0, 0.0}, Fph);
         k << "      } else {\n"
-          << "        ptg::st16<V, " << pb[0] << ">(a, cur, sg, so, active);\n"
-          << "        const uint32_t sb_[4] = {so[1], so[2], so[4], so[8]};\n"
-          << "        ptg::interp_phase<V>(cur, sg, sb_, p, " << ph << ", sel, b, tile, red, active);\n"
-          << "        ptg::ld16<V, " << pb[0] << ">(a, cur, sg, so, active, 1.0);\n";
+          << "        ptg::stg<V, " << N << ", " << pb[0] << ">(a, cur, sg, so, active);\n"
+          << "        const uint32_t sb_[" << GB << "] = {";
+        for (int q = 0; q < GB; ++q) k << "so[" << (1 << q) << "]" << (q + 1 < GB ? ", " : "");
+        k << "};\n"
+          << "        ptg::interp_phase<V>(cur, sg, sb_, " << GB << ", p, " << ph << ", sel, b, tile, red, active);\n"
+          << "        ptg::ldg<V, " << N << ", " << pb[0] << ">(a, cur, sg, so, active, 1.0);\n";
         if (!(inv.re == 1.0 && inv.im == 0.0))   // match the fast path's frame
-          k << "        ptg::cscale16(a, " << ke.lit(inv.re, inv.im) << ");\n";
+          k << "        ptg::cscale(a, " << ke.lit(inv.re, inv.im) << ");\n";
         k << "      }\n";
       }
       F = cxmul(F, Fph);
       if (ph + 1 == gp.phases.size()) {
         const double mag = cxabs(F);
-        if (mag != 1.0) k << "      ptg::rscale16(a, " << hexd(mag) << ");\n";
+        if (mag != 1.0) k << "      ptg::rscale(a, " << hexd(mag) << ");\n";
       }
-      k << "      ptg::st16<V, " << pb[0] << ">(a, cur, sg, so, active);\n"
+      k << "      ptg::stg<V, " << N << ", " << pb[0] << ">(a, cur, sg, so, active);\n"
         << "      __syncthreads();\n"
         << "    }\n";
     }
@@ -398,7 +419,7 @@ inline bool compile(const std::string& src, int n_passes, int dev, Module& out, 
 }
 
 inline size_t smem_bytes(int L, int /*c*/, size_t amp_bytes) {
-  return 2 * ((size_t)1 << L) * amp_bytes + 32 * 8;
+  return 2 * ((size_t)1 << L) * amp_bytes + 32 * 8 + 16;   // tiles | red | emask
 }
 
 }  // namespace gen

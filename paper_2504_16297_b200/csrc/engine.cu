@@ -50,6 +50,7 @@ struct ptsbe_engine {
   DevPhase* d_phases = nullptr;
   int32_t* d_matkind = nullptr;
   int n_phases_total = 0;
+  int phase_bits = 4;              // register bits per phase (4, or 5 for c64 codegen)
   // circuit-specialised kernels (codegen.h); generic pass_kernel when off
   bool gen_active = false;
   std::string gen_note;
@@ -79,6 +80,17 @@ struct ptsbe_engine {
   size_t chunk_cap = 0;
   uint64_t* d_chunks = nullptr;
   long long launches = 0;
+  // shared-trunk schedule (launch_passes): host copy of the batch's outcome table,
+  // pass index of every site, per-pass launch entries and fork lists
+  bool tree_enabled = true;
+  std::vector<uint8_t> host_sel;
+  std::vector<int> site_pass;
+  long long last_entries = 0;
+  int4* d_ent = nullptr;
+  size_t ent_cap = 0;
+  int32_t* d_forks = nullptr;
+  size_t fork_cap = 0;
+  double pass_bytes_total = 0.0;   // algorithmic bytes of profiled pass launches
   // physical layout: logical qubit q stored at physical bit perm[q] (identity unless permuted)
   bool permuted = false;
   BitPerm layout{};
@@ -163,9 +175,77 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero) {
     h->final_general = false;
     return 0;
   }
+  // Launch entries per pass.  Shared-trunk schedule (fresh |0> batches): every
+  // trajectory equals the noiseless "trunk" until f_t, the first pass in which
+  // it takes a non-default outcome.  The trunk (row cap, slots cap / cap+1
+  // alternating) runs while anybody still needs it; trajectory t forks at pass
+  // f_t by reading the trunk's previous state and writing its own slot, then
+  // evolves alone.  Same kernels, same ops, same inputs: bit-identical to
+  // evolving every trajectory from |0> separately.
+  const int P = (int)h->passes.size();
+  const int trunk = h->cap;
+  std::vector<int> fpass(B, 0);
+  const bool tree = from_zero && P >= 2 && h->tree_enabled && !h->host_sel.empty();
+  if (tree) {
+    for (int b = 0; b < B; ++b) {
+      int f = P - 1;
+      const uint8_t* row = h->host_sel.data() + (size_t)b * h->n_sites;
+      for (int s = 0; s < h->n_sites; ++s)
+        if (row[s] && h->site_pass[s] < f) f = h->site_pass[s];
+      fpass[b] = f;
+    }
+  }
+  std::vector<int4> ents;
+  std::vector<int> ent_begin(P + 1, 0);
+  std::vector<std::vector<int32_t>> forks(P);
+  for (int k = 0; k < P; ++k) {
+    ent_begin[k] = (int)ents.size();
+    bool trunk_needed = false;
+    for (int b = 0; b < B; ++b) {
+      if (!tree) { ents.push_back(make_int4(b, b, b, 0)); continue; }
+      if (fpass[b] < k) ents.push_back(make_int4(b, b, b, 0));
+      else if (fpass[b] == k) {
+        ents.push_back(make_int4(b, k == 0 ? b : trunk + ((k - 1) & 1), b, 0));
+        if (k > 0) forks[k].push_back(b);
+      } else trunk_needed = true;
+    }
+    if (trunk_needed) ents.push_back(make_int4(trunk, k == 0 ? trunk : trunk + ((k - 1) & 1), trunk + (k & 1), 0));
+  }
+  ent_begin[P] = (int)ents.size();
+  h->last_entries = (long long)ents.size();
+  if (ents.size() > h->ent_cap) {
+    if (dalloc(h, &h->d_ent, ents.size())) return PTSBE_ERR_CUDA;
+    h->ent_cap = ents.size();
+  }
+  CK(h, cudaMemcpyAsync(h->d_ent, ents.data(), ents.size() * sizeof(int4), cudaMemcpyHostToDevice, h->stream));
+  if (tree) {
+    std::vector<int32_t> allf;
+    for (int k = 0; k < P; ++k) allf.insert(allf.end(), forks[k].begin(), forks[k].end());
+    if (allf.size() > h->fork_cap) {
+      if (dalloc(h, &h->d_forks, allf.size())) return PTSBE_ERR_CUDA;
+      h->fork_cap = allf.size();
+    }
+    if (!allf.empty())
+      CK(h, cudaMemcpyAsync(h->d_forks, allf.data(), allf.size() * 4, cudaMemcpyHostToDevice, h->stream));
+    // trunk row starts like every trajectory
+    batch_reset<<<1, 32, 0, h->stream>>>(h->d_weight + trunk, h->d_nst + trunk, h->d_status + trunk,
+                                         h->d_fail + trunk, 1);
+    CKL(h);
+  }
+  int fork_off = 0;
   for (size_t pi = 0; pi < h->passes.size(); ++pi) {
     const PassHost& ph = h->passes[pi];
+    const int E = ent_begin[pi + 1] - ent_begin[pi];
+    if (!forks[pi].empty()) {   // forks inherit the trunk's weight / norm / status
+      const int nf = (int)forks[pi].size();
+      fork_rows<<<(nf + 127) / 128, 128, 0, h->stream>>>(h->d_forks + fork_off, nf, trunk, h->d_weight, h->d_nst,
+                                                           h->d_status, h->d_fail);
+      CKL(h);
+      fork_off += nf;
+    }
     PassParams p;
+    p.ent = h->d_ent + ent_begin[pi];
+    p.E = E;
     p.states = h->states;
     p.n = h->n;
     p.L = ph.L;
@@ -186,10 +266,10 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero) {
     p.gen_zero = (pi == 0 && from_zero) ? 1 : 0;
     p.partials = h->d_partials;
     p.status = h->d_status;
-    p.B = B;
+    p.B = h->cap + 1;   // row stride (trajectory rows + trunk row)
     p.tiles = 1ll << (h->n - ph.L);
     const size_t smem = pass_smem(ph, sizeof(typename Cplx<R>::V));
-    dim3 grid((unsigned)p.tiles, (unsigned)B);
+    dim3 grid((unsigned)p.tiles, (unsigned)E);
     if (h->profiling) {
       while ((int)h->ev.size() < h->ev_used + 2) {
         cudaEvent_t e;
@@ -199,12 +279,12 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero) {
       CK(h, cudaEventRecord(h->ev[h->ev_used], h->stream));
     }
     if (h->gen_active) {
-      const unsigned threads = std::max(32u, 1u << (ph.L - 4));
+      const unsigned threads = (unsigned)gen::threads_for(ph.L, h->phase_bits);
       const size_t gsm = gen::smem_bytes(ph.L, ph.c, sizeof(typename Cplx<R>::V));
       CUfunction f = h->gen_mod.fns[pi];
       int per_sm = 0;
       if (gen::api().occupancy(&per_sm, f, (int)threads, gsm) != CUDA_SUCCESS) per_sm = 1;
-      const long long total = (long long)B * p.tiles;
+      const long long total = (long long)E * p.tiles;
       const long long want = (long long)std::max(per_sm, 1) * h->num_sms;
       const unsigned nblk = (unsigned)std::max<long long>(1, std::min(total, want));
       void* args[] = {&p};
@@ -216,7 +296,7 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero) {
       const unsigned threads = std::max(32u, 1u << (ph.L - 4));
       int per_sm = 0;
       CK(h, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pass_kernel<R>, threads, smem));
-      const long long total = (long long)B * p.tiles;
+      const long long total = (long long)E * p.tiles;
       const long long want = (long long)std::max(per_sm, 1) * h->num_sms;
       const unsigned nblk = (unsigned)std::max<long long>(1, std::min(total, want));
       pass_kernel<R><<<nblk, threads, smem, h->stream>>>(p);
@@ -227,12 +307,13 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero) {
     if (h->profiling) {
       CK(h, cudaEventRecord(h->ev[h->ev_used + 1], h->stream));
       h->ev_used += 2;
+      h->pass_bytes_total += 2.0 * E * (double)((size_t)1 << h->n) * (double)h->amp_bytes;
     }
     if (ph.n_slots > 0) {
       (void)per_slot;
-      norm_finalize<<<B, 256, 0, h->stream>>>(h->d_partials, ph.n_slots, B, p.tiles,
+      norm_finalize<<<E, 256, 0, h->stream>>>(h->d_partials, ph.n_slots, p.B, p.tiles,
                                               h->d_slot_site + ph.slot_begin, h->d_nst, h->d_weight,
-                                              h->d_status, h->d_fail);
+                                              h->d_status, h->d_fail, p.ent);
       CKL(h);
     }
     prev_general = ph.n_slots > 0;
@@ -283,9 +364,18 @@ int run_common(ptsbe_engine* h, const uint8_t* sel, int B, double* out_weight, i
   if (B < 0 || B > h->cap) return fail(h, PTSBE_ERR_VALIDATION, "batch %d exceeds capacity %d", B, h->cap);
   if (B == 0) return 0;
   CK(h, cudaSetDevice(h->dev));
+  h->host_sel.clear();
   if (h->n_sites > 0) {
     if (!sel) return fail(h, PTSBE_ERR_VALIDATION, "selection table is required");
     if (int r = copy_in(h, h->d_sel, sel, (size_t)B * h->n_sites, flags)) return r;
+    // the shared-trunk schedule needs each trajectory's first non-default site on the host
+    h->host_sel.resize((size_t)B * h->n_sites);
+    if (flags & PTSBE_DEVICE_PTRS) {
+      CK(h, cudaMemcpyAsync(h->host_sel.data(), h->d_sel, h->host_sel.size(), cudaMemcpyDeviceToHost, h->stream));
+      CK(h, cudaStreamSynchronize(h->stream));
+    } else {
+      std::memcpy(h->host_sel.data(), sel, h->host_sel.size());
+    }
   }
   batch_reset<<<(B + 255) / 256, 256, 0, h->stream>>>(h->d_weight, h->d_nst, h->d_status, h->d_fail, B);
   CKL(h);
@@ -472,14 +562,16 @@ int ptsbe_create(int device, int n_qubits, int dtype, int batch_cap, ptsbe_engin
     r = fail(h, PTSBE_ERR_CUDA, "device %d unavailable: %s", device, cudaGetErrorString(e));
   }
   if (!r) {
-    const size_t bytes = (size_t)batch_cap * ((size_t)1 << n_qubits) * h->amp_bytes;
+    // batch slots + the shared trunk's two alternating slots
+    const size_t bytes = (size_t)(batch_cap + 2) * ((size_t)1 << n_qubits) * h->amp_bytes;
     e = cudaMalloc(&h->states, bytes);
     if (e != cudaSuccess) r = fail(h, PTSBE_ERR_CUDA, "cannot allocate %zu bytes of state: %s", bytes, cudaGetErrorString(e));
   }
-  if (!r) r = dalloc(h, &h->d_weight, batch_cap);
-  if (!r) r = dalloc(h, &h->d_nst, batch_cap);
-  if (!r) r = dalloc(h, &h->d_status, batch_cap);
-  if (!r) r = dalloc(h, &h->d_fail, batch_cap);
+  // per-row tables: batch rows + the trunk row (index batch_cap)
+  if (!r) r = dalloc(h, &h->d_weight, batch_cap + 1);
+  if (!r) r = dalloc(h, &h->d_nst, batch_cap + 1);
+  if (!r) r = dalloc(h, &h->d_status, batch_cap + 1);
+  if (!r) r = dalloc(h, &h->d_fail, batch_cap + 1);
   if (!r) r = dalloc(h, &h->d_bs, (size_t)batch_cap * h->nblk);
   if (!r) r = dalloc(h, &h->d_total, batch_cap);
   if (!r) r = dalloc(h, &h->d_off, batch_cap);
@@ -488,10 +580,12 @@ int ptsbe_create(int device, int n_qubits, int dtype, int batch_cap, ptsbe_engin
   if (!r) r = dalloc(h, &h->d_uoff, batch_cap);
   if (!r) r = dalloc(h, &h->d_rng, (size_t)batch_cap * 4);
   if (!r) {
-    std::vector<double> ones(batch_cap, 1.0);
-    std::vector<int32_t> zeros(batch_cap, 0);
-    e = cudaMemcpy(h->d_nst, ones.data(), batch_cap * 8, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(h->d_status, zeros.data(), batch_cap * 4, cudaMemcpyHostToDevice);
+    std::vector<double> ones(batch_cap + 1, 1.0);
+    std::vector<int32_t> zeros(batch_cap + 1, 0);
+    e = cudaMemcpy(h->d_nst, ones.data(), (batch_cap + 1) * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(h->d_status, zeros.data(), (batch_cap + 1) * 4, cudaMemcpyHostToDevice);
+    const char* tree_env = std::getenv("PTSBE_TREE");
+    h->tree_enabled = !(tree_env && std::atoi(tree_env) == 0);
     if (e != cudaSuccess) r = fail(h, PTSBE_ERR_CUDA, "init copy failed: %s", cudaGetErrorString(e));
   }
   if (r) {
@@ -510,7 +604,7 @@ int ptsbe_destroy(ptsbe_engine* h) {
                   h->d_phases, h->d_matkind,
                   h->d_chans, h->d_site_chan, h->d_slot_site, h->d_partials, h->d_bs, h->d_total, h->d_off,
                   h->d_m, h->d_nuniq, h->d_uoff, h->d_rng, h->d_keys, h->d_tmp, h->d_idx, h->d_runidx,
-                  h->d_runcnt, h->d_chunks};
+                  h->d_runcnt, h->d_chunks, h->d_ent, h->d_forks};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
@@ -557,7 +651,7 @@ struct HostOp {
 // the rest of the phase; general-channel sites never overtake each other (their
 // realized weights are ratios of consecutive norms in reference order).
 static void plan_phases(std::vector<HostOp>& ops, int L, std::vector<DevOp>& out_ops,
-                        std::vector<DevPhase>& out_phases) {
+                        std::vector<DevPhase>& out_phases, int GB = 4) {
   std::vector<int> remaining(ops.size());
   for (size_t i = 0; i < ops.size(); ++i) remaining[i] = (int)i;
   const uint32_t full = L >= 32 ? 0xffffffffu : ((1u << L) - 1u);
@@ -574,7 +668,7 @@ static void plan_phases(std::vector<HostOp>& ops, int L, std::vector<DevOp>& out
         continue;
       }
       const uint32_t U = S | o.bits;
-      if (__builtin_popcount(U) <= 4) {
+      if (__builtin_popcount(U) <= GB) {
         S = U;
         taken.push_back(i);
       } else {
@@ -583,18 +677,19 @@ static void plan_phases(std::vector<HostOp>& ops, int L, std::vector<DevOp>& out
         gen_blocked = gen_blocked || o.general;
       }
     }
-    for (int q = 0; q < L && __builtin_popcount(S) < 4; ++q) S |= (1u << q) & full;
-    int pb[4], np_ = 0;
-    for (int q = 0; q < L && np_ < 4; ++q)
+    for (int q = 0; q < L && __builtin_popcount(S) < GB; ++q) S |= (1u << q) & full;
+    int pb[5] = {0, 0, 0, 0, 0}, np_ = 0;
+    for (int q = 0; q < L && np_ < GB; ++q)
       if ((S >> q) & 1) pb[np_++] = q;
     DevPhase P;
-    P.pbits = (uint32_t)pb[0] | ((uint32_t)pb[1] << 5) | ((uint32_t)pb[2] << 10) | ((uint32_t)pb[3] << 15);
+    P.pbits = 0;
+    for (int k = 0; k < GB; ++k) P.pbits |= (uint32_t)pb[k] << (5 * k);
     P.op_begin = (int32_t)out_ops.size();
     P.n_ops = (int32_t)taken.size();
-    P.pad = 0;
+    P.pad = GB;
     for (int i : taken) {
       DevOp d = ops[i].d;
-      auto pos = [&](int bit) { for (int k = 0; k < 4; ++k) if (pb[k] == bit) return k; return -1; };
+      auto pos = [&](int bit) { for (int k = 0; k < GB; ++k) if (pb[k] == bit) return k; return -1; };
       d.k0 = pos(d.b0);
       d.k1 = d.arity == 2 ? pos(d.b1) : -1;
       out_ops.push_back(d);
@@ -603,6 +698,10 @@ static void plan_phases(std::vector<HostOp>& ops, int L, std::vector<DevOp>& out
     remaining.swap(deferred);
   }
 }
+
+static int try_codegen(ptsbe_engine* h, int mode, const std::vector<PassHost>& ph, const std::vector<DevOp>& dops,
+                       const std::vector<DevPhase>& dph, const double* mats, const std::vector<int32_t>& kinds,
+                       const ptsbe_channel* chans, const int32_t* site_chan);
 
 int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const double* mats, int n_mats,
                        const ptsbe_channel* chans, int n_chans, const int32_t* site_chan, int n_sites,
@@ -644,6 +743,7 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
   }
   // validate ops, translate targets to tile bits, bucket by pass
   std::vector<std::vector<HostOp>> per_pass(n_passes);
+  std::vector<int> site_pass_tmp(n_sites, n_passes);   // pass that fires each site
   int prev_pass = -1;
   for (int i = 0; i < n_ops; ++i) {
     const ptsbe_op& o = ops[i];
@@ -683,37 +783,65 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
       return fail(h, PTSBE_ERR_VALIDATION, "op %d: unknown kind %d", i, o.kind);
     }
     per_pass[o.pass].push_back(ho);
+    if (o.kind == 1) site_pass_tmp[o.ref] = std::min(site_pass_tmp[o.ref], o.pass);
   }
-  // phases + norm slots (slot order = reference order of general sites)
-  std::vector<DevOp> dops;
-  std::vector<DevPhase> dph;
+  // norm slots (slot order = reference order of general sites)
   std::vector<int32_t> slot_site;
   for (int p = 0; p < n_passes; ++p) {
     PassHost& P = ph[p];
+    P.n_slots = 0;
     for (HostOp& o : per_pass[p])
       if (o.general) { o.d.slot = P.n_slots++; slot_site.push_back(o.d.ref); }
     P.slot_begin = (int)slot_site.size() - P.n_slots;
-    P.op_begin = (int)dops.size();
-    P.phase_begin = (int)dph.size();
-    if (P.L >= 4) {
-      std::vector<DevOp> pops;
-      std::vector<DevPhase> pphs;
-      plan_phases(per_pass[p], P.L, pops, pphs);
-      dops.insert(dops.end(), pops.begin(), pops.end());
-      dph.insert(dph.end(), pphs.begin(), pphs.end());
-      P.n_phases = (int)pphs.size();
-    } else {
-      for (HostOp& o : per_pass[p]) dops.push_back(o.d);
-      P.n_phases = 0;
-    }
-    P.n_ops = (int)dops.size() - P.op_begin;
   }
+  // register phases of GB tile bits (4 for the generic kernel; 5 for c64 codegen)
+  std::vector<DevOp> dops;
+  std::vector<DevPhase> dph;
+  auto plan_all = [&](int GB) {
+    dops.clear();
+    dph.clear();
+    for (int p = 0; p < n_passes; ++p) {
+      PassHost& P = ph[p];
+      P.op_begin = (int)dops.size();
+      P.phase_begin = (int)dph.size();
+      if (P.L >= GB) {
+        std::vector<DevOp> pops;
+        std::vector<DevPhase> pphs;
+        plan_phases(per_pass[p], P.L, pops, pphs, GB);
+        dops.insert(dops.end(), pops.begin(), pops.end());
+        dph.insert(dph.end(), pphs.begin(), pphs.end());
+        P.n_phases = (int)pphs.size();
+      } else {
+        for (HostOp& o : per_pass[p]) dops.push_back(o.d);
+        P.n_phases = 0;
+      }
+      P.n_ops = (int)dops.size() - P.op_begin;
+    }
+  };
+  // circuit-specialised kernels: PTSBE_CODEGEN=1 forces, =0 disables, default for n >= 16
+  const char* cg_env = std::getenv("PTSBE_CODEGEN");
+  const int cg_mode = cg_env ? std::atoi(cg_env) : -1;
+  bool cg_want = n_passes > 0 && (cg_mode == 1 || (cg_mode < 0 && h->n >= 16));
+  const char* gb_env = std::getenv("PTSBE_PHASE_BITS");   // tuning override (4 or 5)
+  const int cg_gb = gb_env ? std::max(4, std::min(5, std::atoi(gb_env))) : (h->dtype == PTSBE_C64 ? 5 : 4);
+  for (auto& P : ph) cg_want = cg_want && P.L >= cg_gb + 3;
+  h->phase_bits = cg_want ? cg_gb : 4;
+  plan_all(h->phase_bits);
   for (int p = 0; p < n_passes; ++p) {
     const size_t smem = pass_smem(ph[p], h->amp_bytes);
     if (smem > 227 * 1024) return fail(h, PTSBE_ERR_VALIDATION, "pass %d needs %zu B shared memory", p, smem);
   }
   std::vector<int32_t> kinds(std::max(n_mats, 1), MK_GEN1);
   for (int m = 0; m < n_mats; ++m) kinds[m] = classify_matrix(mats + (size_t)m * 32, mat_arity[m] ? mat_arity[m] : 2);
+  h->gen_active = false;
+  h->gen_note.clear();
+  if (cg_want) {
+    if (int r = try_codegen(h, cg_mode, ph, dops, dph, mats, kinds, chans, site_chan)) return r;
+    if (!h->gen_active && h->phase_bits != 4) {   // generic kernel: 4-bit phases
+      h->phase_bits = 4;
+      plan_all(4);
+    }
+  }
   // device tables
   if (dalloc(h, &h->d_ops, std::max<size_t>(dops.size(), 1))) return PTSBE_ERR_CUDA;
   if (!dops.empty()) CK(h, cudaMemcpy(h->d_ops, dops.data(), dops.size() * sizeof(DevOp), cudaMemcpyHostToDevice));
@@ -749,10 +877,11 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
   if (dalloc(h, &h->d_slot_site, std::max<size_t>(slot_site.size(), 1))) return PTSBE_ERR_CUDA;
   if (!slot_site.empty())
     CK(h, cudaMemcpy(h->d_slot_site, slot_site.data(), slot_site.size() * 4, cudaMemcpyHostToDevice));
-  if (dalloc(h, &h->d_sel, (size_t)h->cap * std::max(n_sites, 1))) return PTSBE_ERR_CUDA;
+  if (dalloc(h, &h->d_sel, (size_t)(h->cap + 1) * std::max(n_sites, 1))) return PTSBE_ERR_CUDA;
+  CK(h, cudaMemset(h->d_sel, 0, (size_t)(h->cap + 1) * std::max(n_sites, 1)));   // trunk row: all defaults
   size_t need = 1;
   for (auto& P : ph)
-    if (P.n_slots) need = std::max(need, (size_t)P.n_slots * h->cap * ((size_t)1 << (h->n - P.L)));
+    if (P.n_slots) need = std::max(need, (size_t)P.n_slots * (h->cap + 1) * ((size_t)1 << (h->n - P.L)));
   if (need > h->partial_cap) {
     if (dalloc(h, &h->d_partials, need)) return PTSBE_ERR_CUDA;
     h->partial_cap = need;
@@ -762,18 +891,26 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
     CK(h, cudaFuncSetAttribute(pass_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
   else
     CK(h, cudaFuncSetAttribute(pass_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
-  // circuit-specialised kernels: PTSBE_CODEGEN=1 forces, =0 disables, default for n >= 16
-  h->gen_active = false;
-  h->gen_note.clear();
+  h->passes = ph;
+  h->site_pass = site_pass_tmp;
+  h->n_sites = n_sites;
+  h->n_mats = n_mats;
+  h->n_phases_total = (int)dph.size();
+  h->loaded = true;
+  return 0;
+}
+
+// Generate + compile the circuit-specialised kernels (codegen.h).
+static int try_codegen(ptsbe_engine* h, int mode, const std::vector<PassHost>& ph, const std::vector<DevOp>& dops,
+                       const std::vector<DevPhase>& dph, const double* mats, const std::vector<int32_t>& kinds,
+                       const ptsbe_channel* chans, const int32_t* site_chan) {
+  const int n_passes = (int)ph.size();
   {
-    const char* env = std::getenv("PTSBE_CODEGEN");
-    const int mode = env ? std::atoi(env) : -1;
-    bool want = mode == 1 || (mode < 0 && h->n >= 16);
-    for (auto& P : ph) want = want && P.L >= 4;
-    if (want && n_passes > 0) {
+    {
       gen::GenProgram G;
       G.c64 = h->dtype == PTSBE_C64;
       G.n = h->n;
+      G.gb = h->phase_bits;
       G.mats = mats;
       G.kinds = kinds.data();
       G.chans = chans;
@@ -801,11 +938,6 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
       }
     }
   }
-  h->passes = ph;
-  h->n_sites = n_sites;
-  h->n_mats = n_mats;
-  h->n_phases_total = (int)dph.size();
-  h->loaded = true;
   return 0;
 }
 
@@ -954,6 +1086,7 @@ int ptsbe_profile(ptsbe_engine* h, int enable) {
   h->ev_used = 0;
   h->pass_ms_total = 0.0;
   h->pass_launches = 0;
+  h->pass_bytes_total = 0.0;
   return 0;
 }
 
@@ -971,6 +1104,8 @@ int ptsbe_profile_read(ptsbe_engine* h, double* total_ms, int64_t* launches) {
   if (launches) *launches = h->pass_launches;
   return 0;
 }
+
+double ptsbe_profile_bytes(ptsbe_engine* h) { return h ? h->pass_bytes_total : 0.0; }
 
 int ptsbe_info(ptsbe_engine* h, int64_t* out, int n) {
   if (!h || !out) return PTSBE_ERR_VALIDATION;

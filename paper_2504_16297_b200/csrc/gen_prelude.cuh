@@ -7,9 +7,12 @@
 // outcome.  NVRTC compiles prelude + bodies for sm_100a; the persistent,
 // cp.async double-buffered tile loop below is shared by all passes.
 //
+// A phase keeps N = 2^GB amplitudes per thread in registers (GB = 4 or 5 tile
+// bits); the gate templates deduce N from the register array.
+//
 // This file is embedded verbatim as a string (gen_prelude.inc, produced by
 // build.py) -- it is NOT compiled by nvcc directly.  Keep PassParams identical
-// to pass_kernels.cuh (engine.cu static_asserts the layout).
+// to pass_kernels.cuh.
 typedef unsigned int uint32_t;
 typedef int int32_t;
 typedef unsigned long long uint64_t;
@@ -27,6 +30,7 @@ struct PassParams {
   const uint8_t* sel; int S; const int32_t* site_chan; const DevChan* chans;
   const void* mats; const int32_t* mat_kind; const double* nst; int use_scale; int gen_zero;
   double* partials; const int32_t* status; int B; long long tiles;
+  const int4* ent; int E;   // launch entries {trajectory row, src slot, dst slot, 0}
 };
 
 template <typename R> struct Cplx;
@@ -59,19 +63,19 @@ __device__ __forceinline__ double prob64(double2 a) {
   return __dadd_rn(__dmul_rn(a.x, a.x), __dmul_rn(a.y, a.y));
 }
 
-// ---- gate kernels on a 16-amplitude register group; K* compile-time bit positions
-template <int K, typename V> __device__ __forceinline__ void g1(V* a, V m00, V m01, V m10, V m11) {
+// ---- gate kernels on an N-amplitude register group; K* compile-time bit positions
+template <int K, typename V, int N> __device__ __forceinline__ void g1(V (&a)[N], V m00, V m01, V m10, V m11) {
 #pragma unroll
-  for (int j = 0; j < 16; ++j)
+  for (int j = 0; j < N; ++j)
     if (!(j & (1 << K))) {
       const V x = a[j], y = a[j | (1 << K)];
       a[j] = cmadd2(m00, x, m01, y);
       a[j | (1 << K)] = cmadd2(m10, x, m11, y);
     }
 }
-template <int K, typename V, typename R> __device__ __forceinline__ void g1r(V* a, R m00, R m01, R m10, R m11) {
+template <int K, typename V, int N, typename R> __device__ __forceinline__ void g1r(V (&a)[N], R m00, R m01, R m10, R m11) {
 #pragma unroll
-  for (int j = 0; j < 16; ++j)
+  for (int j = 0; j < N; ++j)
     if (!(j & (1 << K))) {
       const V x = a[j], y = a[j | (1 << K)];
       V u, v;
@@ -80,31 +84,44 @@ template <int K, typename V, typename R> __device__ __forceinline__ void g1r(V* 
       a[j] = u; a[j | (1 << K)] = v;
     }
 }
-template <int K, typename V> __device__ __forceinline__ void g1d(V* a, V d0, V d1) {
+template <int K, typename V, int N> __device__ __forceinline__ void g1d(V (&a)[N], V d0, V d1) {
 #pragma unroll
-  for (int j = 0; j < 16; ++j) a[j] = cmul((j & (1 << K)) ? d1 : d0, a[j]);
+  for (int j = 0; j < N; ++j) a[j] = cmul((j & (1 << K)) ? d1 : d0, a[j]);
 }
-template <int K, typename V> __device__ __forceinline__ void g1p(V* a, V d1) {
+template <int K, typename V, int N> __device__ __forceinline__ void g1p(V (&a)[N], V d1) {
 #pragma unroll
-  for (int j = 0; j < 16; ++j)
+  for (int j = 0; j < N; ++j)
     if (j & (1 << K)) a[j] = cmul(d1, a[j]);
 }
-template <int K, typename V> __device__ __forceinline__ void g1a(V* a, V m01, V m10) {
+template <int K, typename V, int N> __device__ __forceinline__ void g1a(V (&a)[N], V m01, V m10) {
 #pragma unroll
-  for (int j = 0; j < 16; ++j)
+  for (int j = 0; j < N; ++j)
     if (!(j & (1 << K))) {
       const V x = a[j], y = a[j | (1 << K)];
       a[j] = cmul(m01, y); a[j | (1 << K)] = cmul(m10, x);
     }
 }
-template <int K, typename V> __device__ __forceinline__ void g1x(V* a) {   // X: swap, no arithmetic
+template <int K, typename V, int N> __device__ __forceinline__ void g1x(V (&a)[N]) {   // X: renaming only
 #pragma unroll
-  for (int j = 0; j < 16; ++j)
+  for (int j = 0; j < N; ++j)
     if (!(j & (1 << K))) { const V t = a[j]; a[j] = a[j | (1 << K)]; a[j | (1 << K)] = t; }
 }
-template <int KH, int KL, typename V> __device__ __forceinline__ void g2(V* a, const V* m) {
+template <int K, typename V, int N> __device__ __forceinline__ void g1neg(V (&a)[N]) {    // diag(1, -1)
 #pragma unroll
-  for (int j = 0; j < 16; ++j)
+  for (int j = 0; j < N; ++j)
+    if (j & (1 << K)) { a[j].x = -a[j].x; a[j].y = -a[j].y; }
+}
+template <int K, typename V, int N> __device__ __forceinline__ void g1pi(V (&a)[N], bool neg) {   // diag(1, ±i)
+#pragma unroll
+  for (int j = 0; j < N; ++j)
+    if (j & (1 << K)) {
+      const V x = a[j];
+      if (neg) { a[j].x = x.y; a[j].y = -x.x; } else { a[j].x = -x.y; a[j].y = x.x; }
+    }
+}
+template <int KH, int KL, typename V, int N> __device__ __forceinline__ void g2(V (&a)[N], const V* m) {
+#pragma unroll
+  for (int j = 0; j < N; ++j)
     if (!(j & (1 << KH)) && !(j & (1 << KL))) {
       const int i1 = j | (1 << KL), i2 = j | (1 << KH), i3 = j | (1 << KH) | (1 << KL);
       const V v0 = a[j], v1 = a[i1], v2 = a[i2], v3 = a[i3];
@@ -114,67 +131,46 @@ template <int KH, int KL, typename V> __device__ __forceinline__ void g2(V* a, c
       a[i3] = cmadd4(m[12], m[13], m[14], m[15], v0, v1, v2, v3);
     }
 }
-template <int KH, int KL, typename V> __device__ __forceinline__ void g2cx(V* a) {
+template <int KH, int KL, typename V, int N> __device__ __forceinline__ void g2cx(V (&a)[N]) {
 #pragma unroll
-  for (int j = 0; j < 16; ++j)
+  for (int j = 0; j < N; ++j)
     if ((j & (1 << KH)) && !(j & (1 << KL))) { const V t = a[j]; a[j] = a[j | (1 << KL)]; a[j | (1 << KL)] = t; }
 }
-template <int KH, int KL, typename V> __device__ __forceinline__ void g2sw(V* a) {
+template <int KH, int KL, typename V, int N> __device__ __forceinline__ void g2sw(V (&a)[N]) {
 #pragma unroll
-  for (int j = 0; j < 16; ++j)
+  for (int j = 0; j < N; ++j)
     if ((j & (1 << KH)) && !(j & (1 << KL))) {
       const int o = (j & ~(1 << KH)) | (1 << KL);
       const V t = a[j]; a[j] = a[o]; a[o] = t;
     }
 }
-template <int KH, int KL, typename V> __device__ __forceinline__ void g2d(V* a, V d0, V d1, V d2, V d3) {
+template <int KH, int KL, int S, typename V, int N> __device__ __forceinline__ void g2dsel(V (&a)[N], V d) {
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const int s = ((j >> KH) & 1) * 2 + ((j >> KL) & 1);
-    a[j] = cmul(s == 0 ? d0 : s == 1 ? d1 : s == 2 ? d2 : d3, a[j]);
-  }
-}
-
-template <int K, typename V> __device__ __forceinline__ void g1neg(V* a) {    // diag(1, -1)
-#pragma unroll
-  for (int j = 0; j < 16; ++j)
-    if (j & (1 << K)) { a[j].x = -a[j].x; a[j].y = -a[j].y; }
-}
-template <int K, typename V> __device__ __forceinline__ void g1pi(V* a, bool neg) {   // diag(1, ±i)
-#pragma unroll
-  for (int j = 0; j < 16; ++j)
-    if (j & (1 << K)) {
-      const V x = a[j];
-      if (neg) { a[j].x = x.y; a[j].y = -x.x; } else { a[j].x = -x.y; a[j].y = x.x; }
-    }
-}
-template <int KH, int KL, int S, typename V> __device__ __forceinline__ void g2dsel(V* a, V d) {
-#pragma unroll
-  for (int j = 0; j < 16; ++j)
+  for (int j = 0; j < N; ++j)
     if (((j >> KH) & 1) * 2 + ((j >> KL) & 1) == S) a[j] = cmul(d, a[j]);
 }
-template <typename V> __device__ __forceinline__ void cscale16(V* a, V d) {
+template <typename V, int N> __device__ __forceinline__ void cscale(V (&a)[N], V d) {
 #pragma unroll
-  for (int j = 0; j < 16; ++j) a[j] = cmul(d, a[j]);
+  for (int j = 0; j < N; ++j) a[j] = cmul(d, a[j]);
 }
-template <typename V> __device__ __forceinline__ void rscale16(V* a, double s) {
+template <typename V, int N> __device__ __forceinline__ void rscale(V (&a)[N], double s) {
   typedef decltype(a[0].x) R;
   const R sc = (R)s;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) { a[j].x *= sc; a[j].y *= sc; }
+  for (int j = 0; j < N; ++j) { a[j].x *= sc; a[j].y *= sc; }
 }
 
 // ---- interpreter for the rare phases in which a trajectory has a non-default
-// outcome.  The thread's 16-amplitude group is parked in shared memory (its
-// own slots only, so no barrier is needed between ops) and every op of the
-// phase is applied with run-time decoding.  Kind codes as in pass_kernels.cuh.
-template <typename V> __device__ __forceinline__ V ldm(const V* m, int e) { return m[e]; }
-
+// outcome.  The thread's group is parked in shared memory (its own slots only,
+// so no barrier is needed between ops) and every op of the phase is applied
+// with run-time decoding.  sb[q] = swizzled offset of the phase's q-th bit.
 template <typename V>
-__device__ __noinline__ void interp_phase(V* cur, uint32_t sg, const uint32_t* sb, const PassParams& p, int phase,
-                                          const uint8_t* sel, int b, long long tile, double* red, bool active) {
+__device__ __noinline__ void interp_phase(V* cur, uint32_t sg, const uint32_t* sb, int gbits, const PassParams& p,
+                                          int phase, const uint8_t* sel, int b, long long tile, double* red,
+                                          bool active) {
   const DevPhase P = p.phases[phase];
   const V* mats = reinterpret_cast<const V*>(p.mats);
+  const int N = 1 << gbits;
   for (int k = P.op_begin; k < P.op_begin + P.n_ops; ++k) {
     const DevOp op = p.ops[k];
     int mat = op.ref;
@@ -190,20 +186,20 @@ __device__ __noinline__ void interp_phase(V* cur, uint32_t sg, const uint32_t* s
     if (active) {
       if (op.arity == 1) {
         const V m00 = m[0], m01 = m[1], m10 = m[4], m11 = m[5];
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < N; ++j) {
           if (j & (1 << op.k0)) continue;
-          uint32_t a0 = sg, a1;
-          for (int q = 0; q < 4; ++q) if ((j >> q) & 1) a0 ^= sb[q];
-          a1 = a0 ^ sb[op.k0];
+          uint32_t a0 = sg;
+          for (int q = 0; q < gbits; ++q) if ((j >> q) & 1) a0 ^= sb[q];
+          const uint32_t a1 = a0 ^ sb[op.k0];
           const V x = cur[a0], y = cur[a1];
           cur[a0] = cmadd2(m00, x, m01, y);
           cur[a1] = cmadd2(m10, x, m11, y);
         }
       } else {
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < N; ++j) {
           if ((j & (1 << op.k0)) || (j & (1 << op.k1))) continue;
           uint32_t a0 = sg;
-          for (int q = 0; q < 4; ++q) if ((j >> q) & 1) a0 ^= sb[q];
+          for (int q = 0; q < gbits; ++q) if ((j >> q) & 1) a0 ^= sb[q];
           const uint32_t a1 = a0 ^ sb[op.k1], a2 = a0 ^ sb[op.k0], a3 = a2 ^ sb[op.k1];
           const V v0 = cur[a0], v1 = cur[a1], v2 = cur[a2], v3 = cur[a3];
           cur[a0] = cmadd4(m[0], m[1], m[2], m[3], v0, v1, v2, v3);
@@ -216,9 +212,9 @@ __device__ __noinline__ void interp_phase(V* cur, uint32_t sg, const uint32_t* s
     if (general) {
       double s = 0.0;
       if (active)
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < N; ++j) {
           uint32_t a0 = sg;
-          for (int q = 0; q < 4; ++q) if ((j >> q) & 1) a0 ^= sb[q];
+          for (int q = 0; q < gbits; ++q) if ((j >> q) & 1) a0 ^= sb[q];
           s += prob64(cur[a0]);
         }
 #pragma unroll
@@ -243,16 +239,6 @@ __device__ __forceinline__ uint32_t swz(float2*, uint32_t i) {   // never flips 
 __device__ __forceinline__ uint32_t swz(double2*, uint32_t i) {
   const uint32_t h = (i >> 3) ^ (i >> 6) ^ ((i >> 6) << 1) ^ (i >> 9) ^ (i >> 12);
   return i ^ (h & 7u);
-}
-__device__ __forceinline__ uint64_t pdep64(uint64_t src, uint64_t mask) {
-  uint64_t out = 0;
-  while (mask) {
-    const uint64_t low = mask & (~mask + 1);
-    if (src & 1) out |= low;
-    src >>= 1;
-    mask ^= low;
-  }
-  return out;
 }
 __device__ __forceinline__ uint32_t ins0(uint32_t p, int bit) {
   const uint32_t lo = p & ((1u << bit) - 1u);
@@ -282,70 +268,75 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return r;
 }
 
-// ---- phase register load / store (16 amplitudes at sg ^ so[j]; so[] literal)
-template <typename V, int P0>
-__device__ __forceinline__ void ld16(V* a, const V* cur, uint32_t sg, const uint32_t* so, bool active, double scale) {
+// ---- phase register load / store (N amplitudes at sg ^ so[j]; so[] literal)
+template <typename V, int N, int P0>
+__device__ __forceinline__ void ldg(V (&a)[N], const V* cur, uint32_t sg, const uint32_t* so, bool active,
+                                    double scale) {
   if (!active) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) a[j] = mk((V*)0, 0.0, 0.0);
+    for (int j = 0; j < N; ++j) a[j] = mk((V*)0, 0.0, 0.0);
     return;
   }
   if (sizeof(V) == 8 && P0 == 0) {      // bit 0 in the phase: adjacent pairs, 16-B accesses
 #pragma unroll
-    for (int j = 0; j < 16; j += 2) {
+    for (int j = 0; j < N; j += 2) {
       const float4 w = *reinterpret_cast<const float4*>(cur + (sg ^ so[j]));
       a[j] = mk((V*)0, w.x, w.y);
       a[j + 1] = mk((V*)0, w.z, w.w);
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) a[j] = cur[sg ^ so[j]];
+    for (int j = 0; j < N; ++j) a[j] = cur[sg ^ so[j]];
   }
   if (scale != 1.0) {
+    typedef decltype(a[0].x) R;
+    const R sc = (R)scale;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) { a[j].x *= scale; a[j].y *= scale; }
+    for (int j = 0; j < N; ++j) { a[j].x *= sc; a[j].y *= sc; }
   }
 }
-template <typename V, int P0>
-__device__ __forceinline__ void st16(const V* a, V* cur, uint32_t sg, const uint32_t* so, bool active) {
+template <typename V, int N, int P0>
+__device__ __forceinline__ void stg(const V (&a)[N], V* cur, uint32_t sg, const uint32_t* so, bool active) {
   if (!active) return;
   if (sizeof(V) == 8 && P0 == 0) {
 #pragma unroll
-    for (int j = 0; j < 16; j += 2) {
+    for (int j = 0; j < N; j += 2) {
       float4 w; w.x = a[j].x; w.y = a[j].y; w.z = a[j + 1].x; w.w = a[j + 1].y;
       *reinterpret_cast<float4*>(cur + (sg ^ so[j])) = w;
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) cur[sg ^ so[j]] = a[j];
+    for (int j = 0; j < N; ++j) cur[sg ^ so[j]] = a[j];
   }
 }
-template <typename V>
-__device__ __forceinline__ void zero16(V* a, uint64_t base, uint32_t gb, const uint32_t* off, bool active,
-                                       double g_re = 1.0, double g_im = 0.0) {
-  // |0...0> times the program's accumulated global phase G (see codegen.h)
+// |0...0> times the program's accumulated global phase G (see codegen.h)
+template <typename V, int N>
+__device__ __forceinline__ void zerog(V (&a)[N], uint64_t base, uint32_t gb, const uint32_t* off, bool active,
+                                      double g_re, double g_im) {
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
+  for (int j = 0; j < N; ++j) {
     const bool one = active && base == 0 && (gb | off[j]) == 0;
     a[j] = mk((V*)0, one ? g_re : 0.0, one ? g_im : 0.0);
   }
 }
 
 // Persistent, double-buffered tile loop shared by every generated pass kernel.
-// Compile-time: R, tile bits L, contiguous low bits C, TLOG = n - L.
+// Compile-time: R, tile bits L, contiguous low bits C, TLOG = n - L, threads NT.
 // tile_base(tile) / row_off(r) scatter bits onto the pass's fixed qubit masks
 // (generated per pass as shift/mask runs).  Each thread's 16-B vectors sit at
 // rows r0 + k*RSTEP with a fixed in-row offset, so their shared and global
 // offsets are a per-thread base plus compile-time constants (swz and the row
-// scatter are linear on disjoint bits).
-// body(cur, b, sel_row, tile, base, scale, red) runs the pass's phases on one tile.
-template <typename R, int L, int C, int TLOG, class TileBase, class RowOff, class Body>
-__device__ __forceinline__ void run_pass(const PassParams& p, TileBase tile_base, RowOff row_off, Body body) {
+// scatter are linear on disjoint bits).  err_mask(sel_row) runs once per CTA
+// per trajectory.  body(cur, b, sel_row, tile, base, scale, red, emask) runs
+// the pass's phases on one tile.
+template <typename R, int L, int C, int TLOG, int NT, class TileBase, class RowOff, class ErrMask, class Body>
+__device__ __forceinline__ void run_pass(const PassParams& p, TileBase tile_base, RowOff row_off, ErrMask err_mask,
+                                         Body body) {
   typedef typename Cplx<R>::V V;
   typedef typename Cplx<R>::W W;
   constexpr int VPW = sizeof(W) / sizeof(V);
   constexpr uint32_t TL = 1u << L;
-  constexpr int THREADS = (L - 4) >= 5 ? (1 << (L - 4)) : 32;
+  constexpr int THREADS = NT;
   constexpr int CPR_LOG = C - (VPW == 2 ? 1 : 0);          // 16-B vectors per row, log2
   constexpr uint32_t NVEC = TL / VPW;
   constexpr bool FAST = THREADS >= (1 << CPR_LOG) && (NVEC % THREADS) == 0;
@@ -355,17 +346,19 @@ __device__ __forceinline__ void run_pass(const PassParams& p, TileBase tile_base
   V* buf0 = reinterpret_cast<V*>(smem);
   V* buf1 = buf0 + TL;
   double* red = reinterpret_cast<double*>(buf1 + TL);
+  uint64_t* emask_s = reinterpret_cast<uint64_t*>(red + 32);
+  int lb = -1;
   const uint32_t tid = threadIdx.x;
   const uint32_t j0 = tid & ((1u << CPR_LOG) - 1u);
   const uint32_t r0 = tid >> CPR_LOG;
   const uint32_t s0 = swz((V*)0, (r0 << C) | (j0 * VPW));
   const uint64_t g0 = row_off(r0) + (uint64_t)j0 * VPW;
-  const long long total = (long long)p.B << TLOG;
+  const long long total = (long long)p.E << TLOG;
 
   auto load_tile = [&](long long tt, V* dst) {
-    const int bb = (int)(tt >> TLOG);
-    if (p.gen_zero || p.status[bb] != 0) return;
-    const V* src = reinterpret_cast<const V*>(p.states) + ((size_t)bb << p.n) +
+    const int4 en = p.ent[(int)(tt >> TLOG)];
+    if (p.gen_zero || p.status[en.x] != 0) return;
+    const V* src = reinterpret_cast<const V*>(p.states) + ((size_t)en.y << p.n) +
                    tile_base((uint64_t)(tt & ((1ll << TLOG) - 1)));
     if (FAST) {
 #pragma unroll
@@ -389,13 +382,20 @@ __device__ __forceinline__ void run_pass(const PassParams& p, TileBase tile_base
     cp_async_commit();
     cp_async_wait1();
     __syncthreads();
-    const int b = (int)(t >> TLOG);
+    const int4 en = p.ent[(int)(t >> TLOG)];
+    const int b = en.x;                          // trajectory row
     const long long tile = t & ((1ll << TLOG) - 1);
     if (p.status[b] != 0) continue;
+    if (b != lb) {   // per trajectory, once: which phases see a non-default outcome
+      if (tid == 0) *emask_s = err_mask(p.sel + (size_t)b * p.S);
+      __syncthreads();
+      lb = b;
+    }
+    const uint64_t emask = *emask_s;
     const uint64_t base = tile_base((uint64_t)tile);
     const double scale = (p.use_scale && !p.gen_zero) ? rsqrt(p.nst[b]) : 1.0;
-    body(cur, b, p.sel + (size_t)b * p.S, tile, base, scale, red);
-    V* st = reinterpret_cast<V*>(p.states) + ((size_t)b << p.n) + base;
+    body(cur, b, p.sel + (size_t)b * p.S, tile, base, scale, red, emask);
+    V* st = reinterpret_cast<V*>(p.states) + ((size_t)en.z << p.n) + base;
     if (FAST) {
 #pragma unroll
       for (int k = 0; k < ITER; ++k) {

@@ -83,8 +83,10 @@ struct PassParams {
   int gen_zero;              // first pass: synthesize |0...0> instead of loading
   double* partials;          // [slot][B][tiles]
   const int32_t* status;     // [B]
-  int B;
+  int B;                     // trajectory rows (stride of per-row tables)
   long long tiles;
+  const int4* ent;           // [E] launch entries {row, src slot, dst slot, 0}
+  int E;
 };
 
 // ---- shared-memory swizzle: spreads the 32 lanes of a phase access over banks
@@ -288,13 +290,14 @@ __global__ void __launch_bounds__(sizeof(R) == 8 ? 256 : 512) pass_kernel(PassPa
 
   const int cpr_log = c - (VPW == 2 ? 1 : 0);   // 16-B vectors per row, log2
   const uint32_t nvec = TL / VPW;
-  const long long total = (long long)p.B * p.tiles;
+  const long long total = (long long)p.E * p.tiles;
 
   auto issue_load = [&](long long tt, V* dst) {
-    const int bb = (int)(tt / p.tiles);
-    if (p.gen_zero || p.status[bb] != 0) return;
-    const uint64_t base = pdep64((uint64_t)(tt - (long long)bb * p.tiles), comp);
-    const V* src = reinterpret_cast<const V*>(p.states) + ((size_t)bb << p.n) + base;
+    const int eb = (int)(tt / p.tiles);
+    const int4 en = p.ent[eb];
+    if (p.gen_zero || p.status[en.x] != 0) return;
+    const uint64_t base = pdep64((uint64_t)(tt - (long long)eb * p.tiles), comp);
+    const V* src = reinterpret_cast<const V*>(p.states) + ((size_t)en.y << p.n) + base;
 #pragma unroll 4
     for (uint32_t u = threadIdx.x; u < nvec; u += blockDim.x) {
       const uint32_t r = u >> cpr_log;
@@ -317,8 +320,10 @@ __global__ void __launch_bounds__(sizeof(R) == 8 ? 256 : 512) pass_kernel(PassPa
     cp_async_commit();
     cp_async_wait<1>();                         // this thread's copies of `cur` landed
     __syncthreads();                            // ... and everyone else's
-    const int b = (int)(t / p.tiles);
-    const long long tile = t - (long long)b * p.tiles;
+    const int eb = (int)(t / p.tiles);
+    const long long tile = t - (long long)eb * p.tiles;
+    const int4 en = p.ent[eb];
+    const int b = en.x;                         // trajectory row
     if (p.status[b] != 0) continue;             // annihilated: stop evolving (CTA-uniform)
     if (b != cur_b) {
       // warp 0: this trajectory's op list, identity outcomes dropped, decoded once
@@ -429,7 +434,7 @@ __global__ void __launch_bounds__(sizeof(R) == 8 ? 256 : 512) pass_kernel(PassPa
     }
 
     // ---- shared -> HBM
-    V* st = reinterpret_cast<V*>(p.states) + ((size_t)b << p.n) + base;
+    V* st = reinterpret_cast<V*>(p.states) + ((size_t)en.z << p.n) + base;
 #pragma unroll 4
     for (uint32_t u = threadIdx.x; u < nvec; u += blockDim.x) {
       const uint32_t r = u >> cpr_log;
@@ -448,15 +453,17 @@ __global__ void __launch_bounds__(32) pass_kernel_small(PassParams p) {
   using V = typename Cplx<R>::V;
   __shared__ V tile[16];
   __shared__ double red[32];
-  const int b = blockIdx.y;
+  const int4 en = p.ent[blockIdx.y];
+  const int b = en.x;
   if (p.status[b] != 0) return;
   const uint32_t TL = 1u << p.L;                 // == 2^n, one tile
-  V* st = reinterpret_cast<V*>(p.states) + ((size_t)b << p.n);
+  const V* src = reinterpret_cast<const V*>(p.states) + ((size_t)en.y << p.n);
+  V* st = reinterpret_cast<V*>(p.states) + ((size_t)en.z << p.n);
   const R scale = (!p.gen_zero && p.use_scale) ? (R)rsqrt(p.nst[b]) : R(1);
   for (uint32_t i = threadIdx.x; i < TL; i += blockDim.x) {
     V v;
     if (p.gen_zero) { v.x = i == 0 ? R(1) : R(0); v.y = R(0); }
-    else { v = st[i]; v.x *= scale; v.y *= scale; }
+    else { v = src[i]; v.x *= scale; v.y *= scale; }
     tile[i] = v;
   }
   __syncthreads();
@@ -508,9 +515,9 @@ __global__ void __launch_bounds__(32) pass_kernel_small(PassParams p) {
 __global__ void __launch_bounds__(256) norm_finalize(const double* partials, int n_slots, int B,
                                                      long long tiles, const int32_t* slot_site,
                                                      double* nst, double* weight, int32_t* status,
-                                                     int32_t* fail_site) {
+                                                     int32_t* fail_site, const int4* ent) {
   __shared__ double red[32];
-  const int b = blockIdx.x;
+  const int b = ent[blockIdx.x].x;
   if (status[b] != 0) return;
   double prev = 1.0;
   double w = weight[b];
@@ -557,6 +564,16 @@ __global__ void init_zero_kernel(void* states, int n, int B) {
 __global__ void batch_reset(double* weight, double* nst, int32_t* status, int32_t* fail_site, int B) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b < B) { weight[b] = 1.0; nst[b] = 1.0; status[b] = 0; fail_site[b] = -1; }
+}
+
+// Forked trajectories inherit the shared trunk's running weight / norm / status.
+__global__ void fork_rows(const int32_t* rows, int n, int trunk, double* weight, double* nst, int32_t* status,
+                          int32_t* fail_site) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const int r = rows[i];
+    weight[r] = weight[trunk]; nst[r] = nst[trunk]; status[r] = status[trunk]; fail_site[r] = fail_site[trunk];
+  }
 }
 
 // Multiply state b by 1/sqrt(nst[b]) (normalise before download).

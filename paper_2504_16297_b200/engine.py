@@ -191,10 +191,10 @@ class Engine:
         self._check(self.lib.ptsbe_profile(self.h, 1 if enable else 0), "ptsbe_profile")
 
     def profile_read(self):
-        """(total pass-kernel ms, pass launches) since profile(True)."""
+        """(pass-kernel ms, pass launches, algorithmic bytes) since profile(True)."""
         ms, n = C.c_double(), C.c_int64()
         self._check(self.lib.ptsbe_profile_read(self.h, C.byref(ms), C.byref(n)), "ptsbe_profile_read")
-        return float(ms.value), int(n.value)
+        return float(ms.value), int(n.value), float(self.lib.ptsbe_profile_bytes(self.h))
 
     def info(self) -> dict:
         out = np.zeros(11, dtype=np.int64)

@@ -281,3 +281,23 @@ def test_permuted_layout_sampling_modes():
             obs = np.append(obs, s.shots - obs.sum())
             exp = np.append(exp, s.shots - exp.sum())
             assert stats.chisquare(obs, exp).pvalue > 0.01
+
+
+@pytest.mark.parametrize("cfg,dtype", [(2, "c128"), (4, "c64")])
+def test_shared_trunk_schedule_is_bit_identical(cfg, dtype, monkeypatch):
+    """Forking trajectories off the shared noiseless trunk must give exactly the states of
+    evolving each one from |0> on its own (PTSBE_TREE=0)."""
+    c = workloads.build(cfg, P.parse_circuit, P.parse_noise_model, P.attach_noise)
+    specs = P.presample_probabilistic(c, 400, 10, np.random.default_rng(8))[:5]
+    prog = compile_circuit(c, dtype)
+    assert prog.n_passes >= 2
+    out = {}
+    for tree in ("1", "0"):
+        monkeypatch.setenv("PTSBE_TREE", tree)
+        with Engine(c.n_qubits, dtype, batch_cap=len(specs)) as eng:
+            eng.load_program(prog)
+            w, st = eng.run(selection_matrix(prog, specs))
+            out[tree] = (w, st, [eng.get_state(b) for b in range(len(specs))])
+    assert np.array_equal(out["1"][0], out["0"][0]) and np.array_equal(out["1"][1], out["0"][1])
+    for a, b in zip(out["1"][2], out["0"][2]):
+        assert np.array_equal(a, b)

@@ -9,7 +9,7 @@ REPO = Path(__file__).resolve().parents[1]
 
 def declared_symbols():
     text = (REPO / "include" / "ptsbe.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|void\*|int64_t)\s+(ptsbe_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|void\*|int64_t|double)\s+(ptsbe_\w+)\s*\(", text, re.M)))
 
 
 def test_header_lists_entry_points():
