@@ -162,7 +162,7 @@ def run_reference(args):
     cores = os.cpu_count() or 1
     mem = psutil.virtual_memory().available
     state_b = (1 << c.n_qubits) * 16
-    workers = max(1, min(cores, int(mem * 0.5 // (4 * state_b)), 8))
+    workers = max(1, min(cores, int(mem * 0.3 // (4 * state_b)), 4))
     vals = []
     for _ in range(args.warmup and 0):
         pass
