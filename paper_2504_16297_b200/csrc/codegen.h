@@ -139,7 +139,12 @@ struct Emitter {
         double a = m[0], b = m[2], c = m[8], d = m[10];
         double f = 1.0;
         if (scaled) { f = std::fabs(a) >= std::fabs(b) ? a : b; a /= f; b /= f; c /= f; d /= f; }
-        o << "ptg::g1r<" << k0 << ">(a, " << rl(a) << ", " << rl(b) << ", " << rl(c) << ", " << rl(d) << ");\n";
+        if (a == 1.0 && b == 1.0 && c == 1.0 && d == -1.0)        // scaled Hadamard
+          o << "ptg::g1h<" << k0 << ">(a);\n";
+        else if (a == 1.0 && d == 1.0)                             // scaled rotation
+          o << "ptg::g1rot<" << k0 << ">(a, " << rl(b) << ", " << rl(c) << ");\n";
+        else
+          o << "ptg::g1r<" << k0 << ">(a, " << rl(a) << ", " << rl(b) << ", " << rl(c) << ", " << rl(d) << ");\n";
         return {f, 0.0};
       }
       case 2: {  // MK_DIAG1

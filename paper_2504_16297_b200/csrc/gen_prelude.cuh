@@ -40,20 +40,37 @@ template <> struct Cplx<double> { typedef double2 V; typedef double2 W; };
 __device__ __forceinline__ float2 mk(float2*, double x, double y) { return make_float2((float)x, (float)y); }
 __device__ __forceinline__ double2 mk(double2*, double x, double y) { return make_double2(x, y); }
 
-template <typename V> __device__ __forceinline__ V cmul(V d, V x) {
-  V r; r.x = d.x * x.x - d.y * x.y; r.y = d.x * x.y + d.y * x.x; return r;
+// Packed (re, im) arithmetic.  complex64 uses Blackwell's FP32x2 instructions
+// (FFMA2 / FMUL2 / FADD2): one instruction per complex component pair, and the
+// (im, re) swap of a complex multiply folds into the operand selector.
+// complex128 falls back to scalar DFMA.
+__device__ __forceinline__ float2 pfma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 pmul(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 padd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ double2 pfma(double2 a, double2 b, double2 c) {
+  return make_double2(fma(a.x, b.x, c.x), fma(a.y, b.y, c.y));
 }
-template <typename V> __device__ __forceinline__ V cmadd2(V m0, V a, V m1, V b) {
-  V r;
-  r.x = m0.x * a.x - m0.y * a.y + m1.x * b.x - m1.y * b.y;
-  r.y = m0.x * a.y + m0.y * a.x + m1.x * b.y + m1.y * b.x;
-  return r;
+__device__ __forceinline__ double2 pmul(double2 a, double2 b) { return make_double2(a.x * b.x, a.y * b.y); }
+__device__ __forceinline__ double2 padd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+template <typename V, typename S> __device__ __forceinline__ V bc(S s) { V r; r.x = s; r.y = s; return r; }
+template <typename V> __device__ __forceinline__ V swp(V x) { V r; r.x = x.y; r.y = x.x; return r; }
+template <typename V> __device__ __forceinline__ V pm(V d) { V r; r.x = -d.y; r.y = d.y; return r; }   // (-im, im)
+
+template <typename V> __device__ __forceinline__ V cmul(V d, V x) {     // d * x
+  return pfma(bc<V>(d.x), x, pmul(pm(d), swp(x)));
+}
+template <typename V> __device__ __forceinline__ V cmadd2(V m0, V a, V m1, V b) {   // m0*a + m1*b
+  return pfma(bc<V>(m0.x), a, pfma(pm(m0), swp(a), pfma(bc<V>(m1.x), b, pmul(pm(m1), swp(b)))));
 }
 template <typename V> __device__ __forceinline__ V cmadd4(V m0, V m1, V m2, V m3, V a, V b, V c, V d) {
-  V r;
-  r.x = m0.x * a.x - m0.y * a.y + m1.x * b.x - m1.y * b.y + m2.x * c.x - m2.y * c.y + m3.x * d.x - m3.y * d.y;
-  r.y = m0.x * a.y + m0.y * a.x + m1.x * b.y + m1.y * b.x + m2.x * c.y + m2.y * c.x + m3.x * d.y + m3.y * d.x;
-  return r;
+  V r = pmul(pm(m3), swp(d));
+  r = pfma(bc<V>(m3.x), d, r);
+  r = pfma(pm(m2), swp(c), r);
+  r = pfma(bc<V>(m2.x), c, r);
+  r = pfma(pm(m1), swp(b), r);
+  r = pfma(bc<V>(m1.x), b, r);
+  r = pfma(pm(m0), swp(a), r);
+  return pfma(bc<V>(m0.x), a, r);
 }
 __device__ __forceinline__ double prob64(float2 a) {
   const double x = a.x, y = a.y;
@@ -78,10 +95,28 @@ template <int K, typename V, int N, typename R> __device__ __forceinline__ void 
   for (int j = 0; j < N; ++j)
     if (!(j & (1 << K))) {
       const V x = a[j], y = a[j | (1 << K)];
-      V u, v;
-      u.x = m00 * x.x + m01 * y.x; u.y = m00 * x.y + m01 * y.y;
-      v.x = m10 * x.x + m11 * y.x; v.y = m10 * x.y + m11 * y.y;
-      a[j] = u; a[j | (1 << K)] = v;
+      a[j] = pfma(bc<V>(m01), y, pmul(bc<V>(m00), x));
+      a[j | (1 << K)] = pfma(bc<V>(m11), y, pmul(bc<V>(m10), x));
+    }
+}
+// [[1, t0], [t1, 1]] -- a pivot-scaled real rotation (ry): one packed FMA per output
+template <int K, typename V, int N, typename R> __device__ __forceinline__ void g1rot(V (&a)[N], R t0, R t1) {
+#pragma unroll
+  for (int j = 0; j < N; ++j)
+    if (!(j & (1 << K))) {
+      const V x = a[j], y = a[j | (1 << K)];
+      a[j] = pfma(bc<V>(t0), y, x);
+      a[j | (1 << K)] = pfma(bc<V>(t1), x, y);
+    }
+}
+// [[1, 1], [1, -1]] -- a pivot-scaled Hadamard: add / subtract butterfly
+template <int K, typename V, int N> __device__ __forceinline__ void g1h(V (&a)[N]) {
+#pragma unroll
+  for (int j = 0; j < N; ++j)
+    if (!(j & (1 << K))) {
+      const V x = a[j], y = a[j | (1 << K)];
+      a[j] = padd(x, y);
+      a[j | (1 << K)] = pfma(bc<V>(-1.0f), y, x);
     }
 }
 template <int K, typename V, int N> __device__ __forceinline__ void g1d(V (&a)[N], V d0, V d1) {
@@ -109,15 +144,13 @@ template <int K, typename V, int N> __device__ __forceinline__ void g1x(V (&a)[N
 template <int K, typename V, int N> __device__ __forceinline__ void g1neg(V (&a)[N]) {    // diag(1, -1)
 #pragma unroll
   for (int j = 0; j < N; ++j)
-    if (j & (1 << K)) { a[j].x = -a[j].x; a[j].y = -a[j].y; }
+    if (j & (1 << K)) a[j] = pmul(bc<V>(-1.0f), a[j]);
 }
 template <int K, typename V, int N> __device__ __forceinline__ void g1pi(V (&a)[N], bool neg) {   // diag(1, ±i)
+  V s; s.x = neg ? 1.0f : -1.0f; s.y = neg ? -1.0f : 1.0f;   // i*(x+iy) = (-y, x)
 #pragma unroll
   for (int j = 0; j < N; ++j)
-    if (j & (1 << K)) {
-      const V x = a[j];
-      if (neg) { a[j].x = x.y; a[j].y = -x.x; } else { a[j].x = -x.y; a[j].y = x.x; }
-    }
+    if (j & (1 << K)) a[j] = pmul(s, swp(a[j]));
 }
 template <int KH, int KL, typename V, int N> __device__ __forceinline__ void g2(V (&a)[N], const V* m) {
 #pragma unroll
@@ -155,9 +188,9 @@ template <typename V, int N> __device__ __forceinline__ void cscale(V (&a)[N], V
 }
 template <typename V, int N> __device__ __forceinline__ void rscale(V (&a)[N], double s) {
   typedef decltype(a[0].x) R;
-  const R sc = (R)s;
+  const V sc = bc<V>((R)s);
 #pragma unroll
-  for (int j = 0; j < N; ++j) { a[j].x *= sc; a[j].y *= sc; }
+  for (int j = 0; j < N; ++j) a[j] = pmul(sc, a[j]);
 }
 
 // ---- interpreter for the rare phases in which a trajectory has a non-default
