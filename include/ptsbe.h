@@ -58,6 +58,8 @@ typedef enum { PTSBE_C64 = 0, PTSBE_C128 = 1 } ptsbe_dtype;
 
 /* flags */
 #define PTSBE_DEVICE_PTRS 0x1u  /* pointer arguments are device pointers */
+#define PTSBE_ZERO_VECTOR 0x4u  /* ptsbe_run_range from pass 0: start from the all-zero vector
+                                   instead of |0...0> (every shard but shard 0) */
 #define PTSBE_NO_SYNC     0x2u  /* do not synchronise the stream before returning
                                    (only meaningful with PTSBE_DEVICE_PTRS) */
 
@@ -153,6 +155,25 @@ int ptsbe_set_layout(ptsbe_engine* h, const int32_t* perm);
 int ptsbe_plan(int n_qubits, int n_ops, const uint64_t* target_masks, const uint8_t* general,
                int tile_bits, int low_bits, int search_iters, uint64_t seed,
                int32_t* perm_io, int32_t* out_pass, uint64_t* out_masks, int max_passes);
+
+/* ---- intra-trajectory state sharding (sharded.py drives these per shard) ----
+ * A shard holds the 2^n amplitudes of one global-bit pattern of a 2^(n+k)
+ * state; its program covers segments of local-only ops.
+ *
+ * Run passes [pass_begin, pass_end) of the loaded program; pass_begin == 0
+ * starts from |0...0>, otherwise the B states continue where the previous
+ * range stopped (a global<->local qubit swap may have happened in between). */
+int ptsbe_run_range(ptsbe_engine* h, const uint8_t* sel, int B, int pass_begin, int pass_end,
+                    double* out_weight, int32_t* out_status, uint32_t flags);
+/* Copy the half of state b whose local bit `bit` equals `value` to (unpack = 0)
+ * or from (unpack = 1) the contiguous device buffer `buf` (2^(n-1) amplitudes):
+ * the data movement of a global<->local qubit swap. */
+int ptsbe_exchange_half(ptsbe_engine* h, int b, int bit, int value, void* buf, int unpack);
+/* Exact 2^-62 fixed-point sum of |a|^2 of each of the first B states (the
+ * sampler's CDF total), for splitting shots across shards. */
+int ptsbe_norm_totals(ptsbe_engine* h, int B, uint64_t* out_totals);
+/* Device address of state b (exchange buffers, debugging). */
+void* ptsbe_state_ptr(ptsbe_engine* h, int b);
 
 /* Misc */
 int ptsbe_device_memory(int device, uint64_t* free_bytes, uint64_t* total_bytes);

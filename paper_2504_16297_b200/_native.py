@@ -29,6 +29,7 @@ PTSBE_C128 = 1
 
 PTSBE_DEVICE_PTRS = 0x1
 PTSBE_NO_SYNC = 0x2
+PTSBE_ZERO_VECTOR = 0x4
 
 RNG_PCG64 = 0
 RNG_PHILOX = 1
@@ -68,6 +69,11 @@ SIGNATURES = {
     "ptsbe_set_state": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_uint32]),
     "ptsbe_device_memory": (C.c_int, [C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "ptsbe_set_layout": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "ptsbe_run_range": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                  C.c_uint32]),
+    "ptsbe_exchange_half": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int]),
+    "ptsbe_norm_totals": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "ptsbe_state_ptr": (C.c_void_p, [C.c_void_p, C.c_int]),
     "ptsbe_plan": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_uint64,
                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
     "ptsbe_synchronize": (C.c_int, [C.c_void_p]),

@@ -311,7 +311,7 @@ inline std::string generate(const GenProgram& P) {
         k << "      const uint32_t off[" << N << "] = {";
         for (int j = 0; j < N; ++j) k << off[j] << "u" << (j + 1 < N ? ", " : "");
         k << "};\n"
-          << "      if (p.gen_zero) ptg::zerog(a, base, gb, off, active, GZERO_RE, GZERO_IM);\n"
+          << "      if (p.gen_zero) ptg::zerog(a, base, gb, off, active && p.gen_zero == 1, GZERO_RE, GZERO_IM);\n"
           << "      else ptg::ldg<V, " << N << ", " << pb[0] << ">(a, cur, sg, so, active, scale);\n";
         if (pi == 0)   // a loaded (not synthesized) input also needs the global phase G
           k << "      if (!p.gen_zero) ptg::cscale(a, ptg::mk((V*)0, GZERO_RE, GZERO_IM));\n";

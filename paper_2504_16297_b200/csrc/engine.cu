@@ -93,6 +93,7 @@ struct ptsbe_engine {
   double pass_bytes_total = 0.0;   // algorithmic bytes of profiled pass launches
   // physical layout: logical qubit q stored at physical bit perm[q] (identity unless permuted)
   bool permuted = false;
+  bool zero_vector = false;   // current run starts from the all-zero vector (non-zero shards)
   BitPerm layout{};
   std::vector<uint8_t> logical;   // per state: 1 = stored in logical order (canonicalised)
   // optional per-launch timing of the pass kernels (CUDA events on h->stream)
@@ -164,12 +165,13 @@ size_t pass_smem(const PassHost& P, size_t amp_bytes) {
 }
 
 template <typename R>
-int launch_passes(ptsbe_engine* h, int B, bool from_zero) {
-  const size_t per_slot = (size_t)B;
-  bool prev_general = false;
+int launch_passes(ptsbe_engine* h, int B, bool from_zero, int p_begin = 0, int p_end = -1) {
+  if (p_end < 0) p_end = (int)h->passes.size();
+  // a continued range (sharded segments) inherits the deferred-rescale state
+  bool prev_general = p_begin > 0 ? h->final_general : false;
   if (h->passes.empty()) {
     if (from_zero) {
-      init_zero_kernel<R><<<1184, 256, 0, h->stream>>>(h->states, h->n, B);
+      init_zero_kernel<R><<<1184, 256, 0, h->stream>>>(h->states, h->n, B, h->zero_vector ? 1 : 0);
       CKL(h);
     }
     h->final_general = false;
@@ -185,7 +187,7 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero) {
   const int P = (int)h->passes.size();
   const int trunk = h->cap;
   std::vector<int> fpass(B, 0);
-  const bool tree = from_zero && P >= 2 && h->tree_enabled && !h->host_sel.empty();
+  const bool tree = from_zero && p_begin == 0 && p_end == P && P >= 2 && h->tree_enabled && !h->host_sel.empty();
   if (tree) {
     for (int b = 0; b < B; ++b) {
       int f = P - 1;
@@ -233,7 +235,7 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero) {
     CKL(h);
   }
   int fork_off = 0;
-  for (size_t pi = 0; pi < h->passes.size(); ++pi) {
+  for (size_t pi = (size_t)p_begin; pi < (size_t)p_end; ++pi) {
     const PassHost& ph = h->passes[pi];
     const int E = ent_begin[pi + 1] - ent_begin[pi];
     if (!forks[pi].empty()) {   // forks inherit the trunk's weight / norm / status
@@ -263,7 +265,7 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero) {
     p.mats = h->d_mats;
     p.nst = h->d_nst;
     p.use_scale = prev_general ? 1 : 0;
-    p.gen_zero = (pi == 0 && from_zero) ? 1 : 0;
+    p.gen_zero = (pi == 0 && from_zero) ? (h->zero_vector ? 2 : 1) : 0;
     p.partials = h->d_partials;
     p.status = h->d_status;
     p.B = h->cap + 1;   // row stride (trajectory rows + trunk row)
@@ -310,7 +312,6 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero) {
       h->pass_bytes_total += 2.0 * E * (double)((size_t)1 << h->n) * (double)h->amp_bytes;
     }
     if (ph.n_slots > 0) {
-      (void)per_slot;
       norm_finalize<<<E, 256, 0, h->stream>>>(h->d_partials, ph.n_slots, p.B, p.tiles,
                                               h->d_slot_site + ph.slot_begin, h->d_nst, h->d_weight,
                                               h->d_status, h->d_fail, p.ent);
@@ -358,10 +359,16 @@ int rescale_if_needed(ptsbe_engine* h) {
 }
 
 int run_common(ptsbe_engine* h, const uint8_t* sel, int B, double* out_weight, int32_t* out_status,
-               uint32_t flags, bool from_zero) {
+               uint32_t flags, bool from_zero, int p_begin = 0, int p_end = -1) {
   if (!h) return PTSBE_ERR_VALIDATION;
   if (!h->loaded) return fail(h, PTSBE_ERR_VALIDATION, "no program loaded");
   if (B < 0 || B > h->cap) return fail(h, PTSBE_ERR_VALIDATION, "batch %d exceeds capacity %d", B, h->cap);
+  const int P = (int)h->passes.size();
+  if (p_end < 0) p_end = P;
+  if (p_begin < 0 || p_begin > p_end || p_end > P)
+    return fail(h, PTSBE_ERR_VALIDATION, "pass range [%d, %d) outside [0, %d)", p_begin, p_end, P);
+  if (p_begin > 0 && B != h->last_B)
+    return fail(h, PTSBE_ERR_VALIDATION, "a continued pass range must keep the batch of %d states", h->last_B);
   if (B == 0) return 0;
   CK(h, cudaSetDevice(h->dev));
   h->host_sel.clear();
@@ -377,14 +384,18 @@ int run_common(ptsbe_engine* h, const uint8_t* sel, int B, double* out_weight, i
       std::memcpy(h->host_sel.data(), sel, h->host_sel.size());
     }
   }
-  batch_reset<<<(B + 255) / 256, 256, 0, h->stream>>>(h->d_weight, h->d_nst, h->d_status, h->d_fail, B);
-  CKL(h);
+  if (p_begin == 0) {
+    batch_reset<<<(B + 255) / 256, 256, 0, h->stream>>>(h->d_weight, h->d_nst, h->d_status, h->d_fail, B);
+    CKL(h);
+  }
   if (h->permuted && !from_zero)
     for (int b = 0; b < B; ++b)
       if (int r = relayout(h, b, false)) return r;
   for (int b = 0; b < B; ++b) h->logical[b] = 0;
   h->last_B = B;
-  int r = h->dtype == PTSBE_C64 ? launch_passes<float>(h, B, from_zero) : launch_passes<double>(h, B, from_zero);
+  h->zero_vector = (flags & PTSBE_ZERO_VECTOR) != 0;
+  int r = h->dtype == PTSBE_C64 ? launch_passes<float>(h, B, from_zero, p_begin, p_end)
+                                : launch_passes<double>(h, B, from_zero, p_begin, p_end);
   if (r) return r;
   if (out_weight)
     if (int e = copy_out(h, out_weight, h->d_weight, (size_t)B * 8, flags)) return e;
@@ -562,8 +573,11 @@ int ptsbe_create(int device, int n_qubits, int dtype, int batch_cap, ptsbe_engin
     r = fail(h, PTSBE_ERR_CUDA, "device %d unavailable: %s", device, cudaGetErrorString(e));
   }
   if (!r) {
-    // batch slots + the shared trunk's two alternating slots
-    const size_t bytes = (size_t)(batch_cap + 2) * ((size_t)1 << n_qubits) * h->amp_bytes;
+    // batch slots + the shared trunk's two alternating slots (skipped for huge
+    // states, where two extra copies would not fit next to the batch)
+    const char* tree_env = std::getenv("PTSBE_TREE");
+    h->tree_enabled = tree_env ? std::atoi(tree_env) != 0 : n_qubits <= 30;
+    const size_t bytes = (size_t)(batch_cap + (h->tree_enabled ? 2 : 0)) * ((size_t)1 << n_qubits) * h->amp_bytes;
     e = cudaMalloc(&h->states, bytes);
     if (e != cudaSuccess) r = fail(h, PTSBE_ERR_CUDA, "cannot allocate %zu bytes of state: %s", bytes, cudaGetErrorString(e));
   }
@@ -584,8 +598,6 @@ int ptsbe_create(int device, int n_qubits, int dtype, int batch_cap, ptsbe_engin
     std::vector<int32_t> zeros(batch_cap + 1, 0);
     e = cudaMemcpy(h->d_nst, ones.data(), (batch_cap + 1) * 8, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(h->d_status, zeros.data(), (batch_cap + 1) * 4, cudaMemcpyHostToDevice);
-    const char* tree_env = std::getenv("PTSBE_TREE");
-    h->tree_enabled = !(tree_env && std::atoi(tree_env) == 0);
     if (e != cudaSuccess) r = fail(h, PTSBE_ERR_CUDA, "init copy failed: %s", cudaGetErrorString(e));
   }
   if (r) {
@@ -951,6 +963,62 @@ int ptsbe_run_batch(ptsbe_engine* h, const uint8_t* sel, int B, double* out_weig
 int ptsbe_apply_program(ptsbe_engine* h, const uint8_t* sel, int B, double* out_weight, int32_t* out_status,
                         uint32_t flags) {
   return run_common(h, sel, B, out_weight, out_status, flags, false);
+}
+
+int ptsbe_run_range(ptsbe_engine* h, const uint8_t* sel, int B, int pass_begin, int pass_end, double* out_weight,
+                    int32_t* out_status, uint32_t flags) {
+  return run_common(h, sel, B, out_weight, out_status, flags, pass_begin == 0, pass_begin, pass_end);
+}
+
+int ptsbe_exchange_half(ptsbe_engine* h, int b, int bit, int value, void* buf, int unpack) {
+  if (!h) return PTSBE_ERR_VALIDATION;
+  if (b < 0 || b >= h->cap || bit < 0 || bit >= h->n || (value & ~1) || !buf)
+    return fail(h, PTSBE_ERR_VALIDATION, "bad exchange arguments (state %d, bit %d, value %d)", b, bit, value);
+  CK(h, cudaSetDevice(h->dev));
+  if (h->permuted) return fail(h, PTSBE_ERR_VALIDATION, "sharded exchange needs an unpermuted engine layout");
+  const size_t per = ((size_t)1 << h->n);
+  const unsigned g = (unsigned)std::min<size_t>(per / 512 + 1, 8192);
+  if (h->dtype == PTSBE_C64) {
+    float2* st = reinterpret_cast<float2*>(h->states) + (size_t)b * per;
+    pack_half<float2><<<g, 256, 0, h->stream>>>(st, reinterpret_cast<float2*>(buf), h->n, bit, value, unpack);
+  } else {
+    double2* st = reinterpret_cast<double2*>(h->states) + (size_t)b * per;
+    pack_half<double2><<<g, 256, 0, h->stream>>>(st, reinterpret_cast<double2*>(buf), h->n, bit, value, unpack);
+  }
+  CKL(h);
+  CK(h, cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int ptsbe_norm_totals(ptsbe_engine* h, int B, uint64_t* out_totals) {
+  if (!h) return PTSBE_ERR_VALIDATION;
+  if (B < 0 || B > h->last_B) return fail(h, PTSBE_ERR_VALIDATION, "batch %d exceeds the %d prepared states", B, h->last_B);
+  if (B == 0) return 0;
+  CK(h, cudaSetDevice(h->dev));
+  SampleParams sp{};
+  sp.states = h->states;
+  sp.n = h->n;
+  sp.sbits = h->sbits;
+  sp.nblk = h->nblk;
+  sp.B = B;
+  sp.nst = h->d_nst;
+  sp.status = h->d_status;
+  sp.bs = h->d_bs;
+  sp.total = h->d_total;
+  dim3 g1((unsigned)((h->nblk + 7) / 8), (unsigned)B);
+  if (h->dtype == PTSBE_C64) sample_blocksum<float><<<g1, 256, 0, h->stream>>>(sp);
+  else sample_blocksum<double><<<g1, 256, 0, h->stream>>>(sp);
+  CKL(h);
+  sample_blockscan<<<B, 1024, 0, h->stream>>>(sp);
+  CKL(h);
+  CK(h, cudaMemcpyAsync(out_totals, h->d_total, (size_t)B * 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+void* ptsbe_state_ptr(ptsbe_engine* h, int b) {
+  if (!h || b < 0 || b >= h->cap) return nullptr;
+  return (char*)h->states + (size_t)b * ((size_t)1 << h->n) * h->amp_bytes;
 }
 
 int ptsbe_sample(ptsbe_engine* h, int B, const int64_t* shots, int rng_mode, const uint64_t* rng_state,

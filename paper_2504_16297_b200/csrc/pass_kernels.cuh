@@ -80,7 +80,7 @@ struct PassParams {
   const int32_t* mat_kind;   // [n_mats]
   const double* nst;         // [B] norm^2 of the stored state (used when use_scale)
   int use_scale;
-  int gen_zero;              // first pass: synthesize |0...0> instead of loading
+  int gen_zero;              // first pass: synthesize |0...0> (1) or the zero vector (2) instead of loading
   double* partials;          // [slot][B][tiles]
   const int32_t* status;     // [B]
   int B;                     // trajectory rows (stride of per-row tables)
@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(sizeof(R) == 8 ? 256 : 512) pass_kernel(PassPa
       if (ph == 0 && p.gen_zero) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const bool one = base == 0 && active && (gb | ((j & 1) << p0) | (((j >> 1) & 1) << p1) |
+          const bool one = p.gen_zero == 1 && base == 0 && active && (gb | ((j & 1) << p0) | (((j >> 1) & 1) << p1) |
                                                      (((j >> 2) & 1) << p2) | (((j >> 3) & 1) << p3)) == 0;
           a[j] = make_vec2<V>(one ? 1.0 : 0.0, 0.0);
         }
@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(32) pass_kernel_small(PassParams p) {
   const R scale = (!p.gen_zero && p.use_scale) ? (R)rsqrt(p.nst[b]) : R(1);
   for (uint32_t i = threadIdx.x; i < TL; i += blockDim.x) {
     V v;
-    if (p.gen_zero) { v.x = i == 0 ? R(1) : R(0); v.y = R(0); }
+    if (p.gen_zero) { v.x = (i == 0 && p.gen_zero == 1) ? R(1) : R(0); v.y = R(0); }
     else { v = src[i]; v.x *= scale; v.y *= scale; }
     tile[i] = v;
   }
@@ -550,13 +550,13 @@ __global__ void __launch_bounds__(256) norm_finalize(const double* partials, int
 
 // |0...0> for programs with no passes (empty circuits).
 template <typename R>
-__global__ void init_zero_kernel(void* states, int n, int B) {
+__global__ void init_zero_kernel(void* states, int n, int B, int all_zero = 0) {
   using V = typename Cplx<R>::V;
   V* s = reinterpret_cast<V*>(states);
   const size_t total = (size_t)B << n;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
        i += (size_t)gridDim.x * blockDim.x) {
-    V z; z.x = ((i & ((1ull << n) - 1)) == 0) ? R(1) : R(0); z.y = R(0);
+    V z; z.x = (!all_zero && (i & ((1ull << n) - 1)) == 0) ? R(1) : R(0); z.y = R(0);
     s[i] = z;
   }
 }

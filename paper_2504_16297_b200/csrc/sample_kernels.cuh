@@ -398,6 +398,19 @@ __global__ void permute_state(const V* in, V* out, int n, BitPerm P) {
     out[permute_bits(i, P)] = in[i];
 }
 
+// State sharding: the half of a shard whose local bit `bit` equals `value`,
+// packed contiguously (index order) for a global<->local qubit swap.
+template <typename V>
+__global__ void pack_half(const V* st, V* buf, int n, int bit, int value, int unpack) {
+  const size_t half = 1ull << (n - 1);
+  const size_t lowm = (1ull << bit) - 1ull;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < half; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t src = ((i & ~lowm) << 1) | ((size_t)value << bit) | (i & lowm);
+    if (unpack) const_cast<V*>(st)[src] = buf[i];
+    else buf[i] = st[src];
+  }
+}
+
 // Gather each trajectory's runs into one contiguous CSR stream.
 __global__ void compact_runs(const uint64_t* run_idx, const uint32_t* run_cnt, const int64_t* off,
                              const int64_t* nuniq, const int64_t* uoff, uint64_t* out_idx, uint32_t* out_cnt) {

@@ -216,3 +216,33 @@ def pcg64_state_words(seed_or_rng) -> np.ndarray:
     s, inc = int(st["state"]["state"]), int(st["state"]["inc"])
     m = (1 << 64) - 1
     return np.array([s >> 64, s & m, inc >> 64, inc & m], dtype=np.uint64)
+
+
+def _engine_sharding_methods():
+    """Sharding primitives on Engine (ptsbe_run_range / exchange_half / norm_totals)."""
+
+    def run_range(self, sel, pass_begin: int, pass_end: int, zero_vector: bool = False):
+        sel = np.ascontiguousarray(sel, dtype=np.uint8)
+        B = sel.shape[0]
+        w = np.empty(B, dtype=np.float64)
+        s = np.empty(B, dtype=np.int32)
+        flags = N.PTSBE_ZERO_VECTOR if zero_vector else 0
+        self._check(self.lib.ptsbe_run_range(self.h, _ptr(sel), B, int(pass_begin), int(pass_end), _ptr(w),
+                                             _ptr(s), flags), "ptsbe_run_range")
+        return w, s
+
+    def exchange_half(self, b: int, bit: int, value: int, buf_ptr: int, unpack: bool):
+        self._check(self.lib.ptsbe_exchange_half(self.h, int(b), int(bit), int(value), C.c_void_p(buf_ptr),
+                                                 1 if unpack else 0), "ptsbe_exchange_half")
+
+    def norm_totals(self, B: int) -> np.ndarray:
+        out = np.zeros(B, dtype=np.uint64)
+        self._check(self.lib.ptsbe_norm_totals(self.h, int(B), _ptr(out)), "ptsbe_norm_totals")
+        return out
+
+    Engine.run_range = run_range
+    Engine.exchange_half = exchange_half
+    Engine.norm_totals = norm_totals
+
+
+_engine_sharding_methods()

@@ -1,0 +1,310 @@
+"""Intra-trajectory state sharding for states too large for one GPU.
+
+A state of ``n`` qubits is split over ``D = 2^k`` shards: shard ``s`` holds the
+``2^(n-k)`` amplitudes whose top ``k`` physical bits equal ``s``.  Logical
+qubits move between *local* bits (inside a shard) and *global* bits (the shard
+index):
+
+* the op stream (reference order, ``execute.py:85-97``) is cut into
+  **segments** whose ops touch local qubits only; inside a segment every
+  shard runs the same fused passes on its own amplitudes (the global bits are
+  spectators), so a segment is just a pass range of an ordinary program
+  compiled for ``n - k`` qubits (``ptsbe_run_range``);
+* between segments a global qubit is **swapped** with a local one: each shard
+  exchanges the half of its amplitudes whose local bit differs from its
+  global bit with the partner shard ``s ^ (1 << g)`` (``ptsbe_exchange_half``:
+  pack -> send/recv -> unpack).  The victim local qubit is the one used
+  furthest in the future (Belady), so swaps are rare;
+* sampling: each shard's exact fixed-point CDF total (``ptsbe_norm_totals``,
+  integers, so the split is exact) gives the multinomial split of the
+  trajectory's shots over shards; every shard draws its share with its own
+  Philox stream and the physical indices are mapped back to logical
+  bitstrings.  (Bit-exact PCG64 replay needs the logical CDF order and is
+  offered by the unsharded engine only.)
+
+Transports: ``VirtualShards`` keeps all shards in one process (one device;
+used by the GPU tests), ``DistributedShards`` runs one shard per rank and
+exchanges halves with ``torch.distributed`` point-to-point ops (NCCL over
+NVLink on a B200 box; gloo in the CPU tests).  Renormalising (general)
+channels need a cross-shard norm and are rejected here.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from .errors import ValidationError
+from .execute import mix_seed
+from .program import Program, lower, plan_native, selection_matrix
+
+
+@dataclass
+class ShardPlan:
+    n: int
+    k: int
+    segments: list                 # per segment: (pass_begin, pass_end)
+    swaps: list                    # per segment: [(global bit g, local bit l)] applied AFTER it
+    final_map: dict                # logical qubit -> ("L", bit) | ("G", bit)
+    program: Program               # program over n - k local qubits
+    initial_map: dict = field(default_factory=dict)
+
+    @property
+    def n_local(self) -> int:
+        return self.n - self.k
+
+    @property
+    def n_swaps(self) -> int:
+        return sum(len(s) for s in self.swaps)
+
+
+def _next_use(stream, start, q):
+    for i in range(start, len(stream)):
+        if q in stream[i].targets:
+            return i
+    return len(stream) + 1
+
+
+def plan_sharded(circuit, k: int, dtype: str = "c64", tile_bits: int | None = None,
+                 low_bits: int | None = None) -> ShardPlan:
+    """Segments of local-only ops with global<->local swaps between them."""
+    from .program import DEFAULT_LOW_BITS, DEFAULT_TILE_BITS
+    n = circuit.n_qubits
+    if not 1 <= k < n - 2:
+        raise ValidationError(f"cannot shard {n} qubits over 2^{k} shards")
+    prog = lower(circuit)
+    if any(so.general for so in prog.stream):
+        raise ValidationError("sharded execution supports unitary-mixture channels only")
+    stream = prog.stream
+    nl = n - k
+    # initial layout: the k qubits used latest are global; local bits by usage (busiest lowest)
+    first_use = {q: _next_use(stream, 0, q) for q in range(n)}
+    glob = sorted(range(n), key=lambda q: (-first_use[q], q))[:k]
+    uses = {q: sum(q in so.targets for so in stream) for q in range(n)}
+    local = sorted((q for q in range(n) if q not in glob), key=lambda q: (-uses[q], q))
+    where = {q: ("L", i) for i, q in enumerate(local)}
+    where.update({q: ("G", i) for i, q in enumerate(glob)})
+    initial = dict(where)
+    segments_ops, swaps, cur = [], [], []
+    for idx, so in enumerate(stream):
+        need = [q for q in so.targets if where[q][0] == "G"]
+        if need:
+            segments_ops.append((cur, dict(where)))
+            cur = []
+            sw = []
+            for q in need:
+                cands = [r for r in range(n) if where[r][0] == "L" and r not in so.targets]
+                victim = max(cands, key=lambda r: (_next_use(stream, idx, r), -r))
+                g, l = where[q][1], where[victim][1]
+                where[q], where[victim] = ("L", l), ("G", g)
+                sw.append((g, l))
+            swaps.append(sw)
+        cur.append(idx)
+    segments_ops.append((cur, dict(where)))
+    swaps.append([])
+    # one program over the local qubits: segments' passes back to back
+    L = tile_bits if tile_bits is not None else DEFAULT_TILE_BITS[dtype]
+    c = low_bits if low_bits is not None else DEFAULT_LOW_BITS[dtype]
+    new_stream, passes, ranges = [], [], []
+    for ops, mapping in segments_ops:
+        seg_stream = [replace(stream[i], targets=tuple(mapping[q][1] for q in stream[i].targets)) for i in ops]
+        base = len(new_stream)
+        new_stream.extend(seg_stream)
+        p0 = len(passes)
+        if seg_stream:
+            _, seg_passes = plan_native(nl, seg_stream, L, c, search_iters=0)
+            for pp in seg_passes:
+                pp.ops = [base + i for i in pp.ops]
+            passes.extend(seg_passes)
+        ranges.append((p0, len(passes)))
+    sprog = Program(nl, new_stream, prog.mats, prog.chans, prog.chan_index, prog.site_chan,
+                    passes=passes, g_ref=prog.g_ref, perm=None)
+    return ShardPlan(n, k, ranges, swaps, dict(where), sprog, initial)
+
+
+def physical_to_logical(shard: np.ndarray, local_idx: np.ndarray, plan: ShardPlan) -> np.ndarray:
+    """Logical basis index of (shard, local index) pairs under the final layout."""
+    out = np.zeros(local_idx.shape, dtype=np.uint64)
+    s = shard.astype(np.uint64)
+    li = local_idx.astype(np.uint64)
+    for q, (kind, bit) in plan.final_map.items():
+        src = li if kind == "L" else s
+        out |= ((src >> np.uint64(bit)) & np.uint64(1)) << np.uint64(q)
+    return out
+
+
+def _split_shots(totals: np.ndarray, m: int, seed: int) -> np.ndarray:
+    """Multinomial split of m shots over shards with exact integer weights."""
+    if m == 0:
+        return np.zeros(totals.size, dtype=np.int64)
+    t = totals.astype(np.float64)
+    p = t / t.sum()
+    rng = np.random.Generator(np.random.PCG64(seed))
+    return rng.multinomial(m, p).astype(np.int64)
+
+
+class VirtualShards:
+    """All 2^k shards in one process on one device (GPU tests, single-GPU validation)."""
+
+    def __init__(self, plan: ShardPlan, dtype: str = "c64", batch_cap: int = 1, device: int = 0):
+        from .engine import Engine
+        self.plan = plan
+        self.dtype = dtype
+        self.D = 1 << plan.k
+        self.engines = [Engine(plan.n_local, dtype, batch_cap=batch_cap, device=device) for _ in range(self.D)]
+        for e in self.engines:
+            e.load_program(plan.program)
+
+    def close(self):
+        for e in self.engines:
+            e.close()
+
+    def _swap(self, B, g, l):
+        import torch
+        dev = torch.device("cuda", self.engines[0].device)
+        cdt = torch.complex64 if self.dtype == "c64" else torch.complex128
+        half = 1 << (self.plan.n_local - 1)
+        for b in range(B):
+            bufs = [torch.empty(half, dtype=cdt, device=dev) for _ in range(self.D)]
+            for s, e in enumerate(self.engines):
+                e.exchange_half(b, l, 1 - ((s >> g) & 1), bufs[s].data_ptr(), unpack=False)
+            for s, e in enumerate(self.engines):
+                partner = s ^ (1 << g)
+                e.exchange_half(b, l, 1 - ((s >> g) & 1), bufs[partner].data_ptr(), unpack=True)
+
+    def run(self, sel: np.ndarray):
+        B = sel.shape[0]
+        for i, (p0, p1) in enumerate(self.plan.segments):
+            for s, e in enumerate(self.engines):   # only shard 0 holds |0...0> initially
+                e.run_range(sel, p0, p1, zero_vector=(p0 == 0 and s != 0))
+            for g, l in self.plan.swaps[i]:
+                self._swap(B, g, l)
+
+    def sample(self, shots, seeds):
+        """Philox shots per trajectory -> list of (logical indices sorted, counts)."""
+        from . import _native as N
+        shots = np.asarray(shots, dtype=np.int64)
+        B = shots.size
+        totals = np.stack([e.norm_totals(B) for e in self.engines], axis=1)   # (B, D)
+        split = np.stack([_split_shots(totals[b], int(shots[b]), int(seeds[b])) for b in range(B)])
+        per_traj = [[] for _ in range(B)]
+        for s, e in enumerate(self.engines):
+            keys = np.array([mix_seed(int(seeds[b]), s) for b in range(B)], dtype=np.uint64)
+            out = e.sample(split[:, s], N.RNG_PHILOX, rng_state=keys)
+            for b in range(B):
+                lo, hi = out.offsets[b], out.offsets[b + 1]
+                idx = physical_to_logical(np.full(hi - lo, s), out.indices[lo:hi], self.plan)
+                per_traj[b].append((idx, out.counts[lo:hi]))
+        result = []
+        for b in range(B):
+            idx = np.concatenate([x[0] for x in per_traj[b]]) if per_traj[b] else np.zeros(0, np.uint64)
+            cnt = np.concatenate([x[1] for x in per_traj[b]]) if per_traj[b] else np.zeros(0, np.uint32)
+            order = np.argsort(idx, kind="stable")
+            result.append((idx[order], cnt[order]))
+        return result
+
+    def logical_state(self, b: int = 0) -> np.ndarray:
+        """Assemble the full logical state of trajectory b (tests / small n)."""
+        nl = self.plan.n_local
+        parts = [e.get_state(b) for e in self.engines]
+        phys_local = np.arange(1 << nl, dtype=np.uint64)
+        out = np.zeros(1 << self.plan.n, dtype=parts[0].dtype)
+        for s, amp in enumerate(parts):
+            out[physical_to_logical(np.full(phys_local.size, s), phys_local, self.plan).astype(np.int64)] = amp
+        return out
+
+
+class DistributedShards:
+    """One shard per rank (one process per GPU); swaps over torch.distributed P2P (NCCL)."""
+
+    def __init__(self, plan: ShardPlan, backend, dtype: str = "c64", group=None):
+        import torch.distributed as dist
+        self.plan = plan
+        self.dtype = dtype
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        if self.world != 1 << plan.k:
+            raise ValidationError(f"{self.world} ranks for 2^{plan.k} shards")
+        self.backend = backend      # object with run_range / exchange_half / norm_totals / sample / device tensors
+
+    def run(self, sel: np.ndarray):
+        import torch.distributed as dist
+        B = sel.shape[0]
+        s = self.rank
+        for i, (p0, p1) in enumerate(self.plan.segments):
+            self.backend.run_range(sel, p0, p1, p0 == 0 and s != 0)
+            for g, l in self.plan.swaps[i]:
+                partner = s ^ (1 << g)
+                v = 1 - ((s >> g) & 1)
+                for b in range(B):
+                    send = self.backend.half_buffer()
+                    recv = self.backend.half_buffer()
+                    self.backend.exchange_half(b, l, v, send, unpack=False)
+                    reqs = dist.batch_isend_irecv([dist.P2POp(dist.isend, send, partner, self.group),
+                                                   dist.P2POp(dist.irecv, recv, partner, self.group)])
+                    for r in reqs:
+                        r.wait()
+                    self.backend.exchange_half(b, l, v, recv, unpack=True)
+
+    def sample(self, shots, seeds):
+        """Returns per-trajectory (logical indices, counts) on rank 0, None elsewhere."""
+        import torch
+        import torch.distributed as dist
+        shots = np.asarray(shots, dtype=np.int64)
+        B = shots.size
+        mine = torch.tensor(self.backend.norm_totals(B).astype(np.int64))
+        allt = [torch.zeros_like(mine) for _ in range(self.world)]
+        dist.all_gather(allt, mine, group=self.group)
+        totals = np.stack([t.numpy().astype(np.uint64) for t in allt], axis=1)
+        split = np.stack([_split_shots(totals[b], int(shots[b]), int(seeds[b])) for b in range(B)])
+        keys = np.array([mix_seed(int(seeds[b]), self.rank) for b in range(B)], dtype=np.uint64)
+        local = self.backend.sample(split[:, self.rank], keys)      # list of (local idx, counts)
+        mapped = [(physical_to_logical(np.full(ix.size, self.rank), ix, self.plan), ct) for ix, ct in local]
+        gathered = [None] * self.world if self.rank == 0 else None
+        dist.gather_object(mapped, gathered, dst=0, group=self.group)
+        if self.rank != 0:
+            return None
+        result = []
+        for b in range(B):
+            idx = np.concatenate([g[b][0] for g in gathered])
+            cnt = np.concatenate([g[b][1] for g in gathered])
+            order = np.argsort(idx, kind="stable")
+            result.append((idx[order], cnt[order]))
+        return result
+
+
+def sharded_selection(plan: ShardPlan, specs) -> np.ndarray:
+    return selection_matrix(plan.program, specs)
+
+
+class EngineShardBackend:
+    """This rank's shard on its GPU, for DistributedShards (NCCL exchanges)."""
+
+    def __init__(self, plan: ShardPlan, dtype: str = "c64", batch_cap: int = 1, device: int = 0):
+        from .engine import Engine
+        self.plan = plan
+        self.dtype = dtype
+        self.engine = Engine(plan.n_local, dtype, batch_cap=batch_cap, device=device)
+        self.engine.load_program(plan.program)
+
+    def half_buffer(self):
+        import torch
+        cdt = torch.complex64 if self.dtype == "c64" else torch.complex128
+        return torch.empty(1 << (self.plan.n_local - 1), dtype=cdt, device=torch.device("cuda", self.engine.device))
+
+    def run_range(self, sel, p0, p1, zero_vector=False):
+        self.engine.run_range(sel, p0, p1, zero_vector=zero_vector)
+
+    def exchange_half(self, b, bit, value, buf, unpack):
+        self.engine.exchange_half(b, bit, value, buf.data_ptr(), unpack)
+
+    def norm_totals(self, B):
+        return self.engine.norm_totals(B)
+
+    def sample(self, shots, keys):
+        from . import _native as N
+        out = self.engine.sample(shots, N.RNG_PHILOX, rng_state=keys)
+        return [(out.indices[out.offsets[b]:out.offsets[b + 1]], out.counts[out.offsets[b]:out.offsets[b + 1]])
+                for b in range(len(shots))]
