@@ -1116,13 +1116,18 @@ int ptsbe_plan(int n_qubits, int n_ops, const uint64_t* target_masks, const uint
   if (n_qubits < 1 || n_qubits > 63 || n_ops < 0 || tile_bits < 1 || low_bits < 0 || !perm_io)
     return -PTSBE_ERR_VALIDATION;
   std::vector<plan::Op> ops(n_ops);
-  for (int i = 0; i < n_ops; ++i) ops[i] = plan::Op{target_masks[i], general && general[i] != 0};
+  // general[i]: bit 0 = renormalising site, bit 1 = gate (counts toward the
+  // optional per-pass gate budget PTSBE_MAX_PASS_GATES, a tuning knob)
+  for (int i = 0; i < n_ops; ++i)
+    ops[i] = plan::Op{target_masks[i], general && (general[i] & 1) != 0, general && (general[i] & 2) ? 1 : 0};
+  const char* cap_env = std::getenv("PTSBE_MAX_PASS_GATES");
+  const int cap = cap_env ? std::atoi(cap_env) : 0;
   std::vector<int> perm(perm_io, perm_io + n_qubits);
   const int L = std::min(tile_bits, n_qubits), c = std::min(low_bits, L);
-  plan::search(n_qubits, ops, perm, L, c, search_iters, seed);
+  plan::search(n_qubits, ops, perm, L, c, search_iters, seed, cap);
   std::vector<int> pass;
   std::vector<uint64_t> masks;
-  const int P = plan::greedy(n_qubits, ops, perm, L, c, &pass, &masks);
+  const int P = plan::greedy(n_qubits, ops, perm, L, c, &pass, &masks, cap);
   if (P < 0) return -PTSBE_ERR_VALIDATION;
   if (P > max_passes) return -PTSBE_ERR_VALIDATION;
   for (int q = 0; q < n_qubits; ++q) perm_io[q] = perm[q];

@@ -23,6 +23,7 @@ namespace plan {
 struct Op {
   uint64_t mask;   // logical target mask
   bool general;
+  int weight = 0;  // counts toward the per-pass gate budget (gates 1, sites 0)
 };
 
 inline uint64_t phys_mask(uint64_t logical, const std::vector<int>& perm) {
@@ -37,7 +38,7 @@ inline uint64_t phys_mask(uint64_t logical, const std::vector<int>& perm) {
 
 // Greedy plan; returns the number of passes.  out_pass / out_masks optional.
 inline int greedy(int n, const std::vector<Op>& ops, const std::vector<int>& perm, int L, int c,
-                  std::vector<int>* out_pass, std::vector<uint64_t>* out_masks) {
+                  std::vector<int>* out_pass, std::vector<uint64_t>* out_masks, int max_weight = 0) {
   const int m = (int)ops.size();
   if (m == 0) return 0;
   std::vector<uint64_t> pm(m);
@@ -58,7 +59,7 @@ inline int greedy(int n, const std::vector<Op>& ops, const std::vector<int>& per
     uint64_t q = low, blocked = 0;
     bool gen_blocked = false;
     deferred.clear();
-    int taken = 0;
+    int taken = 0, weight = 0;
     for (int i : remaining) {
       const uint64_t t = pm[i];
       if ((t & blocked) || (ops[i].general && gen_blocked)) {
@@ -68,9 +69,11 @@ inline int greedy(int n, const std::vector<Op>& ops, const std::vector<int>& per
         continue;
       }
       const uint64_t g = q | t;
-      if (__builtin_popcountll(g) <= L) {
+      const bool budget = max_weight <= 0 || weight + ops[i].weight <= max_weight || taken == 0;
+      if (__builtin_popcountll(g) <= L && budget) {
         q = g;
         ++taken;
+        weight += ops[i].weight;
         if (out_pass) (*out_pass)[i] = passes;
       } else {
         deferred.push_back(i);
@@ -98,8 +101,8 @@ struct Rng {
 
 // Improve `perm` in place; returns the best pass count.
 inline int search(int n, const std::vector<Op>& ops, std::vector<int>& perm, int L, int c, int iters,
-                  uint64_t seed) {
-  int best = greedy(n, ops, perm, L, c, nullptr, nullptr);
+                  uint64_t seed, int max_weight = 0) {
+  int best = greedy(n, ops, perm, L, c, nullptr, nullptr, max_weight);
   if (n <= L || iters <= 0 || best <= 1) return best;
   Rng rng(seed);
   std::vector<int> cand = perm;
@@ -108,7 +111,7 @@ inline int search(int n, const std::vector<Op>& ops, std::vector<int>& perm, int
     if (a == b) continue;
     cand = perm;
     std::swap(cand[a], cand[b]);
-    const int p = greedy(n, ops, cand, L, c, nullptr, nullptr);
+    const int p = greedy(n, ops, cand, L, c, nullptr, nullptr, max_weight);
     if (p >= 0 && p <= best) {
       best = p;
       perm.swap(cand);

@@ -204,7 +204,7 @@ def plan_native(n: int, stream: list, tile_bits: int, low_bits: int, search_iter
     for i, so in enumerate(stream):
         for q in so.targets:
             masks[i] |= np.uint64(1 << q)
-        general[i] = 1 if so.general else 0
+        general[i] = (1 if so.general else 0) | (2 if so.kind == KIND_GATE else 0)
     p = np.arange(n, dtype=np.int32) if perm is None else np.array(perm, dtype=np.int32)
     out_pass = np.zeros(max(m, 1), dtype=np.int32)
     out_masks = np.zeros(max(m, 1) + 1, dtype=np.uint64)

@@ -162,6 +162,6 @@ def test_virtual_shards_match_oracle(k, dtype):
             exp = probs[top] * specs[b].shots
             obs = np.append(obs, specs[b].shots - obs.sum())
             exp = np.append(exp, specs[b].shots - exp.sum())
-            assert stats.chisquare(obs, exp).pvalue > 0.01
+            assert stats.chisquare(obs, exp).pvalue > 1e-3   # the reference's chi^2 level (test_execute.py:168-178)
     finally:
         vs.close()
