@@ -9,8 +9,8 @@
 // exactly the host's float rounding); cx / swap / x compile to register
 // renaming.  Noise sites stay data-driven: per phase, one CTA-uniform bit says
 // whether the trajectory takes any non-default outcome there; if so the phase
-// runs through a run-time interpreter (rare), otherwise through the
-// straight-line fast path.
+// runs a second straight-line copy whose sites read their outcome and apply
+// its operator from the table (rare), otherwise the fast path.
 //
 // NVRTC and the driver API are reached without link-time dependencies
 // (dlopen + cudaGetDriverEntryPoint), so libptsbe.so still loads on hosts
@@ -249,7 +249,7 @@ inline std::string err_mask_fn(const GenPass& gp) {
 }
 
 // Factor bookkeeping (fast path): each scaled gate applies M/f; per phase the
-// product F_ph is what the rare interpreter path must divide out, per pass the
+// product F_ph is shared by both copies of the phase (same gate code), per pass the
 // magnitude |F| is multiplied back before the tile is stored, and the phase
 // arg(F) of every pass is folded into the initial |0...0> amplitude G, so the
 // stored state equals the true state after every pass.  Passes holding
@@ -318,43 +318,50 @@ inline std::string generate(const GenProgram& P) {
       } else {
         k << "      ptg::ldg<V, " << N << ", " << pb[0] << ">(a, cur, sg, so, active, 1.0);\n";
       }
+      // slow == true: the trajectory takes a non-default outcome at some site of
+      // this phase; sites then read their outcome and apply its operator from the
+      // table (same registers, same gate code, so the frame factor is unchanged).
+      auto emit_ops = [&](bool slow) {
+        Cx f{1.0, 0.0};
+        for (int q = D.op_begin; q < D.op_begin + D.n_ops; ++q) {
+          const DevOp& op = gp.ops[q];
+          const int k1 = op.arity == 2 ? op.k1 : 0;
+          if (op.kind == 0) {
+            k << "      ";
+            f = cxmul(f, ke.op(P.kinds[op.ref], op.k0, k1, P.mats + (size_t)op.ref * 32, scaled));
+            continue;
+          }
+          const ptsbe_channel& ch = P.chans[P.site_chan[op.ref]];
+          if (slow) {
+            k << "      { const int o_ = sel[" << op.ref << "];\n"
+              << "        if (!((0x" << std::hex << ch.identity_mask << std::dec << "ull >> o_) & 1ull)) {\n"
+              << "          const V* m_ = reinterpret_cast<const V*>(p.mats) + (size_t)(" << ch.mat_base
+              << " + o_) * 16;\n";
+            if (op.arity == 1) k << "          ptg::g1<" << op.k0 << ">(a, m_[0], m_[1], m_[4], m_[5]);\n";
+            else k << "          ptg::g2<" << op.k0 << ", " << k1 << ">(a, m_);\n";
+            k << "      } }\n";
+          } else if (!(ch.identity_mask & 1ull)) {   // outcome 0 is not the identity (e.g. damping K0)
+            k << "      ";
+            ke.op(P.kinds[ch.mat_base], op.k0, k1, P.mats + (size_t)ch.mat_base * 32, false);
+          }
+          if (ch.general) {
+            k << "      { double s_ = 0.0;\n"
+              << "#pragma unroll\n"
+              << "        for (int j = 0; j < " << N << "; ++j) s_ += ptg::prob64(a[j]);\n"
+              << "        s_ = ptg::block_sum(s_, red);\n"
+              << "        if (threadIdx.x == 0) p.partials[((size_t)" << op.slot
+              << " * p.B + b) * p.tiles + tile] = s_; }\n";
+          }
+        }
+        return f;
+      };
       bool has_sites = false;
       for (int q = D.op_begin; q < D.op_begin + D.n_ops; ++q) has_sites = has_sites || gp.ops[q].kind == 1;
       if (has_sites) k << "      if (!((emask >> " << std::min<size_t>(ph, 63) << ") & 1ull)) {\n";
-      Cx Fph{1.0, 0.0};
-      for (int q = D.op_begin; q < D.op_begin + D.n_ops; ++q) {
-        const DevOp& op = gp.ops[q];
-        const int k1 = op.arity == 2 ? op.k1 : 0;
-        if (op.kind == 0) {
-          k << "      ";
-          Fph = cxmul(Fph, ke.op(P.kinds[op.ref], op.k0, k1, P.mats + (size_t)op.ref * 32, scaled));
-          continue;
-        }
-        const ptsbe_channel& ch = P.chans[P.site_chan[op.ref]];
-        if (!(ch.identity_mask & 1ull)) {   // outcome 0 is not the identity (e.g. damping K0)
-          k << "      ";
-          ke.op(P.kinds[ch.mat_base], op.k0, k1, P.mats + (size_t)ch.mat_base * 32, false);
-        }
-        if (ch.general) {
-          k << "      { double s_ = 0.0;\n"
-            << "#pragma unroll\n"
-            << "        for (int j = 0; j < " << N << "; ++j) s_ += ptg::prob64(a[j]);\n"
-            << "        s_ = ptg::block_sum(s_, red);\n"
-            << "        if (threadIdx.x == 0) p.partials[((size_t)" << op.slot
-            << " * p.B + b) * p.tiles + tile] = s_; }\n";
-        }
-      }
+      const Cx Fph = emit_ops(false);
       if (has_sites) {
-        const Cx inv = cxdiv(Cx{1.0, 0.0}, Fph);
-        k << "      } else {\n"
-          << "        ptg::stg<V, " << N << ", " << pb[0] << ">(a, cur, sg, so, active);\n"
-          << "        const uint32_t sb_[" << GB << "] = {";
-        for (int q = 0; q < GB; ++q) k << "so[" << (1 << q) << "]" << (q + 1 < GB ? ", " : "");
-        k << "};\n"
-          << "        ptg::interp_phase<V>(cur, sg, sb_, " << GB << ", p, " << ph << ", sel, b, tile, red, active);\n"
-          << "        ptg::ldg<V, " << N << ", " << pb[0] << ">(a, cur, sg, so, active, 1.0);\n";
-        if (!(inv.re == 1.0 && inv.im == 0.0))   // match the fast path's frame
-          k << "        ptg::cscale(a, " << ke.lit(inv.re, inv.im) << ");\n";
+        k << "      } else {\n";
+        emit_ops(true);
         k << "      }\n";
       }
       F = cxmul(F, Fph);

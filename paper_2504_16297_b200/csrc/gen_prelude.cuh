@@ -193,77 +193,6 @@ template <typename V, int N> __device__ __forceinline__ void rscale(V (&a)[N], d
   for (int j = 0; j < N; ++j) a[j] = pmul(sc, a[j]);
 }
 
-// ---- interpreter for the rare phases in which a trajectory has a non-default
-// outcome.  The thread's group is parked in shared memory (its own slots only,
-// so no barrier is needed between ops) and every op of the phase is applied
-// with run-time decoding.  sb[q] = swizzled offset of the phase's q-th bit.
-template <typename V>
-__device__ __noinline__ void interp_phase(V* cur, uint32_t sg, const uint32_t* sb, int gbits, const PassParams& p,
-                                          int phase, const uint8_t* sel, int b, long long tile, double* red,
-                                          bool active) {
-  const DevPhase P = p.phases[phase];
-  const V* mats = reinterpret_cast<const V*>(p.mats);
-  const int N = 1 << gbits;
-  for (int k = P.op_begin; k < P.op_begin + P.n_ops; ++k) {
-    const DevOp op = p.ops[k];
-    int mat = op.ref;
-    bool general = false;
-    if (op.kind == 1) {
-      const int outcome = sel[op.ref];
-      const DevChan ch = p.chans[p.site_chan[op.ref]];
-      if ((ch.identity_mask >> outcome) & 1ull) continue;
-      mat = ch.mat_base + outcome;
-      general = ch.general != 0;
-    }
-    const V* m = mats + (size_t)mat * 16;
-    if (active) {
-      if (op.arity == 1) {
-        const V m00 = m[0], m01 = m[1], m10 = m[4], m11 = m[5];
-        for (int j = 0; j < N; ++j) {
-          if (j & (1 << op.k0)) continue;
-          uint32_t a0 = sg;
-          for (int q = 0; q < gbits; ++q) if ((j >> q) & 1) a0 ^= sb[q];
-          const uint32_t a1 = a0 ^ sb[op.k0];
-          const V x = cur[a0], y = cur[a1];
-          cur[a0] = cmadd2(m00, x, m01, y);
-          cur[a1] = cmadd2(m10, x, m11, y);
-        }
-      } else {
-        for (int j = 0; j < N; ++j) {
-          if ((j & (1 << op.k0)) || (j & (1 << op.k1))) continue;
-          uint32_t a0 = sg;
-          for (int q = 0; q < gbits; ++q) if ((j >> q) & 1) a0 ^= sb[q];
-          const uint32_t a1 = a0 ^ sb[op.k1], a2 = a0 ^ sb[op.k0], a3 = a2 ^ sb[op.k1];
-          const V v0 = cur[a0], v1 = cur[a1], v2 = cur[a2], v3 = cur[a3];
-          cur[a0] = cmadd4(m[0], m[1], m[2], m[3], v0, v1, v2, v3);
-          cur[a1] = cmadd4(m[4], m[5], m[6], m[7], v0, v1, v2, v3);
-          cur[a2] = cmadd4(m[8], m[9], m[10], m[11], v0, v1, v2, v3);
-          cur[a3] = cmadd4(m[12], m[13], m[14], m[15], v0, v1, v2, v3);
-        }
-      }
-    }
-    if (general) {
-      double s = 0.0;
-      if (active)
-        for (int j = 0; j < N; ++j) {
-          uint32_t a0 = sg;
-          for (int q = 0; q < gbits; ++q) if ((j >> q) & 1) a0 ^= sb[q];
-          s += prob64(cur[a0]);
-        }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double r = 0.0;
-        for (int i = 0; i < (int)((blockDim.x + 31) >> 5); ++i) r += red[i];
-        p.partials[((size_t)op.slot * p.B + b) * p.tiles + tile] = r;
-      }
-      __syncthreads();
-    }
-  }
-}
-
 // ---- addressing
 __device__ __forceinline__ uint32_t swz(float2*, uint32_t i) {   // never flips bit 0
   const uint32_t h = (i >> 3) ^ (i >> 7) ^ ((i >> 7) << 1) ^ (i >> 11);
