@@ -195,6 +195,7 @@ def main():
     ap.add_argument("--seed", type=int, default=2024)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--rng", default="philox", choices=["philox", "pcg64"])
+    ap.add_argument("--tile-bits", type=int, default=None, help="fused-pass tile qubits (default: planner's)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -218,7 +219,7 @@ def main():
     # deterministic deal by trajectory id: rank r owns ids [r*per_rank, (r+1)*per_rank)
     ids = list(range(rank * per_rank, (rank + 1) * per_rank))
     specs = [specs_all[i] for i in ids]
-    prog = compile_circuit(c, args.dtype)
+    prog = compile_circuit(c, args.dtype, tile_bits=args.tile_bits)
     eng = Engine(c.n_qubits, args.dtype, batch_cap=B, device=local)
     eng.load_program(prog)
     sel = selection_matrix(prog, specs)

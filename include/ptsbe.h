@@ -175,6 +175,15 @@ int ptsbe_norm_totals(ptsbe_engine* h, int B, uint64_t* out_totals);
 /* Device address of state b (exchange buffers, debugging). */
 void* ptsbe_state_ptr(ptsbe_engine* h, int b);
 
+/* ---- offline tooling (no GPU): a host-only handle runs ptsbe_load_program's
+ * validation, pass/phase planning and kernel generation, and keeps the
+ * generated CUDA source instead of compiling it (tools/gen_offline.py
+ * compiles it with nvcc for SASS inspection).  Compute calls on it fail. */
+int ptsbe_create_host(int n_qubits, int dtype, ptsbe_engine** out);
+/* Copies up to len-1 bytes of the generated source (NUL-terminated) into buf
+ * (buf may be NULL); returns the full source length. */
+int64_t ptsbe_codegen_source(ptsbe_engine* h, char* buf, size_t len);
+
 /* Misc */
 int ptsbe_device_memory(int device, uint64_t* free_bytes, uint64_t* total_bytes);
 int ptsbe_synchronize(ptsbe_engine* h);

@@ -11,7 +11,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT = PKG / "libptsbe.so"
 SOURCES = [CSRC / "engine.cu"]
-DEPS = SOURCES + sorted(CSRC.glob("*.cuh")) + [PKG.parent / "include" / "ptsbe.h"]
+DEPS = SOURCES + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h")) + [PKG.parent / "include" / "ptsbe.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -211,7 +211,25 @@ struct GenProgram {
 
 inline std::string kernel_name(int pass) { return "ptsbe_pass_" + std::to_string(pass); }
 
-inline int threads_for(int L, int gb) { return std::max(32, 1 << (L - gb)); }
+// Register groups a pass kernel's thread walks per phase (a run-time loop over
+// the same straight-line phase body).  The body of a heavy pass is far larger
+// than the 32 KB L1.5 instruction cache, so without reuse every tile streams
+// the whole body from L2 (ncu: "no_instructions" ~45% of stalls); G groups per
+// thread fetch each instruction once per G executions.  Passes with
+// renormalising sites keep G = 1 (their per-tile norm reduction is per phase).
+inline int group_loop(int L, int gb, bool general) {
+  if (general) return 1;
+  static const int want = [] {
+    const char* e = std::getenv("PTSBE_GROUP_LOOP");
+    return e ? std::max(1, std::atoi(e)) : 2;
+  }();
+  int g = 1;
+  while (g < want && ((1 << (L - gb)) / (2 * g)) >= 64) g *= 2;
+  return g;
+}
+inline int threads_for(int L, int gb, bool general) {
+  return std::max(32, (1 << (L - gb)) / group_loop(L, gb, general));
+}
 
 // Lambda scattering the low bits of x onto the set bits of `mask` (PDEP as shift/mask runs).
 inline std::string scatter_fn(uint64_t mask, const char* arg_type) {
@@ -231,18 +249,41 @@ inline std::string scatter_fn(uint64_t mask, const char* arg_type) {
   return o.str();
 }
 
-// Per-trajectory bitmask, evaluated once per CTA when the trajectory changes:
-// bit ph set iff some site of phase ph takes a non-default outcome (phases past
-// 63 share bit 63, which then sends all of them down the exact slow path).
-inline std::string err_mask_fn(const GenPass& gp) {
-  std::ostringstream o;
-  o << "[](const uint8_t* sel) -> uint64_t { uint64_t m_ = 0;";
+// Hit words of a pass: site number i of phase ph (in op order) owns bit i % 64 of
+// word hit_word(ph) + i / 64.
+inline std::vector<int> hit_word_offsets(const GenPass& gp) {
+  std::vector<int> off(gp.phases.size() + 1, 0);
   for (size_t ph = 0; ph < gp.phases.size(); ++ph) {
     const DevPhase& D = gp.phases[ph];
-    std::ostringstream e;
-    for (int q = D.op_begin; q < D.op_begin + D.n_ops; ++q)
-      if (gp.ops[q].kind == 1) e << (e.tellp() > 0 ? " | " : "") << "sel[" << gp.ops[q].ref << "]";
-    if (e.tellp() > 0) o << " m_ |= (uint64_t)((" << e.str() << ") != 0) << " << std::min<size_t>(ph, 63) << ";";
+    int ns = 0;
+    for (int q = D.op_begin; q < D.op_begin + D.n_ops; ++q) ns += gp.ops[q].kind == 1;
+    off[ph + 1] = off[ph] + (ns + 63) / 64;
+  }
+  return off;
+}
+constexpr int kMaxHitWords = 480;   // shared-memory room reserved per CTA (smem_bytes)
+
+// Per-trajectory outcome summary, evaluated by one thread per CTA when the
+// trajectory changes: hit words (bit set iff that site takes a non-default
+// outcome) into shared memory, and the returned phase mask (bit ph set iff phase
+// ph has a hit; phases past 63 share bit 63).  The slow variant of a phase then
+// tests compile-time bits of a word it reads once, instead of re-reading every
+// site's outcome byte for every register group.
+inline std::string err_mask_fn(const GenPass& gp) {
+  const std::vector<int> woff = hit_word_offsets(gp);
+  std::ostringstream o;
+  o << "[](const uint8_t* sel, uint64_t* hw) -> uint64_t { uint64_t m_ = 0, w_;";
+  for (size_t ph = 0; ph < gp.phases.size(); ++ph) {
+    const DevPhase& D = gp.phases[ph];
+    int i = 0;
+    for (int q = D.op_begin; q < D.op_begin + D.n_ops; ++q) {
+      if (gp.ops[q].kind != 1) continue;
+      if (i % 64 == 0) o << " w_ = 0;";
+      o << " w_ |= (uint64_t)(sel[" << gp.ops[q].ref << "] != 0) << " << (i % 64) << ";";
+      ++i;
+      if (i % 64 == 0) o << " hw[" << woff[ph] + i / 64 - 1 << "] = w_; m_ |= (uint64_t)(w_ != 0) << " << std::min<size_t>(ph, 63) << ";";
+    }
+    if (i % 64) o << " hw[" << woff[ph] + i / 64 << "] = w_; m_ |= (uint64_t)(w_ != 0) << " << std::min<size_t>(ph, 63) << ";";
   }
   o << " return m_; }";
   return o.str();
@@ -260,19 +301,25 @@ inline std::string generate(const GenProgram& P) {
   std::ostringstream o;
   Cx G{1.0, 0.0};
   std::vector<std::string> kernels;
+  for (size_t pi = 0; pi < P.passes.size(); ++pi)
+    if (hit_word_offsets(P.passes[pi]).back() > kMaxHitWords) return std::string();   // caller falls back
   for (size_t pi = 0; pi < P.passes.size(); ++pi) {
     const GenPass& gp = P.passes[pi];
     bool has_general = false;
     for (const DevOp& op : gp.ops)
       if (op.kind == 1 && P.chans[P.site_chan[op.ref]].general) has_general = true;
     const bool scaled = !has_general;
-    const int threads = threads_for(gp.L, GB);
-    const bool all_active = threads == (1 << (gp.L - GB));
+    const int threads = threads_for(gp.L, GB, has_general);
+    const int groups = 1 << (gp.L - GB);
+    const int gloop = groups / threads;   // >= 1 when threads <= groups
+    const bool all_active = threads <= groups;
     const int min_blocks = threads <= 128 ? 3 : (threads <= 256 ? 2 : 1);
     const uint64_t nmask = P.n >= 64 ? ~0ull : ((1ull << P.n) - 1);
     const uint64_t comp = ~gp.qmask & nmask;
     const uint64_t hmask = gp.qmask & ~((1ull << gp.c) - 1);
     Emitter ke(P.c64);
+    std::ostringstream slow_fns;   // out-of-line slow variants of this pass's phases
+    const std::vector<int> woff = hit_word_offsets(gp);
     std::ostringstream& k = ke.o;
     Cx F{1.0, 0.0};
     k << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << min_blocks << ") "
@@ -284,10 +331,9 @@ inline std::string generate(const GenProgram& P) {
       << "    " << scatter_fn(hmask, "uint32_t") << ",\n"
       << "    " << err_mask_fn(gp) << ",\n"
       << "    [&](V* cur, int b, const uint8_t* sel, long long tile, uint64_t base, double scale, double* red,\n"
-      << "        uint64_t emask) {\n"
-      << "    const uint32_t g = threadIdx.x;\n"
+      << "        uint64_t emask, const uint64_t* hits) {\n"
       << "    const bool active = "
-      << (all_active ? std::string("true") : "g < " + std::to_string(1u << (gp.L - GB)) + "u") << ";\n"
+      << (all_active ? std::string("true") : "threadIdx.x < " + std::to_string(groups) + "u") << ";\n"
       << "    V a[" << N << "];\n";
     for (size_t ph = 0; ph < gp.phases.size(); ++ph) {
       const DevPhase& D = gp.phases[ph];
@@ -300,29 +346,21 @@ inline std::string generate(const GenProgram& P) {
           if ((j >> q) & 1) off[j] |= 1u << pb[q];
         so[j] = swz_host(P.c64, off[j]);
       }
-      k << "    { // phase " << ph << "\n      const uint32_t gb = ";
-      for (int q = 0; q < GB; ++q) k << "ptg::ins0(";
-      k << "g";
-      for (int q = 0; q < GB; ++q) k << ", " << pb[q] << ")";
-      k << ";\n      const uint32_t sg = ptg::swz((V*)0, gb);\n      const uint32_t so[" << N << "] = {";
-      for (int j = 0; j < N; ++j) k << so[j] << "u" << (j + 1 < N ? ", " : "");
-      k << "};\n";
-      if (ph == 0) {
-        k << "      const uint32_t off[" << N << "] = {";
-        for (int j = 0; j < N; ++j) k << off[j] << "u" << (j + 1 < N ? ", " : "");
-        k << "};\n"
-          << "      if (p.gen_zero) ptg::zerog(a, base, gb, off, active && p.gen_zero == 1, GZERO_RE, GZERO_IM);\n"
-          << "      else ptg::ldg<V, " << N << ", " << pb[0] << ">(a, cur, sg, so, active, scale);\n";
-        if (pi == 0)   // a loaded (not synthesized) input also needs the global phase G
-          k << "      if (!p.gen_zero) ptg::cscale(a, ptg::mk((V*)0, GZERO_RE, GZERO_IM));\n";
-      } else {
-        k << "      ptg::ldg<V, " << N << ", " << pb[0] << ">(a, cur, sg, so, active, 1.0);\n";
-      }
+      bool has_sites = false;
+      for (int q = D.op_begin; q < D.op_begin + D.n_ops; ++q) has_sites = has_sites || gp.ops[q].kind == 1;
+      const bool last = ph + 1 == gp.phases.size();
       // slow == true: the trajectory takes a non-default outcome at some site of
       // this phase; sites then read their outcome and apply its operator from the
-      // table (same registers, same gate code, so the frame factor is unchanged).
+      // table (same gate code, so the frame factor is unchanged).  Each variant is
+      // a complete load -> ops -> store block: no amplitude register is live across
+      // the CTA-uniform branch, so the join costs no register-shuffling moves.
       auto emit_ops = [&](bool slow) {
         Cx f{1.0, 0.0};
+        int site_i = 0;
+        if (slow) {
+          k << "      uint64_t hw_[" << std::max(1, woff[ph + 1] - woff[ph]) << "];\n";
+          for (int w = 0; w < woff[ph + 1] - woff[ph]; ++w) k << "      hw_[" << w << "] = hits[" << woff[ph] + w << "];\n";
+        }
         for (int q = D.op_begin; q < D.op_begin + D.n_ops; ++q) {
           const DevOp& op = gp.ops[q];
           const int k1 = op.arity == 2 ? op.k1 : 0;
@@ -332,14 +370,23 @@ inline std::string generate(const GenProgram& P) {
             continue;
           }
           const ptsbe_channel& ch = P.chans[P.site_chan[op.ref]];
+          const int si = site_i++;
           if (slow) {
-            k << "      { const int o_ = sel[" << op.ref << "];\n"
+            // hit: this trajectory's outcome at the site is not 0 -> apply it from the table
+            k << "      if ((hw_[" << si / 64 << "] >> " << si % 64 << ") & 1ull) { const int o_ = sel[" << op.ref
+              << "];\n"
               << "        if (!((0x" << std::hex << ch.identity_mask << std::dec << "ull >> o_) & 1ull)) {\n"
               << "          const V* m_ = reinterpret_cast<const V*>(p.mats) + (size_t)(" << ch.mat_base
               << " + o_) * 16;\n";
             if (op.arity == 1) k << "          ptg::g1<" << op.k0 << ">(a, m_[0], m_[1], m_[4], m_[5]);\n";
             else k << "          ptg::g2<" << op.k0 << ", " << k1 << ">(a, m_);\n";
-            k << "      } }\n";
+            k << "      } }";
+            if (!(ch.identity_mask & 1ull)) {   // no hit: outcome 0, which is not the identity
+              k << " else {\n        ";
+              ke.op(P.kinds[ch.mat_base], op.k0, k1, P.mats + (size_t)ch.mat_base * 32, false);
+              k << "      }";
+            }
+            k << "\n";
           } else if (!(ch.identity_mask & 1ull)) {   // outcome 0 is not the identity (e.g. damping K0)
             k << "      ";
             ke.op(P.kinds[ch.mat_base], op.k0, k1, P.mats + (size_t)ch.mat_base * 32, false);
@@ -355,28 +402,73 @@ inline std::string generate(const GenProgram& P) {
         }
         return f;
       };
-      bool has_sites = false;
-      for (int q = D.op_begin; q < D.op_begin + D.n_ops; ++q) has_sites = has_sites || gp.ops[q].kind == 1;
-      if (has_sites) k << "      if (!((emask >> " << std::min<size_t>(ph, 63) << ") & 1ull)) {\n";
-      const Cx Fph = emit_ops(false);
-      if (has_sites) {
-        k << "      } else {\n";
-        emit_ops(true);
-        k << "      }\n";
+      auto emit_block = [&](bool slow) {
+        if (gloop > 1)
+          k << "    #pragma unroll 1\n    for (uint32_t g = threadIdx.x; g < " << groups << "u; g += " << threads
+            << "u) {\n";
+        else
+          k << "    { const uint32_t g = threadIdx.x;\n";
+        k << "      const uint32_t gb = ";
+        for (int q = 0; q < GB; ++q) k << "ptg::ins0(";
+        k << "g";
+        for (int q = 0; q < GB; ++q) k << ", " << pb[q] << ")";
+        k << ";\n      const uint32_t sg = ptg::swz((V*)0, gb);\n      const uint32_t so[" << N << "] = {";
+        for (int j = 0; j < N; ++j) k << so[j] << "u" << (j + 1 < N ? ", " : "");
+        k << "};\n";
+        if (ph == 0) {
+          k << "      const uint32_t off[" << N << "] = {";
+          for (int j = 0; j < N; ++j) k << off[j] << "u" << (j + 1 < N ? ", " : "");
+          k << "};\n"
+            << "      if (p.gen_zero) ptg::zerog(a, base, gb, off, active && p.gen_zero == 1, GZERO_RE, GZERO_IM);\n"
+            << "      else ptg::ldg<V, " << N << ", " << pb[0] << ">(a, cur, sg, so, active, scale);\n";
+          if (pi == 0)   // a loaded (not synthesized) input also needs the global phase G
+            k << "      if (!p.gen_zero) ptg::cscale(a, ptg::mk((V*)0, GZERO_RE, GZERO_IM));\n";
+        } else {
+          k << "      ptg::ldg<V, " << N << ", " << pb[0] << ">(a, cur, sg, so, active, 1.0);\n";
+        }
+        const Cx f = emit_ops(slow);
+        if (last) {
+          const double mag = cxabs(cxmul(F, f));
+          if (mag != 1.0) k << "      ptg::rscale(a, " << hexd(mag) << ");\n";
+        }
+        k << "      ptg::stg<V, " << N << ", " << pb[0] << ">(a, cur, sg, so, active);\n"
+          << "    }\n";
+        return f;
+      };
+      k << "    { // phase " << ph << "\n";
+      if (has_sites) k << "    if (!((emask >> " << std::min<size_t>(ph, 63) << ") & 1ull)) {\n";
+      const Cx Fph = emit_block(false);
+      static const bool no_slow = std::getenv("PTSBE_GEN_ANALYSE_FAST_ONLY") != nullptr;   // offline analysis only
+      if (has_sites && no_slow) {
+        k << "    }\n";
+      } else if (has_sites) {
+        // the slow variant lives out of line (a non-inlined function per phase), so
+        // the hot straight-line code stays dense in the instruction cache
+        const std::string fname = "ptsbe_slow_" + std::to_string(pi) + "_" + std::to_string(ph);
+        k << "    } else {\n      " << fname
+          << "(p.mats, p.partials, p.B, p.tiles, p.gen_zero, cur, b, sel, tile, base, scale, red, active, hits);\n    }\n";
+        const std::string before = k.str();
+        emit_block(true);
+        const std::string all = k.str();
+        slow_fns << "__device__ __noinline__ void " << fname << "(const void* mats_, double* partials_, int B_, "
+                 << "long long tiles_, int gen_zero_, " << ke.V << "* cur, int b, const uint8_t* sel, long long tile, "
+                 << "uint64_t base, double scale, double* red, bool active, const uint64_t* hits) {\n"
+                 << "  typedef " << ke.V << " V;\n"
+                 << "  struct { const void* mats; double* partials; int B; long long tiles; int gen_zero; } p = "
+                 << "{mats_, partials_, B_, tiles_, gen_zero_};\n"
+                 << "  V a[" << N << "];\n"
+                 << all.substr(before.size()) << "}\n";
+        k.str(before);
+        k.seekp(0, std::ios_base::end);
       }
       F = cxmul(F, Fph);
-      if (ph + 1 == gp.phases.size()) {
-        const double mag = cxabs(F);
-        if (mag != 1.0) k << "      ptg::rscale(a, " << hexd(mag) << ");\n";
-      }
-      k << "      ptg::stg<V, " << N << ", " << pb[0] << ">(a, cur, sg, so, active);\n"
-        << "      __syncthreads();\n"
+      k << "      __syncthreads();\n"
         << "    }\n";
     }
     k << "  });\n}\n";
     const double mag = cxabs(F);
     G = cxmul(G, Cx{F.re / mag, F.im / mag});
-    kernels.push_back(k.str());
+    kernels.push_back(slow_fns.str() + k.str());
   }
   o << kGenPrelude << "\n"
     << "#define GZERO_RE " << hexd(G.re) << "\n#define GZERO_IM " << hexd(G.im) << "\n";
@@ -393,6 +485,7 @@ struct Module {
 inline bool compile(const std::string& src, int n_passes, int dev, Module& out, std::string& err) {
   Api& A = api();
   if (!A.ok) { err = A.why; return false; }
+  if (src.empty()) { err = "program exceeds the generated kernels' limits (noise sites per pass)"; return false; }
   static std::mutex mu;
   static std::map<std::pair<int, std::string>, Module> cache;
   std::lock_guard<std::mutex> lock(mu);
@@ -431,7 +524,7 @@ inline bool compile(const std::string& src, int n_passes, int dev, Module& out, 
 }
 
 inline size_t smem_bytes(int L, int /*c*/, size_t amp_bytes) {
-  return 2 * ((size_t)1 << L) * amp_bytes + 32 * 8 + 16;   // tiles | red | emask
+  return 2 * ((size_t)1 << L) * amp_bytes + 32 * 8 + 16 + 8 * kMaxHitWords;   // tiles | red | emask | hits
 }
 
 }  // namespace gen

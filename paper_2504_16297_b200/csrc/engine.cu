@@ -102,6 +102,10 @@ struct ptsbe_engine {
   int ev_used = 0;
   double pass_ms_total = 0.0;
   long long pass_launches = 0;
+  // host-only handle (ptsbe_create_host): load_program plans and generates the
+  // pass kernels' source without touching a device (offline SASS inspection)
+  bool host_only = false;
+  std::string gen_src;
   std::string err;
 };
 
@@ -281,7 +285,7 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero, int p_begin = 0, int p
       CK(h, cudaEventRecord(h->ev[h->ev_used], h->stream));
     }
     if (h->gen_active) {
-      const unsigned threads = (unsigned)gen::threads_for(ph.L, h->phase_bits);
+      const unsigned threads = (unsigned)gen::threads_for(ph.L, h->phase_bits, ph.n_slots > 0);
       const size_t gsm = gen::smem_bytes(ph.L, ph.c, sizeof(typename Cplx<R>::V));
       CUfunction f = h->gen_mod.fns[pi];
       int per_sm = 0;
@@ -609,8 +613,35 @@ int ptsbe_create(int device, int n_qubits, int dtype, int batch_cap, ptsbe_engin
   return 0;
 }
 
+int ptsbe_create_host(int n_qubits, int dtype, ptsbe_engine** out) {
+  if (!out) return PTSBE_ERR_VALIDATION;
+  *out = nullptr;
+  if (n_qubits < 1 || n_qubits > 40) return PTSBE_ERR_VALIDATION;
+  if (dtype != PTSBE_C64 && dtype != PTSBE_C128) return PTSBE_ERR_VALIDATION;
+  ptsbe_engine* h = new ptsbe_engine();
+  h->host_only = true;
+  h->dev = -1;
+  h->n = n_qubits;
+  h->dtype = dtype;
+  h->cap = 1;
+  h->amp_bytes = dtype == PTSBE_C64 ? 8 : 16;
+  *out = h;
+  return 0;
+}
+
+int64_t ptsbe_codegen_source(ptsbe_engine* h, char* buf, size_t len) {
+  if (!h) return -PTSBE_ERR_VALIDATION;
+  if (buf && len) {
+    const size_t k = std::min(len - 1, h->gen_src.size());
+    std::memcpy(buf, h->gen_src.data(), k);
+    buf[k] = 0;
+  }
+  return (int64_t)h->gen_src.size();
+}
+
 int ptsbe_destroy(ptsbe_engine* h) {
   if (!h) return 0;
+  if (h->host_only) { delete h; return 0; }
   cudaSetDevice(h->dev);
   void* ptrs[] = {h->states, h->d_sel, h->d_weight, h->d_nst, h->d_status, h->d_fail, h->d_ops, h->d_mats,
                   h->d_phases, h->d_matkind,
@@ -752,12 +783,15 @@ static void plan_phases(std::vector<HostOp>& ops, int L, std::vector<DevOp>& out
 static int try_codegen(ptsbe_engine* h, int mode, const std::vector<PassHost>& ph, const std::vector<DevOp>& dops,
                        const std::vector<DevPhase>& dph, const double* mats, const std::vector<int32_t>& kinds,
                        const ptsbe_channel* chans, const int32_t* site_chan);
+static std::string gen_source(ptsbe_engine* h, const std::vector<PassHost>& ph, const std::vector<DevOp>& dops,
+                              const std::vector<DevPhase>& dph, const double* mats, const std::vector<int32_t>& kinds,
+                              const ptsbe_channel* chans, const int32_t* site_chan);
 
 int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const double* mats, int n_mats,
                        const ptsbe_channel* chans, int n_chans, const int32_t* site_chan, int n_sites,
                        const ptsbe_pass* passes, int n_passes) {
   if (!h) return PTSBE_ERR_VALIDATION;
-  CK(h, cudaSetDevice(h->dev));
+  if (!h->host_only) CK(h, cudaSetDevice(h->dev));
   h->loaded = false;
   if (n_ops < 0 || n_mats < 0 || n_chans < 0 || n_sites < 0 || n_passes < 0)
     return fail(h, PTSBE_ERR_VALIDATION, "negative table size");
@@ -887,6 +921,10 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
   for (int m = 0; m < n_mats; ++m) kinds[m] = classify_matrix(mats + (size_t)m * 32, mat_arity[m] ? mat_arity[m] : 2);
   h->gen_active = false;
   h->gen_note.clear();
+  if (h->host_only) {   // plan + generate only (the generic kernel needs no source)
+    h->gen_src = cg_want ? gen_source(h, ph, dops, dph, mats, kinds, chans, site_chan) : std::string();
+    return 0;
+  }
   if (cg_want) {
     if (int r = try_codegen(h, cg_mode, ph, dops, dph, mats, kinds, chans, site_chan)) return r;
     if (!h->gen_active && h->phase_bits != 4) {   // generic kernel: 4-bit phases
@@ -952,43 +990,44 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
   return 0;
 }
 
+// Source of the circuit-specialised kernels (codegen.h) for the planned passes.
+static std::string gen_source(ptsbe_engine* h, const std::vector<PassHost>& ph, const std::vector<DevOp>& dops,
+                              const std::vector<DevPhase>& dph, const double* mats, const std::vector<int32_t>& kinds,
+                              const ptsbe_channel* chans, const int32_t* site_chan) {
+  gen::GenProgram G;
+  G.c64 = h->dtype == PTSBE_C64;
+  G.n = h->n;
+  G.gb = h->phase_bits;
+  G.mats = mats;
+  G.kinds = kinds.data();
+  G.chans = chans;
+  G.site_chan = site_chan;
+  for (const PassHost& P : ph) {
+    gen::GenPass gp;
+    gp.L = P.L;
+    gp.c = P.c;
+    gp.qmask = P.qmask;
+    gp.phases.assign(dph.begin() + P.phase_begin, dph.begin() + P.phase_begin + P.n_phases);
+    gp.ops.assign(dops.begin() + P.op_begin, dops.begin() + P.op_begin + P.n_ops);
+    G.passes.push_back(gp);
+  }
+  return gen::generate(G);
+}
+
 // Generate + compile the circuit-specialised kernels (codegen.h).
 static int try_codegen(ptsbe_engine* h, int mode, const std::vector<PassHost>& ph, const std::vector<DevOp>& dops,
                        const std::vector<DevPhase>& dph, const double* mats, const std::vector<int32_t>& kinds,
                        const ptsbe_channel* chans, const int32_t* site_chan) {
-  const int n_passes = (int)ph.size();
-  {
-    {
-      gen::GenProgram G;
-      G.c64 = h->dtype == PTSBE_C64;
-      G.n = h->n;
-      G.gb = h->phase_bits;
-      G.mats = mats;
-      G.kinds = kinds.data();
-      G.chans = chans;
-      G.site_chan = site_chan;
-      for (int p = 0; p < n_passes; ++p) {
-        gen::GenPass gp;
-        gp.L = ph[p].L;
-        gp.c = ph[p].c;
-        gp.qmask = ph[p].qmask;
-        gp.phases.assign(dph.begin() + ph[p].phase_begin, dph.begin() + ph[p].phase_begin + ph[p].n_phases);
-        for (auto& D : gp.phases) D.op_begin -= 0;
-        gp.ops.assign(dops.begin() + ph[p].op_begin, dops.begin() + ph[p].op_begin + ph[p].n_ops);
-        G.passes.push_back(gp);
-      }
-      const std::string src = gen::generate(G);
-      if (const char* dump = std::getenv("PTSBE_CODEGEN_DUMP")) {
-        if (FILE* f = std::fopen(dump, "w")) { std::fputs(src.c_str(), f); std::fclose(f); }
-      }
-      std::string err;
-      if (gen::compile(src, n_passes, h->dev, h->gen_mod, err)) {
-        h->gen_active = true;
-      } else {
-        h->gen_note = err;
-        if (mode == 1) return fail(h, PTSBE_ERR_CUDA, "codegen: %s", err.c_str());
-      }
-    }
+  const std::string src = gen_source(h, ph, dops, dph, mats, kinds, chans, site_chan);
+  if (const char* dump = std::getenv("PTSBE_CODEGEN_DUMP")) {
+    if (FILE* f = std::fopen(dump, "w")) { std::fputs(src.c_str(), f); std::fclose(f); }
+  }
+  std::string err;
+  if (gen::compile(src, (int)ph.size(), h->dev, h->gen_mod, err)) {
+    h->gen_active = true;
+  } else {
+    h->gen_note = err;
+    if (mode == 1) return fail(h, PTSBE_ERR_CUDA, "codegen: %s", err.c_str());
   }
   return 0;
 }

@@ -13,11 +13,15 @@
 // This file is embedded verbatim as a string (gen_prelude.inc, produced by
 // build.py) -- it is NOT compiled by nvcc directly.  Keep PassParams identical
 // to pass_kernels.cuh.
+#if defined(__CUDACC_RTC__)   // NVRTC has no <stdint.h>; nvcc (tools/gen_offline.py) does
 typedef unsigned int uint32_t;
 typedef int int32_t;
 typedef unsigned long long uint64_t;
 typedef unsigned char uint8_t;
 typedef long long int64_t;
+#else
+#include <stdint.h>
+#endif
 
 namespace ptg {
 
@@ -41,9 +45,12 @@ __device__ __forceinline__ float2 mk(float2*, double x, double y) { return make_
 __device__ __forceinline__ double2 mk(double2*, double x, double y) { return make_double2(x, y); }
 
 // Packed (re, im) arithmetic.  complex64 uses Blackwell's FP32x2 instructions
-// (FFMA2 / FMUL2 / FADD2): one instruction per complex component pair, and the
-// (im, re) swap of a complex multiply folds into the operand selector.
-// complex128 falls back to scalar DFMA.
+// (FFMA2 / FMUL2 / FADD2).  Complex products are written as
+//   d * x = x * d.re + (i x) * d.im,   i x = (-x.im, x.re)
+// so that, with a literal d, each term is ONE instruction: the scalar is a
+// 32-bit immediate broadcast to both lanes and i*x is an operand modifier
+// (FFMA2 Rd, -Rx.F32x2.LO_HI.NP, imm, Rc) -- no register pairs of constants
+// (which cost two MOVs per use).  complex128 falls back to scalar DFMA.
 __device__ __forceinline__ float2 pfma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 __device__ __forceinline__ float2 pmul(float2 a, float2 b) { return __fmul2_rn(a, b); }
 __device__ __forceinline__ float2 padd(float2 a, float2 b) { return __fadd2_rn(a, b); }
@@ -53,24 +60,26 @@ __device__ __forceinline__ double2 pfma(double2 a, double2 b, double2 c) {
 __device__ __forceinline__ double2 pmul(double2 a, double2 b) { return make_double2(a.x * b.x, a.y * b.y); }
 __device__ __forceinline__ double2 padd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 template <typename V, typename S> __device__ __forceinline__ V bc(S s) { V r; r.x = s; r.y = s; return r; }
-template <typename V> __device__ __forceinline__ V swp(V x) { V r; r.x = x.y; r.y = x.x; return r; }
-template <typename V> __device__ __forceinline__ V pm(V d) { V r; r.x = -d.y; r.y = d.y; return r; }   // (-im, im)
+template <typename V> __device__ __forceinline__ V ix(V x) { V r; r.x = -x.y; r.y = x.x; return r; }   // i * x
 
 template <typename V> __device__ __forceinline__ V cmul(V d, V x) {     // d * x
-  return pfma(bc<V>(d.x), x, pmul(pm(d), swp(x)));
+  typedef decltype(d.x) R;
+  return pfma(ix(x), bc<V, R>(d.y), pmul(x, bc<V, R>(d.x)));
 }
 template <typename V> __device__ __forceinline__ V cmadd2(V m0, V a, V m1, V b) {   // m0*a + m1*b
-  return pfma(bc<V>(m0.x), a, pfma(pm(m0), swp(a), pfma(bc<V>(m1.x), b, pmul(pm(m1), swp(b)))));
+  typedef decltype(a.x) R;
+  return pfma(ix(b), bc<V, R>(m1.y), pfma(b, bc<V, R>(m1.x), pfma(ix(a), bc<V, R>(m0.y), pmul(a, bc<V, R>(m0.x)))));
 }
 template <typename V> __device__ __forceinline__ V cmadd4(V m0, V m1, V m2, V m3, V a, V b, V c, V d) {
-  V r = pmul(pm(m3), swp(d));
-  r = pfma(bc<V>(m3.x), d, r);
-  r = pfma(pm(m2), swp(c), r);
-  r = pfma(bc<V>(m2.x), c, r);
-  r = pfma(pm(m1), swp(b), r);
-  r = pfma(bc<V>(m1.x), b, r);
-  r = pfma(pm(m0), swp(a), r);
-  return pfma(bc<V>(m0.x), a, r);
+  typedef decltype(a.x) R;
+  V r = pmul(a, bc<V, R>(m0.x));
+  r = pfma(ix(a), bc<V, R>(m0.y), r);
+  r = pfma(b, bc<V, R>(m1.x), r);
+  r = pfma(ix(b), bc<V, R>(m1.y), r);
+  r = pfma(c, bc<V, R>(m2.x), r);
+  r = pfma(ix(c), bc<V, R>(m2.y), r);
+  r = pfma(d, bc<V, R>(m3.x), r);
+  return pfma(ix(d), bc<V, R>(m3.y), r);
 }
 __device__ __forceinline__ double prob64(float2 a) {
   const double x = a.x, y = a.y;
@@ -116,7 +125,7 @@ template <int K, typename V, int N> __device__ __forceinline__ void g1h(V (&a)[N
     if (!(j & (1 << K))) {
       const V x = a[j], y = a[j | (1 << K)];
       a[j] = padd(x, y);
-      a[j | (1 << K)] = pfma(bc<V>(-1.0f), y, x);
+      a[j | (1 << K)] = pfma(y, bc<V>(-1.0f), x);
     }
 }
 template <int K, typename V, int N> __device__ __forceinline__ void g1d(V (&a)[N], V d0, V d1) {
@@ -142,15 +151,16 @@ template <int K, typename V, int N> __device__ __forceinline__ void g1x(V (&a)[N
     if (!(j & (1 << K))) { const V t = a[j]; a[j] = a[j | (1 << K)]; a[j | (1 << K)] = t; }
 }
 template <int K, typename V, int N> __device__ __forceinline__ void g1neg(V (&a)[N]) {    // diag(1, -1)
+  typedef decltype(a[0].x) R;
 #pragma unroll
   for (int j = 0; j < N; ++j)
-    if (j & (1 << K)) a[j] = pmul(bc<V>(-1.0f), a[j]);
+    if (j & (1 << K)) a[j] = pmul(a[j], bc<V, R>((R)-1));
 }
 template <int K, typename V, int N> __device__ __forceinline__ void g1pi(V (&a)[N], bool neg) {   // diag(1, ±i)
-  V s; s.x = neg ? 1.0f : -1.0f; s.y = neg ? -1.0f : 1.0f;   // i*(x+iy) = (-y, x)
+  typedef decltype(a[0].x) R;
 #pragma unroll
   for (int j = 0; j < N; ++j)
-    if (j & (1 << K)) a[j] = pmul(s, swp(a[j]));
+    if (j & (1 << K)) a[j] = pmul(ix(a[j]), bc<V, R>(neg ? (R)-1 : (R)1));
 }
 template <int KH, int KL, typename V, int N> __device__ __forceinline__ void g2(V (&a)[N], const V* m) {
 #pragma unroll
@@ -188,9 +198,8 @@ template <typename V, int N> __device__ __forceinline__ void cscale(V (&a)[N], V
 }
 template <typename V, int N> __device__ __forceinline__ void rscale(V (&a)[N], double s) {
   typedef decltype(a[0].x) R;
-  const V sc = bc<V>((R)s);
 #pragma unroll
-  for (int j = 0; j < N; ++j) a[j] = pmul(sc, a[j]);
+  for (int j = 0; j < N; ++j) a[j] = pmul(a[j], bc<V, R>((R)s));
 }
 
 // ---- addressing
@@ -250,12 +259,7 @@ __device__ __forceinline__ void ldg(V (&a)[N], const V* cur, uint32_t sg, const 
 #pragma unroll
     for (int j = 0; j < N; ++j) a[j] = cur[sg ^ so[j]];
   }
-  if (scale != 1.0) {
-    typedef decltype(a[0].x) R;
-    const R sc = (R)scale;
-#pragma unroll
-    for (int j = 0; j < N; ++j) { a[j].x *= sc; a[j].y *= sc; }
-  }
+  if (scale != 1.0) rscale(a, scale);
 }
 template <typename V, int N, int P0>
 __device__ __forceinline__ void stg(const V (&a)[N], V* cur, uint32_t sg, const uint32_t* so, bool active) {
@@ -289,7 +293,8 @@ __device__ __forceinline__ void zerog(V (&a)[N], uint64_t base, uint32_t gb, con
 // rows r0 + k*RSTEP with a fixed in-row offset, so their shared and global
 // offsets are a per-thread base plus compile-time constants (swz and the row
 // scatter are linear on disjoint bits).  err_mask(sel_row) runs once per CTA
-// per trajectory.  body(cur, b, sel_row, tile, base, scale, red, emask) runs
+// per trajectory (and fills the hit words).  body(cur, b, sel_row, tile, base,
+// scale, red, emask, hits) runs
 // the pass's phases on one tile.
 template <typename R, int L, int C, int TLOG, int NT, class TileBase, class RowOff, class ErrMask, class Body>
 __device__ __forceinline__ void run_pass(const PassParams& p, TileBase tile_base, RowOff row_off, ErrMask err_mask,
@@ -309,6 +314,7 @@ __device__ __forceinline__ void run_pass(const PassParams& p, TileBase tile_base
   V* buf1 = buf0 + TL;
   double* red = reinterpret_cast<double*>(buf1 + TL);
   uint64_t* emask_s = reinterpret_cast<uint64_t*>(red + 32);
+  uint64_t* hits_s = emask_s + 2;   // per-phase hit words (codegen.h err_mask_fn)
   int lb = -1;
   const uint32_t tid = threadIdx.x;
   const uint32_t j0 = tid & ((1u << CPR_LOG) - 1u);
@@ -349,14 +355,14 @@ __device__ __forceinline__ void run_pass(const PassParams& p, TileBase tile_base
     const long long tile = t & ((1ll << TLOG) - 1);
     if (p.status[b] != 0) continue;
     if (b != lb) {   // per trajectory, once: which phases see a non-default outcome
-      if (tid == 0) *emask_s = err_mask(p.sel + (size_t)b * p.S);
+      if (tid == 0) *emask_s = err_mask(p.sel + (size_t)b * p.S, hits_s);
       __syncthreads();
       lb = b;
     }
     const uint64_t emask = *emask_s;
     const uint64_t base = tile_base((uint64_t)tile);
     const double scale = (p.use_scale && !p.gen_zero) ? rsqrt(p.nst[b]) : 1.0;
-    body(cur, b, p.sel + (size_t)b * p.S, tile, base, scale, red, emask);
+    body(cur, b, p.sel + (size_t)b * p.S, tile, base, scale, red, emask, hits_s);
     V* st = reinterpret_cast<V*>(p.states) + ((size_t)en.z << p.n) + base;
     if (FAST) {
 #pragma unroll

@@ -47,6 +47,49 @@ class Shots:
         return {format(int(v), fmt): int(c) for v, c in zip(self.indices[lo:hi], self.counts[lo:hi])}
 
 
+def program_args(prog: Program):
+    """ptsbe_load_program arguments (after the handle), the physical layout, and the
+    numpy buffers the pointer arguments refer to (keep them alive across the call)."""
+    n = prog.n_qubits
+    order = [(p, i) for p, plan in enumerate(prog.passes) for i in plan.ops]
+    perm = list(range(n)) if prog.perm is None else list(prog.perm)
+    ops = (N.Op * max(len(order), 1))()
+    for j, (p, i) in enumerate(order):
+        so = prog.stream[i]
+        t0 = perm[so.targets[0]]
+        t1 = perm[so.targets[1]] if len(so.targets) > 1 else -1
+        ops[j] = N.Op(so.kind, len(so.targets), t0, t1, so.ref, p)
+    mats = np.ascontiguousarray(np.ascontiguousarray(prog.mats.reshape(-1, 16)).view(np.float64).reshape(-1))
+    chans = (N.Channel * max(len(prog.chans), 1))()
+    for k, ch in enumerate(prog.chans):
+        chans[k] = N.Channel(ch["n_outcomes"], ch["mat_base"], ch["general"], ch["arity"], ch["identity_mask"])
+    site_chan = np.ascontiguousarray(prog.site_chan, dtype=np.int32)
+    passes = (N.Pass * max(len(prog.passes), 1))()
+    for p, plan in enumerate(prog.passes):
+        passes[p] = N.Pass(plan.mask, len(plan.qubits), plan.low_bits)
+    args = (ops, len(order), _ptr(mats), int(prog.mats.shape[0]), chans, len(prog.chans), _ptr(site_chan),
+            int(site_chan.size), passes, len(prog.passes))
+    return args, perm, (mats, site_chan)
+
+
+def generated_source(prog: Program, dtype: str = "c64") -> str:
+    """CUDA source of the circuit-specialised pass kernels for ``prog`` (host only, no GPU):
+    the planner and code generator of ptsbe_load_program on a host-only handle."""
+    lib = N.load_library()
+    h = C.c_void_p()
+    N.check(lib, None, lib.ptsbe_create_host(prog.n_qubits, DTYPES[dtype][0], C.byref(h)), "ptsbe_create_host")
+    try:
+        args, _, keep = program_args(prog)
+        N.check(lib, h, lib.ptsbe_load_program(h, *args), "ptsbe_load_program (host only)")
+        del keep
+        n = lib.ptsbe_codegen_source(h, None, 0)
+        buf = C.create_string_buffer(int(n) + 1)
+        lib.ptsbe_codegen_source(h, buf, len(buf))
+        return buf.value.decode()
+    finally:
+        lib.ptsbe_destroy(h)
+
+
 class Engine:
     def __init__(self, n_qubits: int, dtype: str = "c128", batch_cap: int = 1, device: int = 0):
         if dtype not in DTYPES:
@@ -98,26 +141,9 @@ class Engine:
     def load_program(self, prog: Program) -> None:
         if prog.n_qubits != self.n:
             raise ValidationError(f"program is for {prog.n_qubits} qubits, engine holds {self.n}")
-        order = [(p, i) for p, plan in enumerate(prog.passes) for i in plan.ops]
-        perm = list(range(self.n)) if prog.perm is None else list(prog.perm)
-        ops = (N.Op * max(len(order), 1))()
-        for j, (p, i) in enumerate(order):
-            so = prog.stream[i]
-            t0 = perm[so.targets[0]]
-            t1 = perm[so.targets[1]] if len(so.targets) > 1 else -1
-            ops[j] = N.Op(so.kind, len(so.targets), t0, t1, so.ref, p)
-        mats = np.ascontiguousarray(prog.mats.reshape(-1, 16)).view(np.float64).reshape(-1)
-        chans = (N.Channel * max(len(prog.chans), 1))()
-        for k, ch in enumerate(prog.chans):
-            chans[k] = N.Channel(ch["n_outcomes"], ch["mat_base"], ch["general"], ch["arity"], ch["identity_mask"])
-        site_chan = np.ascontiguousarray(prog.site_chan, dtype=np.int32)
-        passes = (N.Pass * max(len(prog.passes), 1))()
-        for p, plan in enumerate(prog.passes):
-            passes[p] = N.Pass(plan.mask, len(plan.qubits), plan.low_bits)
-        mats = np.ascontiguousarray(mats)
-        st = self.lib.ptsbe_load_program(self.h, ops, len(order), _ptr(mats), int(prog.mats.shape[0]),
-                                         chans, len(prog.chans), _ptr(site_chan), int(site_chan.size),
-                                         passes, len(prog.passes))
+        args, perm, keep = program_args(prog)
+        st = self.lib.ptsbe_load_program(self.h, *args)
+        del keep
         self._check(st, "ptsbe_load_program")
         lay = np.array(perm, dtype=np.int32)
         self._check(self.lib.ptsbe_set_layout(self.h, C.c_void_p(lay.ctypes.data)), "ptsbe_set_layout")

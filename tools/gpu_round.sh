@@ -1,0 +1,15 @@
+#!/bin/bash
+# usage (on the GPU box via gpurun): tools/gpu_round.sh TAG [ncu]
+# smoke + pytest -m gpu + bench (+ ncu launch list and one --set full capture of the top pass kernel)
+mkdir -p gpurun_out
+tag=${1:-r}
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv > gpurun_out/gpu_$tag.txt
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_$tag.log 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$tag.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke_$tag.log
+timeout 1500 python -m pytest tests -q -m gpu -x --durations=15 > gpurun_out/pytest_gpu_$tag.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu_$tag.log
+timeout 900 python bench.py > gpurun_out/bench_$tag.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_$tag.log
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_$tag.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref_$tag.log
+if [ "$2" = "ncu" ]; then
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches_$tag.csv python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_launch_$tag.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:ptsbe_pass -s 40 -c 2 -o gpurun_out/pass_$tag -f python bench.py --steps 1 --warmup 3 --no-cpu > gpurun_out/ncu_full_$tag.log 2>&1
+fi
