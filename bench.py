@@ -276,6 +276,7 @@ def main():
         barrier()
     launches = eng.launches - l0
     pass_ms, pass_n, pass_bytes = eng.profile_read()
+    pp_ms, pp_bytes = eng.profile_passes()
     eng.profile(False)
     ms = max_over_ranks(e0.elapsed_time(e1))
     total_traj = K * B * world
@@ -313,7 +314,9 @@ def main():
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                 "traffic": None, "kernel": "pass_kernel", "peak_kind": peak_kind,
                 "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_ms,
-                "pass_share_of_step": pass_ms / max(1e-9, e0.elapsed_time(e1))}
+                "pass_share_of_step": pass_ms / max(1e-9, e0.elapsed_time(e1)),
+                "per_pass_ms": [round(float(x) / K, 3) for x in pp_ms],
+                "per_pass_gbs": [round(float(b) / max(float(m), 1e-9) / 1e6, 1) for m, b in zip(pp_ms, pp_bytes)]}
     traj_bytes = prog.n_passes * 2 * (1 << c.n_qubits) * amp + (1 << c.n_qubits) * amp + 16 * SHOTS
     line = {
         "metric": "shots/sec (config 4: 28 q QEC, 1e4 shots/trajectory)", "value": value, "unit": "shots/s",

@@ -198,6 +198,9 @@ int ptsbe_profile_read(ptsbe_engine* h, double* total_ms, int64_t* launches);
 /* Algorithmic bytes (one read + one write of every state a launch processes)
  * of the pass launches profiled since ptsbe_profile(h, 1). */
 double ptsbe_profile_bytes(ptsbe_engine* h);
+/* Per pass index: accumulated kernel milliseconds and algorithmic bytes of the
+ * launches read by ptsbe_profile_read so far.  Returns the number of passes. */
+int ptsbe_profile_passes(ptsbe_engine* h, double* ms, double* bytes, int max_passes);
 /* Kernel launches issued by this handle since creation (for bench gpu_launches). */
 int64_t ptsbe_launch_count(ptsbe_engine* h);
 

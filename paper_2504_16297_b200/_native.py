@@ -84,6 +84,7 @@ SIGNATURES = {
     "ptsbe_profile": (C.c_int, [C.c_void_p, C.c_int]),
     "ptsbe_profile_read": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "ptsbe_profile_bytes": (C.c_double, [C.c_void_p]),
+    "ptsbe_profile_passes": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
     "ptsbe_create_host": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "ptsbe_codegen_source": (C.c_int64, [C.c_void_p, C.c_char_p, C.c_size_t]),
 }

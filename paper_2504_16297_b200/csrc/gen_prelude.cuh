@@ -35,6 +35,7 @@ struct PassParams {
   const void* mats; const int32_t* mat_kind; const double* nst; int use_scale; int gen_zero;
   double* partials; const int32_t* status; int B; long long tiles;
   const int4* ent; int E;   // launch entries {trajectory row, src slot, dst slot, 0}
+  const void* emats; const int4* efix;   // outcome corrections (codegen.h build_fix_tables)
 };
 
 template <typename R> struct Cplx;
@@ -275,6 +276,121 @@ __device__ __forceinline__ void stg(const V (&a)[N], V* cur, uint32_t sg, const 
     for (int j = 0; j < N; ++j) cur[sg ^ so[j]] = a[j];
   }
 }
+// A non-default outcome (slow variant of a phase): the thread's N amplitudes are
+// stored to their own tile slots, this out-of-line routine applies the outcome's
+// operator there, and the caller reloads them.  Keeping the operator off the
+// register path means the per-site branch joins with the registers unchanged,
+// so the common (no-hit) path pays no register-shuffling moves.  k0 / k1 are
+// register-bit positions (first-listed target = MSB of the local index).
+template <typename V, int GB>
+__device__ __noinline__ void err_apply(V* cur, uint32_t gb, uint32_t pbits, int arity, int k0, int k1, const V* m) {
+  constexpr int N = 1 << GB;
+  uint32_t addr[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    uint32_t off = 0;
+#pragma unroll
+    for (int q = 0; q < GB; ++q)
+      if ((j >> q) & 1) off |= 1u << ((pbits >> (5 * q)) & 31);
+    addr[j] = swz((V*)0, gb | off);
+  }
+  if (arity == 1) {
+    const V m00 = m[0], m01 = m[1], m10 = m[4], m11 = m[5];
+    for (int j = 0; j < N; ++j)
+      if (!(j & (1 << k0))) {
+        const V x = cur[addr[j]], y = cur[addr[j | (1 << k0)]];
+        cur[addr[j]] = cmadd2(m00, x, m01, y);
+        cur[addr[j | (1 << k0)]] = cmadd2(m10, x, m11, y);
+      }
+  } else {
+    for (int j = 0; j < N; ++j)
+      if (!(j & (1 << k0)) && !(j & (1 << k1))) {
+        const int i1 = j | (1 << k1), i2 = j | (1 << k0), i3 = i1 | i2;
+        const V v0 = cur[addr[j]], v1 = cur[addr[i1]], v2 = cur[addr[i2]], v3 = cur[addr[i3]];
+        cur[addr[j]] = cmadd4(m[0], m[1], m[2], m[3], v0, v1, v2, v3);
+        cur[addr[i1]] = cmadd4(m[4], m[5], m[6], m[7], v0, v1, v2, v3);
+        cur[addr[i2]] = cmadd4(m[8], m[9], m[10], m[11], v0, v1, v2, v3);
+        cur[addr[i3]] = cmadd4(m[12], m[13], m[14], m[15], v0, v1, v2, v3);
+      }
+  }
+}
+
+// Outcome correction of a unitary-mixture site (codegen.h build_fix_tables).  The
+// phase always runs its fast (default-outcome) code; a site that takes outcome o
+// instead is corrected afterwards by E' = T E_o T^dagger, T = the phase's ops after
+// the site, E_o = U_o U_0^dagger, restricted to the site's light cone in the phase
+// (fx.x = cone register-bit mask, fx.y = 2^|cone|).  It runs on the tile in shared
+// memory after the phase, cooperatively over all register groups, with the matrix
+// staged in shared memory (rows read as broadcasts).  Compact code: the slow path
+// no longer duplicates the phase.
+template <typename V, int GB, int D>
+__device__ __forceinline__ void fix_group(V* cur, uint32_t gb, const uint32_t* pos, const int* cb, uint32_t cone,
+                                          const V* M) {
+  constexpr int N = 1 << GB;
+  for (int j = 0; j < N; ++j) {
+    if (j & cone) continue;
+    V v[D];
+    uint32_t ad[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      int idx = j;
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        if ((1 << m) < D && ((d >> m) & 1)) idx |= 1 << cb[m];
+      uint32_t off = 0;
+#pragma unroll
+      for (int q = 0; q < GB; ++q)
+        if ((idx >> q) & 1) off |= pos[q];
+      ad[d] = swz((V*)0, gb | off);
+      v[d] = cur[ad[d]];
+    }
+    V w[D];
+#pragma unroll 1
+    for (int r = 0; r < D; ++r) {
+      V acc = mk((V*)0, 0.0, 0.0);
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        const V m = M[r * D + c];
+        acc = pfma(v[c], bc<V>(m.x), pfma(ix(v[c]), bc<V>(m.y), acc));
+      }
+      w[r] = acc;
+    }
+#pragma unroll
+    for (int d = 0; d < D; ++d) cur[ad[d]] = w[d];
+  }
+}
+// CTA-cooperative (every thread calls it with the same arguments).
+template <typename V, int GB>
+__device__ __noinline__ void fix_site(V* cur, int groups, uint32_t pbits, int4 fx, int o, const void* emats, V* msm) {
+  if (o == 0 || (o < 32 && ((fx.w >> o) & 1))) return;   // default outcome, or one equal to it
+  const V* M = reinterpret_cast<const V*>(emats) + fx.z + (size_t)(o - 1) * fx.y * fx.y;
+  for (int i = threadIdx.x; i < fx.y * fx.y; i += blockDim.x) msm[i] = M[i];
+  uint32_t pos[GB];
+  int pb[GB];
+#pragma unroll
+  for (int q = 0; q < GB; ++q) {
+    pb[q] = (pbits >> (5 * q)) & 31;
+    pos[q] = 1u << pb[q];
+  }
+  int cb[4] = {0, 0, 0, 0}, k = 0;
+#pragma unroll
+  for (int q = 0; q < GB; ++q)
+    if (((uint32_t)fx.x >> q) & 1) cb[k++] = q;
+  __syncthreads();
+  for (int g = threadIdx.x; g < groups; g += blockDim.x) {
+    uint32_t gb = (uint32_t)g;
+#pragma unroll
+    for (int q = 0; q < GB; ++q) gb = ins0(gb, pb[q]);
+    switch (fx.y) {
+      case 2: fix_group<V, GB, 2>(cur, gb, pos, cb, (uint32_t)fx.x, msm); break;
+      case 4: fix_group<V, GB, 4>(cur, gb, pos, cb, (uint32_t)fx.x, msm); break;
+      case 8: fix_group<V, GB, 8>(cur, gb, pos, cb, (uint32_t)fx.x, msm); break;
+      default: fix_group<V, GB, 16>(cur, gb, pos, cb, (uint32_t)fx.x, msm); break;
+    }
+  }
+  __syncthreads();
+}
+
 // |0...0> times the program's accumulated global phase G (see codegen.h)
 template <typename V, int N>
 __device__ __forceinline__ void zerog(V (&a)[N], uint64_t base, uint32_t gb, const uint32_t* off, bool active,
@@ -315,6 +431,7 @@ __device__ __forceinline__ void run_pass(const PassParams& p, TileBase tile_base
   double* red = reinterpret_cast<double*>(buf1 + TL);
   uint64_t* emask_s = reinterpret_cast<uint64_t*>(red + 32);
   uint64_t* hits_s = emask_s + 2;   // per-phase hit words (codegen.h err_mask_fn)
+  V* fixm_s = reinterpret_cast<V*>(hits_s + 480);   // staged correction matrix (<= 16 x 16)
   int lb = -1;
   const uint32_t tid = threadIdx.x;
   const uint32_t j0 = tid & ((1u << CPR_LOG) - 1u);
@@ -362,7 +479,7 @@ __device__ __forceinline__ void run_pass(const PassParams& p, TileBase tile_base
     const uint64_t emask = *emask_s;
     const uint64_t base = tile_base((uint64_t)tile);
     const double scale = (p.use_scale && !p.gen_zero) ? rsqrt(p.nst[b]) : 1.0;
-    body(cur, b, p.sel + (size_t)b * p.S, tile, base, scale, red, emask, hits_s);
+    body(cur, b, p.sel + (size_t)b * p.S, tile, base, scale, red, emask, hits_s, fixm_s);
     V* st = reinterpret_cast<V*>(p.states) + ((size_t)en.z << p.n) + base;
     if (FAST) {
 #pragma unroll

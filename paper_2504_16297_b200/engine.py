@@ -222,6 +222,14 @@ class Engine:
         self._check(self.lib.ptsbe_profile_read(self.h, C.byref(ms), C.byref(n)), "ptsbe_profile_read")
         return float(ms.value), int(n.value), float(self.lib.ptsbe_profile_bytes(self.h))
 
+    def profile_passes(self):
+        """Per pass index: (ms, algorithmic bytes) accumulated by profile_read()."""
+        n = self.lib.ptsbe_profile_passes(self.h, None, None, 0)
+        ms = np.zeros(max(n, 1))
+        by = np.zeros(max(n, 1))
+        self.lib.ptsbe_profile_passes(self.h, _ptr(ms), _ptr(by), n)
+        return ms[:n], by[:n]
+
     def info(self) -> dict:
         out = np.zeros(11, dtype=np.int64)
         self._check(self.lib.ptsbe_info(self.h, _ptr(out), out.size), "ptsbe_info")
