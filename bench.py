@@ -196,6 +196,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--rng", default="philox", choices=["philox", "pcg64"])
     ap.add_argument("--tile-bits", type=int, default=None, help="fused-pass tile qubits (default: planner's)")
+    ap.add_argument("--no-errors", action="store_true",
+                    help="analysis only: zero every sampled Kraus selection (all trajectories noiseless)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -223,6 +225,8 @@ def main():
     eng = Engine(c.n_qubits, args.dtype, batch_cap=B, device=local)
     eng.load_program(prog)
     sel = selection_matrix(prog, specs)
+    if args.no_errors:
+        sel[:] = 0
     shots = np.full(per_rank, SHOTS, dtype=np.int64)
     if args.rng == "philox":
         rng_mode = N.RNG_PHILOX

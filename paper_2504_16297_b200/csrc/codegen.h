@@ -20,7 +20,6 @@
 #include <dlfcn.h>
 
 #include <cmath>
-#include <complex>
 #include <cstdio>
 #include <map>
 #include <mutex>
@@ -212,65 +211,6 @@ struct GenProgram {
 
 inline std::string kernel_name(int pass) { return "ptsbe_pass_" + std::to_string(pass); }
 
-// ---------------------------------------------------------------- outcome corrections
-// A phase whose sites all belong to unitary mixtures always runs its fast code
-// (every site at its default outcome U_0).  If the trajectory takes outcome o at
-// site s instead, the phase result is corrected afterwards:
-//   T E_o A  =  (T E_o T^dagger) (T A),   E_o = U_o U_0^dagger,
-// where A / T are the phase's ops before / after s (unitary).  T E_o T^dagger acts
-// only on the light cone of s through T (the register bits reachable from s's
-// targets via T's ops), so it is stored as a dense 2^k x 2^k matrix, k <= 4.
-// Several hits in one phase are applied in site order (E1' first).  Scaled
-// (pivot-factored) gate code does not matter: T's scalar factor cancels.
-typedef std::complex<double> cplx;
-
-struct FixSite {        // per site id
-  int cone = 0;         // register-bit mask of the light cone (0: not correctable this way)
-  int dim = 0;
-  int base = 0;         // offset (complex entries) of outcome 1's matrix
-  int same = 0;         // outcomes (< 32) whose operator equals the default's: no correction
-};
-
-inline cplx mat_at(const double* m, int r, int c) { return cplx(m[2 * (4 * r + c)], m[2 * (4 * r + c) + 1]); }
-
-// Embed an arity-1/2 operator (4x4 padded, first-listed target = MSB) acting on
-// register bits (k0[, k1]) into the cone space spanned by cone bits cb[0..k).
-inline std::vector<cplx> embed(const double* m, int arity, int k0, int k1, const std::vector<int>& cb) {
-  const int D = 1 << cb.size();
-  auto local = [&](int bit) { for (size_t i = 0; i < cb.size(); ++i) if (cb[i] == bit) return (int)i; return -1; };
-  std::vector<cplx> M((size_t)D * D, 0.0);
-  const int a = local(k0), b = arity == 2 ? local(k1) : -1;
-  for (int c = 0; c < D; ++c) {
-    if (arity == 1) {
-      const int in = (c >> a) & 1;
-      for (int o = 0; o < 2; ++o) M[(size_t)((c & ~(1 << a)) | (o << a)) * D + c] = mat_at(m, o, in);
-    } else {
-      const int in = (((c >> a) & 1) << 1) | ((c >> b) & 1);
-      for (int o = 0; o < 4; ++o) {
-        const int r = (c & ~(1 << a) & ~(1 << b)) | (((o >> 1) & 1) << a) | ((o & 1) << b);
-        M[(size_t)r * D + c] = mat_at(m, o, in);
-      }
-    }
-  }
-  return M;
-}
-inline std::vector<cplx> mmul(const std::vector<cplx>& A, const std::vector<cplx>& B, int D) {
-  std::vector<cplx> C((size_t)D * D, 0.0);
-  for (int i = 0; i < D; ++i)
-    for (int k = 0; k < D; ++k) {
-      const cplx a = A[(size_t)i * D + k];
-      if (a == cplx(0.0)) continue;
-      for (int j = 0; j < D; ++j) C[(size_t)i * D + j] += a * B[(size_t)k * D + j];
-    }
-  return C;
-}
-inline std::vector<cplx> dagger(const std::vector<cplx>& A, int D) {
-  std::vector<cplx> C((size_t)D * D);
-  for (int i = 0; i < D; ++i)
-    for (int j = 0; j < D; ++j) C[(size_t)j * D + i] = std::conj(A[(size_t)i * D + j]);
-  return C;
-}
-
 // Register groups a pass kernel's thread walks per phase (a run-time loop over
 // the same straight-line phase body): G groups per thread fetch each instruction
 // once per G executions.  Once the slow variants moved out of line the hot body
@@ -351,101 +291,6 @@ inline std::string err_mask_fn(const GenPass& gp) {
 }
 
 
-// A phase takes corrections iff it has sites, none of them renormalises, and every
-// site's light cone has at most PTSBE_FIX_MAX_CONE qubits.  A 2^k-dimensional
-// correction costs ~2^k complex MACs per amplitude plus two CTA barriers; on bench
-// config 4 even k = 1 lost to the out-of-line slow variants (946 K vs 965 K
-// shots/s; k <= 2: 929 K; k <= 3: 922 K), so the default is 0 = off.
-inline bool phase_fixable(const GenProgram& P, const GenPass& gp, const DevPhase& D) {
-  static const int max_cone = [] {   // default 0: see above
-    const char* e = std::getenv("PTSBE_FIX_MAX_CONE");
-    return e ? std::max(0, std::min(4, std::atoi(e))) : 0;
-  }();
-  if (max_cone == 0) return false;
-  bool sites = false;
-  for (int q = D.op_begin; q < D.op_begin + D.n_ops; ++q) {
-    const DevOp& op = gp.ops[q];
-    if (op.kind != 1) continue;
-    sites = true;
-    const ptsbe_channel& ch = P.chans[P.site_chan[op.ref]];
-    if (ch.general) return false;
-  }
-  if (!sites) return false;
-  // every cone must fit the dense kernels (<= 4 register bits)
-  for (int q = D.op_begin; q < D.op_begin + D.n_ops; ++q) {
-    if (gp.ops[q].kind != 1) continue;
-    int cone = (1 << gp.ops[q].k0) | (gp.ops[q].arity == 2 ? (1 << gp.ops[q].k1) : 0);
-    for (int r = q + 1; r < D.op_begin + D.n_ops; ++r) {
-      const DevOp& o = gp.ops[r];
-      const int bits = (1 << o.k0) | (o.arity == 2 ? (1 << o.k1) : 0);
-      if (bits & cone) cone |= bits;
-    }
-    if (__builtin_popcount(cone) > max_cone) return false;
-  }
-  return true;
-}
-
-// Correction tables for every site of the passes' fixable phases (indexed by
-// site id; sites of other phases keep cone = 0).  emats: complex entries.
-inline void build_fix_tables(const GenProgram& P, int n_sites, std::vector<FixSite>& fix, std::vector<cplx>& emats) {
-  fix.assign(std::max(n_sites, 1), FixSite());
-  emats.clear();
-  for (const GenPass& gp : P.passes)
-    for (const DevPhase& D : gp.phases) {
-      if (!phase_fixable(P, gp, D)) continue;
-      const int end = D.op_begin + D.n_ops;
-      for (int q = D.op_begin; q < end; ++q) {
-        const DevOp& so = gp.ops[q];
-        if (so.kind != 1) continue;
-        const ptsbe_channel& ch = P.chans[P.site_chan[so.ref]];
-        int cone = (1 << so.k0) | (so.arity == 2 ? (1 << so.k1) : 0);
-        for (int r = q + 1; r < end; ++r) {
-          const DevOp& o = gp.ops[r];
-          const int bits = (1 << o.k0) | (o.arity == 2 ? (1 << o.k1) : 0);
-          if (bits & cone) cone |= bits;
-        }
-        std::vector<int> cb;
-        for (int b = 0; b < 5; ++b) if ((cone >> b) & 1) cb.push_back(b);
-        const int Dm = 1 << cb.size();
-        // T restricted to the cone: the later ops inside it, default outcomes for sites
-        std::vector<cplx> T((size_t)Dm * Dm, 0.0);
-        for (int i = 0; i < Dm; ++i) T[(size_t)i * Dm + i] = 1.0;
-        int grow = (1 << so.k0) | (so.arity == 2 ? (1 << so.k1) : 0);
-        for (int r = q + 1; r < end; ++r) {
-          const DevOp& o = gp.ops[r];
-          const int bits = (1 << o.k0) | (o.arity == 2 ? (1 << o.k1) : 0);
-          if (!(bits & grow)) continue;
-          grow |= bits;
-          const double* m = nullptr;
-          if (o.kind == 0) m = P.mats + (size_t)o.ref * 32;
-          else {
-            const ptsbe_channel& oc = P.chans[P.site_chan[o.ref]];
-            if (oc.identity_mask & 1ull) continue;
-            m = P.mats + (size_t)oc.mat_base * 32;
-          }
-          T = mmul(embed(m, o.arity, o.k0, o.arity == 2 ? o.k1 : -1, cb), T, Dm);
-        }
-        const std::vector<cplx> Td = dagger(T, Dm);
-        const double* u0 = P.mats + (size_t)ch.mat_base * 32;
-        const std::vector<cplx> U0d = dagger(embed(u0, so.arity, so.k0, so.arity == 2 ? so.k1 : -1, cb), Dm);
-        FixSite f;
-        f.cone = cone;
-        f.dim = Dm;
-        f.base = (int)emats.size();
-        for (int o = 1; o < ch.n_outcomes; ++o) {
-          const double* uo = P.mats + (size_t)(ch.mat_base + o) * 32;
-          bool same = true;
-          for (int i = 0; i < 32; ++i) same = same && uo[i] == u0[i];
-          if (same && o < 32) f.same |= 1 << o;
-          const std::vector<cplx> E = mmul(embed(uo, so.arity, so.k0, so.arity == 2 ? so.k1 : -1, cb), U0d, Dm);
-          const std::vector<cplx> C = mmul(mmul(T, E, Dm), Td, Dm);
-          emats.insert(emats.end(), C.begin(), C.end());
-        }
-        fix[so.ref] = f;
-      }
-    }
-}
-
 // Factor bookkeeping (fast path): each scaled gate applies M/f; per phase the
 // product F_ph is shared by both copies of the phase (same gate code), per pass the
 // magnitude |F| is multiplied back before the tile is stored, and the phase
@@ -488,7 +333,7 @@ inline std::string generate(const GenProgram& P) {
       << "    " << scatter_fn(hmask, "uint32_t") << ",\n"
       << "    " << err_mask_fn(gp) << ",\n"
       << "    [&](V* cur, int b, const uint8_t* sel, long long tile, uint64_t base, double scale, double* red,\n"
-      << "        uint64_t emask, const uint64_t* hits, V* fixm) {\n"
+      << "        uint64_t emask, const uint64_t* hits) {\n"
       << "    const bool active = "
       << (all_active ? std::string("true") : "threadIdx.x < " + std::to_string(groups) + "u") << ";\n"
       << "    V a[" << N << "];\n";
@@ -506,7 +351,6 @@ inline std::string generate(const GenProgram& P) {
       bool has_sites = false;
       for (int q = D.op_begin; q < D.op_begin + D.n_ops; ++q) has_sites = has_sites || gp.ops[q].kind == 1;
       const bool last = ph + 1 == gp.phases.size();
-      const bool fixable = phase_fixable(P, gp, D);
       // slow == true: the trajectory takes a non-default outcome at some site of
       // this phase; sites then read their outcome and apply its operator from the
       // table (same gate code, so the frame factor is unchanged).  Each variant is
@@ -601,7 +445,7 @@ inline std::string generate(const GenProgram& P) {
         return f;
       };
       k << "    { // phase " << ph << "\n";
-      const bool branchy = has_sites && !fixable;   // renormalising sites: fast / slow variants
+      const bool branchy = has_sites;
       if (branchy) k << "    if (!((emask >> " << std::min<size_t>(ph, 63) << ") & 1ull)) {\n";
       const Cx Fph = emit_block(false);
       static const bool no_slow = std::getenv("PTSBE_GEN_ANALYSE_FAST_ONLY") != nullptr;   // offline analysis only
@@ -630,26 +474,6 @@ inline std::string generate(const GenProgram& P) {
       }
       F = cxmul(F, Fph);
       k << "      __syncthreads();\n";
-      if (fixable) {   // corrections for sites that took a non-default outcome (rare; out of line)
-        const std::string fname = "ptsbe_fix_" + std::to_string(pi) + "_" + std::to_string(ph);
-        std::ostringstream fx;
-        fx << "__device__ __noinline__ void " << fname << "(" << ke.V << "* cur, const uint8_t* sel, "
-           << "const uint64_t* hits, const int4* efix, const void* emats, " << ke.V << "* msm) {\n  typedef " << ke.V
-           << " V;\n  uint64_t hw_;\n";
-        int i = 0;
-        for (int q = D.op_begin; q < D.op_begin + D.n_ops; ++q) {
-          const DevOp& op = gp.ops[q];
-          if (op.kind != 1) continue;
-          if (i % 64 == 0) fx << "  hw_ = hits[" << woff[ph] + i / 64 << "];\n";
-          fx << "  if ((hw_ >> " << i % 64 << ") & 1ull) ptg::fix_site<V, " << GB << ">(cur, " << groups << ", "
-             << D.pbits << "u, efix[" << op.ref << "], sel[" << op.ref << "], emats, msm);\n";
-          ++i;
-        }
-        fx << "}\n";
-        slow_fns << fx.str();
-        k << "      if ((emask >> " << std::min<size_t>(ph, 63) << ") & 1ull) " << fname
-          << "(cur, sel, hits, p.efix, p.emats, fixm);\n";
-      }
       k << "    }\n";
     }
     k << "  });\n}\n";
@@ -711,8 +535,7 @@ inline bool compile(const std::string& src, int n_passes, int dev, Module& out, 
 }
 
 inline size_t smem_bytes(int L, int /*c*/, size_t amp_bytes) {
-  // tiles | red | emask | hits | staged correction matrix (16 x 16)
-  return 2 * ((size_t)1 << L) * amp_bytes + 32 * 8 + 16 + 8 * kMaxHitWords + 256 * amp_bytes;
+  return 2 * ((size_t)1 << L) * amp_bytes + 32 * 8 + 16 + 8 * kMaxHitWords;   // tiles | red | emask | hits
 }
 
 }  // namespace gen

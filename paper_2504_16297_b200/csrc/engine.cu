@@ -56,8 +56,6 @@ struct ptsbe_engine {
   std::string gen_note;
   gen::Module gen_mod;
   void* d_mats = nullptr;
-  void* d_emats = nullptr;          // outcome-correction matrices of the generated kernels (codegen.h)
-  int4* d_efix = nullptr;           // [n_sites] correction descriptors
   DevChan* d_chans = nullptr;
   int32_t* d_site_chan = nullptr;
   int32_t* d_slot_site = nullptr;
@@ -110,7 +108,6 @@ struct ptsbe_engine {
   // host-only handle (ptsbe_create_host): load_program plans and generates the
   // pass kernels' source without touching a device (offline SASS inspection)
   bool host_only = false;
-  int n_sites_loading = 0;         // n_sites of the program being loaded (codegen tables)
   std::string gen_src;
   std::string err;
 };
@@ -273,8 +270,6 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero, int p_begin = 0, int p
     p.site_chan = h->d_site_chan;
     p.chans = h->d_chans;
     p.mats = h->d_mats;
-    p.emats = h->d_emats;
-    p.efix = h->d_efix;
     p.nst = h->d_nst;
     p.use_scale = prev_general ? 1 : 0;
     p.gen_zero = (pi == 0 && from_zero) ? (h->zero_vector ? 2 : 1) : 0;
@@ -658,7 +653,7 @@ int ptsbe_destroy(ptsbe_engine* h) {
                   h->d_phases, h->d_matkind,
                   h->d_chans, h->d_site_chan, h->d_slot_site, h->d_partials, h->d_bs, h->d_total, h->d_off,
                   h->d_m, h->d_nuniq, h->d_uoff, h->d_rng, h->d_keys, h->d_tmp, h->d_idx, h->d_runidx,
-                  h->d_runcnt, h->d_chunks, h->d_ent, h->d_forks, h->d_emats, h->d_efix};
+                  h->d_runcnt, h->d_chunks, h->d_ent, h->d_forks};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
@@ -825,7 +820,6 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
       return fail(h, PTSBE_ERR_VALIDATION, "channel %d: arity %d unsupported on device (1 or 2)", k, chans[k].arity);
     for (int o = 0; o < chans[k].n_outcomes; ++o) mat_arity[chans[k].mat_base + o] = chans[k].arity;
   }
-  h->n_sites_loading = n_sites;
   std::vector<PassHost> ph(n_passes);
   const uint64_t nmask = (h->n >= 64) ? ~0ull : ((1ull << h->n) - 1);
   for (int p = 0; p < n_passes; ++p) {
@@ -939,15 +933,6 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
   h->gen_note.clear();
   if (h->host_only) {   // plan + generate only (the generic kernel needs no source)
     h->gen_src = cg_want ? gen_source(h, ph, dops, dph, mats, kinds, chans, site_chan) : std::string();
-    if (cg_want && std::getenv("PTSBE_FIX_STATS")) {   // offline: light-cone sizes of the outcome corrections
-      std::vector<gen::FixSite> fix;
-      std::vector<gen::cplx> em;
-      gen::build_fix_tables(gen_program(h, ph, dops, dph, mats, kinds, chans, site_chan), n_sites, fix, em);
-      int hist[33] = {0};
-      for (auto& f : fix) hist[std::min(f.dim, 32)]++;
-      std::fprintf(stderr, "fix cones: none %d, dim2 %d, dim4 %d, dim8 %d, dim16 %d\n", hist[0], hist[2], hist[4],
-                   hist[8], hist[16]);
-    }
     return 0;
   }
   if (cg_want) {
@@ -1057,29 +1042,6 @@ static int try_codegen(ptsbe_engine* h, int mode, const std::vector<PassHost>& p
   }
   std::string err;
   if (gen::compile(src, (int)ph.size(), h->dev, h->gen_mod, err)) {
-    // outcome corrections of the fixable phases (gen_prelude.cuh fix_site)
-    gen::GenProgram G = gen_program(h, ph, dops, dph, mats, kinds, chans, site_chan);
-    std::vector<gen::FixSite> fix;
-    std::vector<gen::cplx> em;
-    gen::build_fix_tables(G, h->n_sites_loading, fix, em);
-    std::vector<int4> fx(fix.size());
-    for (size_t i = 0; i < fix.size(); ++i) fx[i] = make_int4(fix[i].cone, fix[i].dim, fix[i].base, fix[i].same);
-    if (dalloc(h, &h->d_efix, fx.size())) return PTSBE_ERR_CUDA;
-    CK(h, cudaMemcpy(h->d_efix, fx.data(), fx.size() * sizeof(int4), cudaMemcpyHostToDevice));
-    if (h->d_emats) { cudaFree(h->d_emats); h->d_emats = nullptr; }
-    if (!em.empty()) {
-      if (h->dtype == PTSBE_C64) {
-        std::vector<float2> v(em.size());
-        for (size_t i = 0; i < em.size(); ++i) v[i] = make_float2((float)em[i].real(), (float)em[i].imag());
-        CK(h, cudaMalloc(&h->d_emats, v.size() * sizeof(float2)));
-        CK(h, cudaMemcpy(h->d_emats, v.data(), v.size() * sizeof(float2), cudaMemcpyHostToDevice));
-      } else {
-        std::vector<double2> v(em.size());
-        for (size_t i = 0; i < em.size(); ++i) v[i] = make_double2(em[i].real(), em[i].imag());
-        CK(h, cudaMalloc(&h->d_emats, v.size() * sizeof(double2)));
-        CK(h, cudaMemcpy(h->d_emats, v.data(), v.size() * sizeof(double2), cudaMemcpyHostToDevice));
-      }
-    }
     h->gen_active = true;
   } else {
     h->gen_note = err;

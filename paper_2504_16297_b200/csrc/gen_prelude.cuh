@@ -35,7 +35,6 @@ struct PassParams {
   const void* mats; const int32_t* mat_kind; const double* nst; int use_scale; int gen_zero;
   double* partials; const int32_t* status; int B; long long tiles;
   const int4* ent; int E;   // launch entries {trajectory row, src slot, dst slot, 0}
-  const void* emats; const int4* efix;   // outcome corrections (codegen.h build_fix_tables)
 };
 
 template <typename R> struct Cplx;
@@ -315,82 +314,6 @@ __device__ __noinline__ void err_apply(V* cur, uint32_t gb, uint32_t pbits, int 
   }
 }
 
-// Outcome correction of a unitary-mixture site (codegen.h build_fix_tables).  The
-// phase always runs its fast (default-outcome) code; a site that takes outcome o
-// instead is corrected afterwards by E' = T E_o T^dagger, T = the phase's ops after
-// the site, E_o = U_o U_0^dagger, restricted to the site's light cone in the phase
-// (fx.x = cone register-bit mask, fx.y = 2^|cone|).  It runs on the tile in shared
-// memory after the phase, cooperatively over all register groups, with the matrix
-// staged in shared memory (rows read as broadcasts).  Compact code: the slow path
-// no longer duplicates the phase.
-template <typename V, int GB, int D>
-__device__ __forceinline__ void fix_group(V* cur, uint32_t gb, const uint32_t* pos, const int* cb, uint32_t cone,
-                                          const V* M) {
-  constexpr int N = 1 << GB;
-  for (int j = 0; j < N; ++j) {
-    if (j & cone) continue;
-    V v[D];
-    uint32_t ad[D];
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      int idx = j;
-#pragma unroll
-      for (int m = 0; m < 4; ++m)
-        if ((1 << m) < D && ((d >> m) & 1)) idx |= 1 << cb[m];
-      uint32_t off = 0;
-#pragma unroll
-      for (int q = 0; q < GB; ++q)
-        if ((idx >> q) & 1) off |= pos[q];
-      ad[d] = swz((V*)0, gb | off);
-      v[d] = cur[ad[d]];
-    }
-    V w[D];
-#pragma unroll 1
-    for (int r = 0; r < D; ++r) {
-      V acc = mk((V*)0, 0.0, 0.0);
-#pragma unroll
-      for (int c = 0; c < D; ++c) {
-        const V m = M[r * D + c];
-        acc = pfma(v[c], bc<V>(m.x), pfma(ix(v[c]), bc<V>(m.y), acc));
-      }
-      w[r] = acc;
-    }
-#pragma unroll
-    for (int d = 0; d < D; ++d) cur[ad[d]] = w[d];
-  }
-}
-// CTA-cooperative (every thread calls it with the same arguments).
-template <typename V, int GB>
-__device__ __noinline__ void fix_site(V* cur, int groups, uint32_t pbits, int4 fx, int o, const void* emats, V* msm) {
-  if (o == 0 || (o < 32 && ((fx.w >> o) & 1))) return;   // default outcome, or one equal to it
-  const V* M = reinterpret_cast<const V*>(emats) + fx.z + (size_t)(o - 1) * fx.y * fx.y;
-  for (int i = threadIdx.x; i < fx.y * fx.y; i += blockDim.x) msm[i] = M[i];
-  uint32_t pos[GB];
-  int pb[GB];
-#pragma unroll
-  for (int q = 0; q < GB; ++q) {
-    pb[q] = (pbits >> (5 * q)) & 31;
-    pos[q] = 1u << pb[q];
-  }
-  int cb[4] = {0, 0, 0, 0}, k = 0;
-#pragma unroll
-  for (int q = 0; q < GB; ++q)
-    if (((uint32_t)fx.x >> q) & 1) cb[k++] = q;
-  __syncthreads();
-  for (int g = threadIdx.x; g < groups; g += blockDim.x) {
-    uint32_t gb = (uint32_t)g;
-#pragma unroll
-    for (int q = 0; q < GB; ++q) gb = ins0(gb, pb[q]);
-    switch (fx.y) {
-      case 2: fix_group<V, GB, 2>(cur, gb, pos, cb, (uint32_t)fx.x, msm); break;
-      case 4: fix_group<V, GB, 4>(cur, gb, pos, cb, (uint32_t)fx.x, msm); break;
-      case 8: fix_group<V, GB, 8>(cur, gb, pos, cb, (uint32_t)fx.x, msm); break;
-      default: fix_group<V, GB, 16>(cur, gb, pos, cb, (uint32_t)fx.x, msm); break;
-    }
-  }
-  __syncthreads();
-}
-
 // |0...0> times the program's accumulated global phase G (see codegen.h)
 template <typename V, int N>
 __device__ __forceinline__ void zerog(V (&a)[N], uint64_t base, uint32_t gb, const uint32_t* off, bool active,
@@ -431,7 +354,6 @@ __device__ __forceinline__ void run_pass(const PassParams& p, TileBase tile_base
   double* red = reinterpret_cast<double*>(buf1 + TL);
   uint64_t* emask_s = reinterpret_cast<uint64_t*>(red + 32);
   uint64_t* hits_s = emask_s + 2;   // per-phase hit words (codegen.h err_mask_fn)
-  V* fixm_s = reinterpret_cast<V*>(hits_s + 480);   // staged correction matrix (<= 16 x 16)
   int lb = -1;
   const uint32_t tid = threadIdx.x;
   const uint32_t j0 = tid & ((1u << CPR_LOG) - 1u);
@@ -440,11 +362,24 @@ __device__ __forceinline__ void run_pass(const PassParams& p, TileBase tile_base
   const uint64_t g0 = row_off(r0) + (uint64_t)j0 * VPW;
   const long long total = (long long)p.E << TLOG;
 
+  // Launch entries change every 2^TLOG tiles: the entry record, its row's status
+  // and scale are cached per entry (separately for the prefetch, which runs one
+  // tile ahead), so a tile costs no dependent global loads before its cp.async.
+  int le = -1, ce = -1;          // cached entry index: load side / compute side
+  const V* lsrc = nullptr;       // load side: source state of entry le (nullptr: skip)
+  int4 cen = make_int4(0, 0, 0, 0);
+  bool cdead = false;
+  double cscale_v = 1.0;
   auto load_tile = [&](long long tt, V* dst) {
-    const int4 en = p.ent[(int)(tt >> TLOG)];
-    if (p.gen_zero || p.status[en.x] != 0) return;
-    const V* src = reinterpret_cast<const V*>(p.states) + ((size_t)en.y << p.n) +
-                   tile_base((uint64_t)(tt & ((1ll << TLOG) - 1)));
+    const int e = (int)(tt >> TLOG);
+    if (e != le) {
+      le = e;
+      const int4 en = p.ent[e];
+      lsrc = (p.gen_zero || p.status[en.x] != 0) ? nullptr
+                                                  : reinterpret_cast<const V*>(p.states) + ((size_t)en.y << p.n);
+    }
+    if (!lsrc) return;
+    const V* src = lsrc + tile_base((uint64_t)(tt & ((1ll << TLOG) - 1)));
     if (FAST) {
 #pragma unroll
       for (int k = 0; k < ITER; ++k)
@@ -467,10 +402,16 @@ __device__ __forceinline__ void run_pass(const PassParams& p, TileBase tile_base
     cp_async_commit();
     cp_async_wait1();
     __syncthreads();
-    const int4 en = p.ent[(int)(t >> TLOG)];
+    if ((int)(t >> TLOG) != ce) {
+      ce = (int)(t >> TLOG);
+      cen = p.ent[ce];
+      cdead = p.status[cen.x] != 0;
+      cscale_v = (p.use_scale && !p.gen_zero && !cdead) ? rsqrt(p.nst[cen.x]) : 1.0;
+    }
+    const int4 en = cen;
     const int b = en.x;                          // trajectory row
     const long long tile = t & ((1ll << TLOG) - 1);
-    if (p.status[b] != 0) continue;
+    if (cdead) continue;
     if (b != lb) {   // per trajectory, once: which phases see a non-default outcome
       if (tid == 0) *emask_s = err_mask(p.sel + (size_t)b * p.S, hits_s);
       __syncthreads();
@@ -478,8 +419,8 @@ __device__ __forceinline__ void run_pass(const PassParams& p, TileBase tile_base
     }
     const uint64_t emask = *emask_s;
     const uint64_t base = tile_base((uint64_t)tile);
-    const double scale = (p.use_scale && !p.gen_zero) ? rsqrt(p.nst[b]) : 1.0;
-    body(cur, b, p.sel + (size_t)b * p.S, tile, base, scale, red, emask, hits_s, fixm_s);
+    const double scale = cscale_v;
+    body(cur, b, p.sel + (size_t)b * p.S, tile, base, scale, red, emask, hits_s);
     V* st = reinterpret_cast<V*>(p.states) + ((size_t)en.z << p.n) + base;
     if (FAST) {
 #pragma unroll

@@ -87,8 +87,6 @@ struct PassParams {
   long long tiles;
   const int4* ent;           // [E] launch entries {row, src slot, dst slot, 0}
   int E;
-  const void* emats;         // generated kernels: outcome corrections (codegen.h fix tables), V entries
-  const int4* efix;          // [S] {cone register-bit mask, dim, matrix base, same-as-default outcome mask}
 };
 
 // ---- shared-memory swizzle: spreads the 32 lanes of a phase access over banks
