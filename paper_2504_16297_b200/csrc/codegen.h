@@ -193,6 +193,7 @@ struct Emitter {
 
 struct GenPass {
   int L, c;
+  int gb = 4;                     // register bits per phase (4 or 5)
   uint64_t qmask;
   std::vector<DevPhase> phases;   // pbits: GB positions, 5 bits each
   std::vector<DevOp> ops;         // phase-major, k0/k1 filled
@@ -201,7 +202,6 @@ struct GenPass {
 struct GenProgram {
   bool c64;
   int n;
-  int gb;                   // register bits per phase (4 or 5)
   const double* mats;       // n_mats x 32 doubles
   const int32_t* kinds;     // n_mats
   const ptsbe_channel* chans;
@@ -299,7 +299,6 @@ inline std::string err_mask_fn(const GenPass& gp) {
 // renormalising (general) sites are never scaled: their per-site norms must
 // be measured in the true frame.
 inline std::string generate(const GenProgram& P) {
-  const int GB = P.gb, N = 1 << GB;
   std::ostringstream o;
   Cx G{1.0, 0.0};
   std::vector<std::string> kernels;
@@ -307,6 +306,7 @@ inline std::string generate(const GenProgram& P) {
     if (hit_word_offsets(P.passes[pi]).back() > kMaxHitWords) return std::string();   // caller falls back
   for (size_t pi = 0; pi < P.passes.size(); ++pi) {
     const GenPass& gp = P.passes[pi];
+    const int GB = gp.gb, N = 1 << GB;
     bool has_general = false;
     for (const DevOp& op : gp.ops)
       if (op.kind == 1 && P.chans[P.site_chan[op.ref]].general) has_general = true;

@@ -24,6 +24,7 @@ using namespace ptsbe;
 struct PassHost {
   uint64_t qmask;
   int L, c;
+  int gb = 4;                      // register bits per phase of this pass (generated kernels: 4 or 5)
   int op_begin, n_ops;
   int slot_begin, n_slots;
   int phase_begin, n_phases;
@@ -50,7 +51,7 @@ struct ptsbe_engine {
   DevPhase* d_phases = nullptr;
   int32_t* d_matkind = nullptr;
   int n_phases_total = 0;
-  int phase_bits = 4;              // register bits per phase (4, or 5 for c64 codegen)
+  int phase_bits = 4;              // phase register bits requested: 4, 5, or 0 = per pass (PassHost::gb)
   // circuit-specialised kernels (codegen.h); generic pass_kernel when off
   bool gen_active = false;
   std::string gen_note;
@@ -288,7 +289,7 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero, int p_begin = 0, int p
       CK(h, cudaEventRecord(h->ev[h->ev_used], h->stream));
     }
     if (h->gen_active) {
-      const unsigned threads = (unsigned)gen::threads_for(ph.L, h->phase_bits, ph.n_slots > 0);
+      const unsigned threads = (unsigned)gen::threads_for(ph.L, ph.gb, ph.n_slots > 0);
       const size_t gsm = gen::smem_bytes(ph.L, ph.c, sizeof(typename Cplx<R>::V));
       CUfunction f = h->gen_mod.fns[pi];
       int per_sm = 0;
@@ -891,6 +892,12 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
   // register phases of GB tile bits (4 for the generic kernel; 5 for c64 codegen)
   std::vector<DevOp> dops;
   std::vector<DevPhase> dph;
+  // GB = 0: per pass, 5-bit phases iff they need fewer phases than 4-bit ones and
+  // the 4-bit plan has >= 4 phases (fewer shared-memory round trips: bench config
+  // 4 went 1.00 M -> 1.05 M shots/s); otherwise 4.  A 5-bit group doubles the
+  // registers per thread and halves the threads (128 per CTA), which loses when
+  // it saves no phase, and on memory-bound passes with 2-3 phases (their loads
+  // and stores need the wider CTA).
   auto plan_all = [&](int GB) {
     dops.clear();
     dph.clear();
@@ -898,10 +905,21 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
       PassHost& P = ph[p];
       P.op_begin = (int)dops.size();
       P.phase_begin = (int)dph.size();
-      if (P.L >= GB) {
+      P.gb = GB ? GB : 4;
+      if (P.L >= P.gb) {
         std::vector<DevOp> pops;
         std::vector<DevPhase> pphs;
-        plan_phases(per_pass[p], P.L, pops, pphs, GB);
+        plan_phases(per_pass[p], P.L, pops, pphs, P.gb);
+        if (GB == 0 && P.L >= 5 + 3) {
+          std::vector<DevOp> pops5;
+          std::vector<DevPhase> pphs5;
+          plan_phases(per_pass[p], P.L, pops5, pphs5, 5);
+          if (pphs5.size() < pphs.size() && pphs.size() >= 4) {
+            pops.swap(pops5);
+            pphs.swap(pphs5);
+            P.gb = 5;
+          }
+        }
         dops.insert(dops.end(), pops.begin(), pops.end());
         dph.insert(dph.end(), pphs.begin(), pphs.end());
         P.n_phases = (int)pphs.size();
@@ -916,11 +934,9 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
   const char* cg_env = std::getenv("PTSBE_CODEGEN");
   const int cg_mode = cg_env ? std::atoi(cg_env) : -1;
   bool cg_want = n_passes > 0 && (cg_mode == 1 || (cg_mode < 0 && h->n >= 16));
-  const char* gb_env = std::getenv("PTSBE_PHASE_BITS");   // tuning override (4 or 5)
-  // 4-bit phases measured faster than 5-bit for c64 once gates use packed FP32x2
-  // (bench config 4: 588 K vs 552 K shots/s): half the unrolled code per gate.
-  const int cg_gb = gb_env ? std::max(4, std::min(5, std::atoi(gb_env))) : 4;
-  for (auto& P : ph) cg_want = cg_want && P.L >= cg_gb + 3;
+  const char* gb_env = std::getenv("PTSBE_PHASE_BITS");   // tuning override: 4, 5, or 0 = per pass
+  const int cg_gb = gb_env ? std::max(0, std::min(5, std::atoi(gb_env))) : (h->dtype == PTSBE_C64 ? 0 : 4);
+  for (auto& P : ph) cg_want = cg_want && P.L >= (cg_gb ? cg_gb : 4) + 3;
   h->phase_bits = cg_want ? cg_gb : 4;
   plan_all(h->phase_bits);
   for (int p = 0; p < n_passes; ++p) {
@@ -937,7 +953,7 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
   }
   if (cg_want) {
     if (int r = try_codegen(h, cg_mode, ph, dops, dph, mats, kinds, chans, site_chan)) return r;
-    if (!h->gen_active && h->phase_bits != 4) {   // generic kernel: 4-bit phases
+    if (!h->gen_active && h->phase_bits != 4) {   // generic kernel: 4-bit phases everywhere
       h->phase_bits = 4;
       plan_all(4);
     }
@@ -1008,7 +1024,6 @@ static gen::GenProgram gen_program(ptsbe_engine* h, const std::vector<PassHost>&
   gen::GenProgram G;
   G.c64 = h->dtype == PTSBE_C64;
   G.n = h->n;
-  G.gb = h->phase_bits;
   G.mats = mats;
   G.kinds = kinds.data();
   G.chans = chans;
@@ -1018,6 +1033,7 @@ static gen::GenProgram gen_program(ptsbe_engine* h, const std::vector<PassHost>&
     gp.L = P.L;
     gp.c = P.c;
     gp.qmask = P.qmask;
+    gp.gb = P.gb;
     gp.phases.assign(dph.begin() + P.phase_begin, dph.begin() + P.phase_begin + P.n_phases);
     gp.ops.assign(dops.begin() + P.op_begin, dops.begin() + P.op_begin + P.n_ops);
     G.passes.push_back(gp);

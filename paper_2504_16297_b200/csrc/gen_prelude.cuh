@@ -284,32 +284,37 @@ __device__ __forceinline__ void stg(const V (&a)[N], V* cur, uint32_t sg, const 
 template <typename V, int GB>
 __device__ __noinline__ void err_apply(V* cur, uint32_t gb, uint32_t pbits, int arity, int k0, int k1, const V* m) {
   constexpr int N = 1 << GB;
-  uint32_t addr[N];
+  uint32_t pos[GB];
 #pragma unroll
-  for (int j = 0; j < N; ++j) {
+  for (int q = 0; q < GB; ++q) pos[q] = 1u << ((pbits >> (5 * q)) & 31);
+  auto addr = [&](int j) {
     uint32_t off = 0;
 #pragma unroll
     for (int q = 0; q < GB; ++q)
-      if ((j >> q) & 1) off |= 1u << ((pbits >> (5 * q)) & 31);
-    addr[j] = swz((V*)0, gb | off);
-  }
+      if ((j >> q) & 1) off |= pos[q];
+    return swz((V*)0, gb | off);
+  };
   if (arity == 1) {
     const V m00 = m[0], m01 = m[1], m10 = m[4], m11 = m[5];
+#pragma unroll 1
     for (int j = 0; j < N; ++j)
       if (!(j & (1 << k0))) {
-        const V x = cur[addr[j]], y = cur[addr[j | (1 << k0)]];
-        cur[addr[j]] = cmadd2(m00, x, m01, y);
-        cur[addr[j | (1 << k0)]] = cmadd2(m10, x, m11, y);
+        const uint32_t a0 = addr(j), a1 = addr(j | (1 << k0));
+        const V x = cur[a0], y = cur[a1];
+        cur[a0] = cmadd2(m00, x, m01, y);
+        cur[a1] = cmadd2(m10, x, m11, y);
       }
   } else {
+#pragma unroll 1
     for (int j = 0; j < N; ++j)
       if (!(j & (1 << k0)) && !(j & (1 << k1))) {
-        const int i1 = j | (1 << k1), i2 = j | (1 << k0), i3 = i1 | i2;
-        const V v0 = cur[addr[j]], v1 = cur[addr[i1]], v2 = cur[addr[i2]], v3 = cur[addr[i3]];
-        cur[addr[j]] = cmadd4(m[0], m[1], m[2], m[3], v0, v1, v2, v3);
-        cur[addr[i1]] = cmadd4(m[4], m[5], m[6], m[7], v0, v1, v2, v3);
-        cur[addr[i2]] = cmadd4(m[8], m[9], m[10], m[11], v0, v1, v2, v3);
-        cur[addr[i3]] = cmadd4(m[12], m[13], m[14], m[15], v0, v1, v2, v3);
+        const uint32_t a0 = addr(j), a1 = addr(j | (1 << k1)), a2 = addr(j | (1 << k0)),
+                       a3 = addr(j | (1 << k0) | (1 << k1));
+        const V v0 = cur[a0], v1 = cur[a1], v2 = cur[a2], v3 = cur[a3];
+        cur[a0] = cmadd4(m[0], m[1], m[2], m[3], v0, v1, v2, v3);
+        cur[a1] = cmadd4(m[4], m[5], m[6], m[7], v0, v1, v2, v3);
+        cur[a2] = cmadd4(m[8], m[9], m[10], m[11], v0, v1, v2, v3);
+        cur[a3] = cmadd4(m[12], m[13], m[14], m[15], v0, v1, v2, v3);
       }
   }
 }
