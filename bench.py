@@ -329,7 +329,8 @@ def main():
         "data": "synthetic (PTS-sampled Kraus selections of a generated circuit)",
         "config": {"workload": "config4 steane_blocks(4): 28 q, %d ops, %d sites" % (len(c.ops), len(c.sites)),
                    "batch_per_gpu": B, "shots_per_trajectory": SHOTS, "passes": prog.n_passes, "g_ref": prog.g_ref,
-                   "rng": args.rng, "l2": "inputs larger than L2 (2 GiB states)", "parallelism": f"traj-dp{world}"},
+                   "rng": args.rng, "l2": "inputs larger than L2 (2 GiB states)", "parallelism": f"traj-dp{world}",
+                   "codegen": bool(eng.info()["codegen"])},
         "trajectories_per_s": total_traj / (ms / 1e3),
         "traj_roofline_frac": (total_traj / (ms / 1e3)) / (hbm * 1e9 * world / traj_bytes),
         "roofline": roofline,

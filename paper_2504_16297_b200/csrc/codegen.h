@@ -59,8 +59,17 @@ inline Api& api() {
   static Api a;
   static std::once_flag once;
   std::call_once(once, [] {
-    void* lib = dlopen("libnvrtc.so.12", RTLD_NOW | RTLD_LOCAL);
+    // The CUDA toolkit's NVRTC first (the one nvcc ships with): a process that
+    // imported torch already has torch's bundled NVRTC under the same soname, and
+    // that older ptxas materialises i*x with MOV + FADD instead of the FFMA2 .NP
+    // operand modifier (config 4: +2.1 K instructions, hot bodies 20% larger).
+    void* lib = nullptr;
+    if (const char* home = std::getenv("CUDA_HOME")) {
+      const std::string path = std::string(home) + "/lib64/libnvrtc.so.12";
+      lib = dlopen(path.c_str(), RTLD_NOW | RTLD_LOCAL);
+    }
     if (!lib) lib = dlopen("/usr/local/cuda/lib64/libnvrtc.so.12", RTLD_NOW | RTLD_LOCAL);
+    if (!lib) lib = dlopen("libnvrtc.so.12", RTLD_NOW | RTLD_LOCAL);
     if (!lib) { a.why = "libnvrtc.so.12 not found"; return; }
     a.create = (nvrtcCreateProgram_t)dlsym(lib, "nvrtcCreateProgram");
     a.compile = (nvrtcCompileProgram_t)dlsym(lib, "nvrtcCompileProgram");

@@ -301,3 +301,13 @@ def test_shared_trunk_schedule_is_bit_identical(cfg, dtype, monkeypatch):
     assert np.array_equal(out["1"][0], out["0"][0]) and np.array_equal(out["1"][1], out["0"][1])
     for a, b in zip(out["1"][2], out["0"][2]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("cfg,dtype", [(3, "c64"), (4, "c64"), (4, "c128")])
+def test_circuit_specialised_kernels_are_active(cfg, dtype):
+    """The generated (NVRTC) pass kernels compile and load for the bench-size programs: the
+    generic interpreter kernel is a correctness fallback only, it must not be what runs."""
+    c = workloads.build(cfg, P.parse_circuit, P.parse_noise_model, P.attach_noise)
+    with Engine(c.n_qubits, dtype, batch_cap=1) as eng:
+        eng.load(c)
+        assert eng.info()["codegen"] == 1

@@ -1,5 +1,5 @@
 """Offline look at the generated pass kernels (no GPU): plan a config, generate its
-CUDA source on a host-only handle, compile it with nvcc for sm_100a and report per
+CUDA source on a host-only handle, compile it with NVRTC (as the engine does) for sm_100a and report per
 pass kernel registers, spills, SASS size and instruction mix.
 
   python tools/gen_offline.py [config] [dtype] [--keep DIR]
@@ -22,10 +22,31 @@ src = generated_source(prog, dtype)
 cu = os.path.join(out, f"gen_cfg{cfg}_{dtype}.cu")
 open(cu, "w").write(src)
 cubin = cu[:-3] + ".cubin"
-r = subprocess.run(["nvcc", "-cubin", "-arch=sm_100a", "-std=c++17", "-lineinfo", "-Xptxas", "-v", "-o", cubin, cu],
-                   capture_output=True, text=True)
-if r.returncode:
-    print(r.stderr[-3000:]); sys.exit(1)
+# compile exactly as the engine does: the CUDA toolkit's NVRTC (codegen.h api()), same options
+import ctypes as C
+import torch  # noqa: F401  (the bench/tests process has torch's own NVRTC loaded too)
+nv = C.CDLL(os.environ.get("PTSBE_NVRTC", "/usr/local/cuda/lib64/libnvrtc.so.12"), mode=os.RTLD_NOW | os.RTLD_LOCAL)
+maj, mnr = C.c_int(), C.c_int()
+nv.nvrtcVersion(C.byref(maj), C.byref(mnr))
+nvprog = C.c_void_p()
+assert nv.nvrtcCreateProgram(C.byref(nvprog), src.encode(), b"ptsbe_gen.cu", 0, None, None) == 0
+opts = [b"--gpu-architecture=sm_100a", b"-std=c++17", b"-lineinfo", b"--device-as-default-execution-space",
+        b"-Xptxas", b"-v"]
+arr = (C.c_char_p * len(opts))(*opts)
+rc = nv.nvrtcCompileProgram(nvprog, len(opts), arr)
+n = C.c_size_t()
+nv.nvrtcGetProgramLogSize(nvprog, C.byref(n))
+log = C.create_string_buffer(n.value)
+nv.nvrtcGetProgramLog(nvprog, log)
+if rc:
+    print(log.value.decode()[-3000:]); sys.exit(1)
+nv.nvrtcGetCUBINSize(nvprog, C.byref(n))
+buf = C.create_string_buffer(n.value)
+nv.nvrtcGetCUBIN(nvprog, buf)
+open(cubin, "wb").write(buf.raw)
+class R: pass
+r = R(); r.stderr = log.value.decode()
+print(f"NVRTC {maj.value}.{mnr.value}")
 regs = {}
 cur = None
 for line in r.stderr.splitlines():
