@@ -111,6 +111,109 @@ inline uint32_t swz_host(bool c64, uint32_t i) {
   return i ^ (h & 7u);
 }
 
+// Shared-memory swizzle of one pass: slot(i) = i ^ XOR_{b set in i} m[b], where
+// only bits above the bank-select bits carry masks and the masks touch only the
+// bank-select bits (c64: bits 1-3 of the 8-B amplitude index, bit 0 stays so
+// amplitude pairs remain aligned 16-B vectors; c128: bits 0-2).  Linear over
+// GF(2) and triangular, hence a bijection, and slot(a ^ b) = slot(a) ^ slot(b),
+// so every phase address is a per-thread base XOR a compile-time constant.
+struct Swizzle {
+  bool c64 = true;
+  uint32_t m[32] = {0};
+  uint32_t operator()(uint32_t i) const {
+    uint32_t r = i;
+    for (int b = 0; b < 32; ++b)
+      if ((i >> b) & 1u) r ^= m[b];
+    return r;
+  }
+  static Swizzle fixed(bool c64) {   // the default map (swz_host)
+    Swizzle z;
+    z.c64 = c64;
+    for (int b = 0; b < 20; ++b) z.m[b] = swz_host(c64, 1u << b) ^ (1u << b);
+    return z;
+  }
+};
+
+inline uint32_t ins0_host(uint32_t p, int bit) {
+  const uint32_t lo = p & ((1u << bit) - 1u);
+  return ((p ^ lo) << 1) | lo;
+}
+
+// Shared-memory wavefronts of one warp's phase loads (stores are symmetric) under
+// swizzle z: lanes 0..31 hold consecutive register groups.  16-B accesses (c128,
+// or c64 phases holding bit 0, which load amplitude pairs) are served per quarter
+// warp by distinct 16-B chunks of a 128-B line; 8-B accesses per warp by slot load
+// (>= 2).  Minimum = conflict free.
+inline int phase_wavefronts(const Swizzle& z, const DevPhase& D, int GB) {
+  int pb[5];
+  for (int q = 0; q < GB; ++q) pb[q] = (int)((D.pbits >> (5 * q)) & 31);
+  uint32_t lanes[32];
+  for (int l = 0; l < 32; ++l) {
+    uint32_t g = (uint32_t)l;
+    for (int q = 0; q < GB; ++q) g = ins0_host(g, pb[q]);
+    lanes[l] = g;
+  }
+  const bool wide = !z.c64 || pb[0] == 0;
+  int tot = 0;
+  for (int j = 0; j < (1 << GB); j += (z.c64 && wide) ? 2 : 1) {
+    uint32_t off = 0;
+    for (int q = 0; q < GB; ++q)
+      if ((j >> q) & 1) off |= 1u << pb[q];
+    if (wide) {
+      for (int qw = 0; qw < 4; ++qw) {
+        int cnt[8] = {0}, mx = 0;
+        for (int l = qw * 8; l < qw * 8 + 8; ++l) {
+          const uint32_t a = z(lanes[l] | off);
+          const int c = z.c64 ? (int)((a >> 1) & 7u) : (int)(a & 7u);
+          mx = std::max(mx, ++cnt[c]);
+        }
+        tot += mx;
+      }
+    } else {
+      int cnt[16] = {0}, mx = 0;
+      for (int l = 0; l < 32; ++l) mx = std::max(mx, ++cnt[z(lanes[l] | off) & 15u]);
+      tot += std::max(2, mx);
+    }
+  }
+  return tot;
+}
+
+// Per pass: coordinate descent over the masks of the tile bits above the
+// bank-select bits, from the default map, minimising the phases' wavefronts.
+inline Swizzle choose_swizzle(bool c64, int L, const std::vector<DevPhase>& phases, int GB) {
+  Swizzle best = Swizzle::fixed(c64);
+  for (int b = L; b < 32; ++b) best.m[b] = 0;
+  auto cost = [&](const Swizzle& z) {
+    int t = 0;
+    for (const DevPhase& D : phases) t += phase_wavefronts(z, D, GB);
+    return t;
+  };
+  int bc = cost(best);
+  const int lo = c64 ? 4 : 3;
+  for (int sweep = 0; sweep < 3; ++sweep) {
+    bool improved = false;
+    for (int b = lo; b < L; ++b)
+      for (uint32_t v = 0; v < 8; ++v) {
+        Swizzle cand = best;
+        cand.m[b] = c64 ? (v << 1) : v;
+        const int c = cost(cand);
+        if (c < bc) { bc = c; best = cand; improved = true; }
+      }
+    if (!improved) break;
+  }
+  return best;
+}
+
+// Device functor for a swizzle (compile-time masks).
+inline std::string swizzle_struct(const std::string& name, const Swizzle& z, int L) {
+  std::ostringstream o;
+  o << "struct " << name << " { __device__ __forceinline__ uint32_t operator()(uint32_t i) const { return i";
+  for (int b = 0; b < L; ++b)
+    if (z.m[b]) o << " ^ ((0u - ((i >> " << b << ") & 1u)) & " << z.m[b] << "u)";
+  o << "; } };\n";
+  return o.str();
+}
+
 // Complex scalar helpers for the host-side factor bookkeeping.
 struct Cx { double re, im; };
 inline Cx cxmul(Cx a, Cx b) { return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
@@ -328,6 +431,9 @@ inline std::string generate(const GenProgram& P) {
     const uint64_t nmask = P.n >= 64 ? ~0ull : ((1ull << P.n) - 1);
     const uint64_t comp = ~gp.qmask & nmask;
     const uint64_t hmask = gp.qmask & ~((1ull << gp.c) - 1);
+    const Swizzle sw = std::getenv("PTSBE_FIXED_SWIZZLE") ? Swizzle::fixed(P.c64)   // A/B knob
+                                                        : choose_swizzle(P.c64, gp.L, gp.phases, GB);
+    const std::string swname = "Swz" + std::to_string(pi);
     Emitter ke(P.c64);
     std::ostringstream slow_fns;   // out-of-line slow variants of this pass's phases
     const std::vector<int> woff = hit_word_offsets(gp);
@@ -337,7 +443,7 @@ inline std::string generate(const GenProgram& P) {
       << kernel_name((int)pi) << "(const ptg::PassParams p) {\n"
       << "  typedef " << ke.V << " V;\n"
       << "  ptg::run_pass<" << ke.R << ", " << gp.L << ", " << gp.c << ", " << (P.n - gp.L) << ", " << threads
-      << ">(p,\n"
+      << ">(p, " << swname << "(),\n"
       << "    " << scatter_fn(comp, "uint64_t") << ",\n"
       << "    " << scatter_fn(hmask, "uint32_t") << ",\n"
       << "    " << err_mask_fn(gp) << ",\n"
@@ -355,7 +461,7 @@ inline std::string generate(const GenProgram& P) {
         off[j] = 0;
         for (int q = 0; q < GB; ++q)
           if ((j >> q) & 1) off[j] |= 1u << pb[q];
-        so[j] = swz_host(P.c64, off[j]);
+        so[j] = sw(off[j]);
       }
       bool has_sites = false;
       for (int q = D.op_begin; q < D.op_begin + D.n_ops; ++q) has_sites = has_sites || gp.ops[q].kind == 1;
@@ -384,14 +490,17 @@ inline std::string generate(const GenProgram& P) {
           const int si = site_i++;
           if (slow) {
             // hit: this trajectory's outcome at the site is not 0 -> apply it from the table
-            k << "      if ((hw_[" << si / 64 << "] >> " << si % 64 << ") & 1ull) { const int o_ = sel[" << op.ref
+            // 32-bit halves + immediate mask: one predicate-setting LOP3 per site on the no-hit path
+            k << "      if (__builtin_expect(((uint32_t)(hw_[" << si / 64 << "] >> " << (si % 64 >= 32 ? 32 : 0)
+              << ") & 0x" << std::hex << (1u << (si % 32)) << std::dec << "u) != 0, 0)) { const int o_ = sel[" << op.ref
               << "];\n"
               << "        if (!((0x" << std::hex << ch.identity_mask << std::dec << "ull >> o_) & 1ull)) {\n"
               << "          const V* m_ = reinterpret_cast<const V*>(p.mats) + (size_t)(" << ch.mat_base
               << " + o_) * 16;\n";
             if (ch.identity_mask & 1ull) {   // through the tile slots (no register shuffle on the no-hit path)
               k << "          if (active) { ptg::stg<V, " << N << ", " << pb[0] << ">(a, cur, sg, so, true);\n"
-                << "            ptg::err_apply<V, " << GB << ">(cur, gb, " << D.pbits << "u, " << op.arity << ", "
+                << "            ptg::err_apply<V, " << GB << ", " << swname << ">(cur, gb, " << D.pbits << "u, "
+            << op.arity << ", "
                 << op.k0 << ", " << k1 << ", m_);\n"
                 << "            ptg::ldg<V, " << N << ", " << pb[0] << ">(a, cur, sg, so, true, 1.0); }\n";
             } else {
@@ -430,7 +539,7 @@ inline std::string generate(const GenProgram& P) {
         for (int q = 0; q < GB; ++q) k << "ptg::ins0(";
         k << "g";
         for (int q = 0; q < GB; ++q) k << ", " << pb[q] << ")";
-        k << ";\n      const uint32_t sg = ptg::swz((V*)0, gb);\n      const uint32_t so[" << N << "] = {";
+        k << ";\n      const uint32_t sg = " << swname << "()(gb);\n      const uint32_t so[" << N << "] = {";
         for (int j = 0; j < N; ++j) k << so[j] << "u" << (j + 1 < N ? ", " : "");
         k << "};\n";
         if (ph == 0) {
@@ -488,7 +597,7 @@ inline std::string generate(const GenProgram& P) {
     k << "  });\n}\n";
     const double mag = cxabs(F);
     G = cxmul(G, Cx{F.re / mag, F.im / mag});
-    kernels.push_back(slow_fns.str() + k.str());
+    kernels.push_back(swizzle_struct(swname, sw, gp.L) + slow_fns.str() + k.str());
   }
   o << kGenPrelude << "\n"
     << "#define GZERO_RE " << hexd(G.re) << "\n#define GZERO_IM " << hexd(G.im) << "\n";

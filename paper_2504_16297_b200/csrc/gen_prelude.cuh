@@ -203,14 +203,7 @@ template <typename V, int N> __device__ __forceinline__ void rscale(V (&a)[N], d
 }
 
 // ---- addressing
-__device__ __forceinline__ uint32_t swz(float2*, uint32_t i) {   // never flips bit 0
-  const uint32_t h = (i >> 3) ^ (i >> 7) ^ ((i >> 7) << 1) ^ (i >> 11);
-  return i ^ (h & 14u);
-}
-__device__ __forceinline__ uint32_t swz(double2*, uint32_t i) {
-  const uint32_t h = (i >> 3) ^ (i >> 6) ^ ((i >> 6) << 1) ^ (i >> 9) ^ (i >> 12);
-  return i ^ (h & 7u);
-}
+// (shared-memory swizzles are per pass: codegen.h Swizzle / swizzle_struct)
 __device__ __forceinline__ uint32_t ins0(uint32_t p, int bit) {
   const uint32_t lo = p & ((1u << bit) - 1u);
   return ((p ^ lo) << 1) | lo;
@@ -281,7 +274,7 @@ __device__ __forceinline__ void stg(const V (&a)[N], V* cur, uint32_t sg, const 
 // register path means the per-site branch joins with the registers unchanged,
 // so the common (no-hit) path pays no register-shuffling moves.  k0 / k1 are
 // register-bit positions (first-listed target = MSB of the local index).
-template <typename V, int GB>
+template <typename V, int GB, class Sw>
 __device__ __noinline__ void err_apply(V* cur, uint32_t gb, uint32_t pbits, int arity, int k0, int k1, const V* m) {
   constexpr int N = 1 << GB;
   uint32_t pos[GB];
@@ -292,7 +285,7 @@ __device__ __noinline__ void err_apply(V* cur, uint32_t gb, uint32_t pbits, int 
 #pragma unroll
     for (int q = 0; q < GB; ++q)
       if ((j >> q) & 1) off |= pos[q];
-    return swz((V*)0, gb | off);
+    return Sw()(gb | off);
   };
   if (arity == 1) {
     const V m00 = m[0], m01 = m[1], m10 = m[4], m11 = m[5];
@@ -340,9 +333,9 @@ __device__ __forceinline__ void zerog(V (&a)[N], uint64_t base, uint32_t gb, con
 // per trajectory (and fills the hit words).  body(cur, b, sel_row, tile, base,
 // scale, red, emask, hits) runs
 // the pass's phases on one tile.
-template <typename R, int L, int C, int TLOG, int NT, class TileBase, class RowOff, class ErrMask, class Body>
-__device__ __forceinline__ void run_pass(const PassParams& p, TileBase tile_base, RowOff row_off, ErrMask err_mask,
-                                         Body body) {
+template <typename R, int L, int C, int TLOG, int NT, class Sw, class TileBase, class RowOff, class ErrMask, class Body>
+__device__ __forceinline__ void run_pass(const PassParams& p, Sw swz_, TileBase tile_base, RowOff row_off,
+                                         ErrMask err_mask, Body body) {
   typedef typename Cplx<R>::V V;
   typedef typename Cplx<R>::W W;
   constexpr int VPW = sizeof(W) / sizeof(V);
@@ -363,7 +356,7 @@ __device__ __forceinline__ void run_pass(const PassParams& p, TileBase tile_base
   const uint32_t tid = threadIdx.x;
   const uint32_t j0 = tid & ((1u << CPR_LOG) - 1u);
   const uint32_t r0 = tid >> CPR_LOG;
-  const uint32_t s0 = swz((V*)0, (r0 << C) | (j0 * VPW));
+  const uint32_t s0 = swz_((r0 << C) | (j0 * VPW));
   const uint64_t g0 = row_off(r0) + (uint64_t)j0 * VPW;
   const long long total = (long long)p.E << TLOG;
 
@@ -388,11 +381,11 @@ __device__ __forceinline__ void run_pass(const PassParams& p, TileBase tile_base
     if (FAST) {
 #pragma unroll
       for (int k = 0; k < ITER; ++k)
-        cp_async16(dst + (s0 ^ swz((V*)0, (uint32_t)(k * RSTEP) << C)), src + g0 + row_off((uint32_t)(k * RSTEP)));
+        cp_async16(dst + (s0 ^ swz_((uint32_t)(k * RSTEP) << C)), src + g0 + row_off((uint32_t)(k * RSTEP)));
     } else {
       for (uint32_t u = tid; u < NVEC; u += blockDim.x) {
         const uint32_t r = u >> CPR_LOG, j = u & ((1u << CPR_LOG) - 1u);
-        cp_async16(dst + swz((V*)0, (r << C) | (j * VPW)), src + row_off(r) + (uint64_t)j * VPW);
+        cp_async16(dst + swz_((r << C) | (j * VPW)), src + row_off(r) + (uint64_t)j * VPW);
       }
     }
   };
@@ -430,13 +423,13 @@ __device__ __forceinline__ void run_pass(const PassParams& p, TileBase tile_base
     if (FAST) {
 #pragma unroll
       for (int k = 0; k < ITER; ++k) {
-        const W w = *reinterpret_cast<const W*>(cur + (s0 ^ swz((V*)0, (uint32_t)(k * RSTEP) << C)));
+        const W w = *reinterpret_cast<const W*>(cur + (s0 ^ swz_((uint32_t)(k * RSTEP) << C)));
         st_stream(reinterpret_cast<W*>(st + g0 + row_off((uint32_t)(k * RSTEP))), w);
       }
     } else {
       for (uint32_t u = tid; u < NVEC; u += blockDim.x) {
         const uint32_t r = u >> CPR_LOG, j = u & ((1u << CPR_LOG) - 1u);
-        const W w = *reinterpret_cast<const W*>(cur + swz((V*)0, (r << C) | (j * VPW)));
+        const W w = *reinterpret_cast<const W*>(cur + swz_((r << C) | (j * VPW)));
         st_stream(reinterpret_cast<W*>(st + row_off(r) + (uint64_t)j * VPW), w);
       }
     }
