@@ -443,7 +443,7 @@ inline std::string generate(const GenProgram& P) {
       << kernel_name((int)pi) << "(const ptg::PassParams p) {\n"
       << "  typedef " << ke.V << " V;\n"
       << "  ptg::run_pass<" << ke.R << ", " << gp.L << ", " << gp.c << ", " << (P.n - gp.L) << ", " << threads
-      << ">(p, " << swname << "(),\n"
+      << ", " << (pi + 1 == P.passes.size() ? "true" : "false") << ">(p, " << swname << "(),\n"
       << "    " << scatter_fn(comp, "uint64_t") << ",\n"
       << "    " << scatter_fn(hmask, "uint32_t") << ",\n"
       << "    " << err_mask_fn(gp) << ",\n"

@@ -109,6 +109,13 @@ struct ptsbe_engine {
   // host-only handle (ptsbe_create_host): load_program plans and generates the
   // pass kernels' source without touching a device (offline SASS inspection)
   bool host_only = false;
+  // fused sampler block sums: the last generated pass of a unitary program writes
+  // d_bs in TILE order of its geometry (gen_prelude.cuh run_pass); valid until the
+  // states change by other means
+  bool any_general = false;
+  bool tsum_ok = false;
+  uint64_t tsum_qmask = 0;
+  int tsum_L = 0, tsum_c = 0, tsum_threads = 0;
   std::string gen_src;
   std::string err;
 };
@@ -177,6 +184,7 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero, int p_begin = 0, int p
   if (p_end < 0) p_end = (int)h->passes.size();
   // a continued range (sharded segments) inherits the deferred-rescale state
   bool prev_general = p_begin > 0 ? h->final_general : false;
+  h->tsum_ok = false;
   if (h->passes.empty()) {
     if (from_zero) {
       init_zero_kernel<R><<<1184, 256, 0, h->stream>>>(h->states, h->n, B, h->zero_vector ? 1 : 0);
@@ -196,6 +204,12 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero, int p_begin = 0, int p
   const int trunk = h->cap;
   std::vector<int> fpass(B, 0);
   const bool tree = from_zero && p_begin == 0 && p_end == P && P >= 2 && h->tree_enabled && !h->host_sel.empty();
+  h->tsum_ok = false;
+  // (a sampler block must be exactly one warp's amplitudes of the last pass's tile)
+  const bool fuse_sums = h->gen_active && !h->any_general && from_zero && p_begin == 0 && p_end == P && P >= 1 &&
+                         (32ll << h->passes[P - 1].L) / gen::threads_for(h->passes[P - 1].L, h->passes[P - 1].gb, false) ==
+                             (1ll << h->sbits) &&
+                         !std::getenv("PTSBE_NO_FUSED_SUMS");
   if (tree) {
     for (int b = 0; b < B; ++b) {
       int f = P - 1;
@@ -256,6 +270,10 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero, int p_begin = 0, int p
     PassParams p;
     p.ent = h->d_ent + ent_begin[pi];
     p.E = E;
+    const bool last_fused = fuse_sums && (int)pi == P - 1;
+    p.tsum = last_fused ? h->d_bs : nullptr;
+    p.tsum_stride = h->nblk;
+    p.tsum_sbits = h->sbits;
     p.states = h->states;
     p.n = h->n;
     p.L = ph.L;
@@ -331,12 +349,20 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero, int p_begin = 0, int p
     prev_general = ph.n_slots > 0;
   }
   h->final_general = prev_general;
+  if (fuse_sums) {
+    h->tsum_ok = true;
+    h->tsum_qmask = h->passes[P - 1].qmask;
+    h->tsum_L = h->passes[P - 1].L;
+    h->tsum_c = h->passes[P - 1].c;
+    h->tsum_threads = gen::threads_for(h->passes[P - 1].L, h->passes[P - 1].gb, false);
+  }
   return 0;
 }
 
 // Re-store state b in logical (to_logical) or physical order.
 int relayout(ptsbe_engine* h, int b, bool to_logical) {
   if (!h->permuted || (h->logical[b] != 0) == to_logical) return 0;
+  h->tsum_ok = false;
   const size_t bytes = ((size_t)1 << h->n) * h->amp_bytes;
   char* st = (char*)h->states + (size_t)b * bytes;
   void* scratch = nullptr;
@@ -474,6 +500,11 @@ int sample_impl(ptsbe_engine* h, int B, const int64_t* shots, int rng_mode, cons
   sp.total = h->d_total;
   sp.off = h->d_off;
   sp.m = h->d_m;
+  sp.tiled = 0;
+  sp.tq = h->tsum_qmask;
+  sp.tL = h->tsum_L;
+  sp.tC = h->tsum_c;
+  sp.tT = h->tsum_threads;
 
   // Exact RNG modes replay the reference's CDF, which runs in LOGICAL index
   // order: canonicalise permuted states first.  Philox mode samples the physical
@@ -489,10 +520,19 @@ int sample_impl(ptsbe_engine* h, int B, const int64_t* shots, int rng_mode, cons
       unperm = true;
     }
   }
+  // Philox mode on the fused block sums of the last pass: no state read here; the
+  // CDF runs in that pass's tile order, so indices are mapped back and re-sorted.
+  bool some_logical = false;
+  for (int b = 0; b < B; ++b) some_logical = some_logical || h->logical[b];
+  const bool tiled = h->tsum_ok && rng_mode == PTSBE_RNG_PHILOX && !some_logical;
   if (total > 0) {
-    dim3 g1((unsigned)((h->nblk + 7) / 8), (unsigned)B);
-    sample_blocksum<R><<<g1, 256, 0, h->stream>>>(sp);
-    CKL(h);
+    if (tiled) {
+      sp.tiled = 1;
+    } else {
+      dim3 g1((unsigned)((h->nblk + 7) / 8), (unsigned)B);
+      sample_blocksum<R><<<g1, 256, 0, h->stream>>>(sp);
+      CKL(h);
+    }
     sample_blockscan<<<B, 1024, 0, h->stream>>>(sp);
     CKL(h);
     const unsigned gw = (unsigned)((n_chunks * 32 + 255) / 256);
@@ -516,10 +556,12 @@ int sample_impl(ptsbe_engine* h, int B, const int64_t* shots, int rng_mode, cons
     }
     sample_resolve<R><<<gw, 256, 0, h->stream>>>(sp, h->d_chunks, n_chunks, h->d_keys, h->d_idx);
     CKL(h);
-    if (unperm) {   // physical -> logical bitstrings, then ascending order again
-      unpermute_indices<<<std::min<long long>((total + 255) / 256, 4096), 256, 0, h->stream>>>(h->d_idx, total,
-                                                                                                 h->layout);
-      CKL(h);
+    if (unperm || tiled) {   // physical -> logical bitstrings, then ascending order again
+      if (h->permuted) {
+        unpermute_indices<<<std::min<long long>((total + 255) / 256, 4096), 256, 0, h->stream>>>(h->d_idx, total,
+                                                                                                   h->layout);
+        CKL(h);
+      }
       seg_radix_sort<<<B, 1024, 0, h->stream>>>(h->d_idx, h->d_tmp, h->d_off, h->d_m, h->d_status, h->n);
       CKL(h);
     }
@@ -889,6 +931,8 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
       if (o.general) { o.d.slot = P.n_slots++; slot_site.push_back(o.d.ref); }
     P.slot_begin = (int)slot_site.size() - P.n_slots;
   }
+  h->any_general = !slot_site.empty();
+  h->tsum_ok = false;
   // register phases of GB tile bits (4 for the generic kernel; 5 for c64 codegen)
   std::vector<DevOp> dops;
   std::vector<DevPhase> dph;
@@ -1087,6 +1131,7 @@ int ptsbe_exchange_half(ptsbe_engine* h, int b, int bit, int value, void* buf, i
     return fail(h, PTSBE_ERR_VALIDATION, "bad exchange arguments (state %d, bit %d, value %d)", b, bit, value);
   CK(h, cudaSetDevice(h->dev));
   if (h->permuted) return fail(h, PTSBE_ERR_VALIDATION, "sharded exchange needs an unpermuted engine layout");
+  if (unpack) h->tsum_ok = false;
   const size_t per = ((size_t)1 << h->n);
   const unsigned g = (unsigned)std::min<size_t>(per / 512 + 1, 8192);
   if (h->dtype == PTSBE_C64) {
@@ -1200,6 +1245,7 @@ int ptsbe_set_state(ptsbe_engine* h, int b, const void* buf, uint32_t flags) {
   CK(h, cudaStreamSynchronize(h->stream));
   h->last_B = std::max(h->last_B, b + 1);
   h->final_general = false;
+  h->tsum_ok = false;
   return 0;
 }
 

@@ -35,6 +35,7 @@ struct PassParams {
   const void* mats; const int32_t* mat_kind; const double* nst; int use_scale; int gen_zero;
   double* partials; const int32_t* status; int B; long long tiles;
   const int4* ent; int E;   // launch entries {trajectory row, src slot, dst slot, 0}
+  uint64_t* tsum; long long tsum_stride; int tsum_sbits;   // fused sampler block sums (last pass)
 };
 
 template <typename R> struct Cplx;
@@ -80,6 +81,14 @@ template <typename V> __device__ __forceinline__ V cmadd4(V m0, V m1, V m2, V m3
   r = pfma(ix(c), bc<V, R>(m2.y), r);
   r = pfma(d, bc<V, R>(m3.x), r);
   return pfma(ix(d), bc<V, R>(m3.y), r);
+}
+// Fixed-point probability of the fused sampler sums (2^-62 units); identical
+// definition in sample_kernels.cuh qfix (the resolve step recomputes it).
+__device__ __forceinline__ uint64_t qfix(float2 a) {
+  return __float2ull_rn(__fmul_rn(__fmaf_rn(a.x, a.x, __fmul_rn(a.y, a.y)), 0x1p62f));
+}
+__device__ __forceinline__ uint64_t qfix(double2 a) {
+  return __double2ull_rn(__dmul_rn(__fma_rn(a.x, a.x, __dmul_rn(a.y, a.y)), 0x1p62));
 }
 __device__ __forceinline__ double prob64(float2 a) {
   const double x = a.x, y = a.y;
@@ -333,7 +342,8 @@ __device__ __forceinline__ void zerog(V (&a)[N], uint64_t base, uint32_t gb, con
 // per trajectory (and fills the hit words).  body(cur, b, sel_row, tile, base,
 // scale, red, emask, hits) runs
 // the pass's phases on one tile.
-template <typename R, int L, int C, int TLOG, int NT, class Sw, class TileBase, class RowOff, class ErrMask, class Body>
+template <typename R, int L, int C, int TLOG, int NT, bool SUMS, class Sw, class TileBase, class RowOff, class ErrMask,
+          class Body>
 __device__ __forceinline__ void run_pass(const PassParams& p, Sw swz_, TileBase tile_base, RowOff row_off,
                                          ErrMask err_mask, Body body) {
   typedef typename Cplx<R>::V V;
@@ -420,7 +430,28 @@ __device__ __forceinline__ void run_pass(const PassParams& p, Sw swz_, TileBase 
     const double scale = cscale_v;
     body(cur, b, p.sel + (size_t)b * p.S, tile, base, scale, red, emask, hits_s);
     V* st = reinterpret_cast<V*>(p.states) + ((size_t)en.z << p.n) + base;
-    if (FAST) {
+    if (SUMS && FAST && p.tsum) {
+      // Last pass of a unitary program: the sampler's block sums of q = qfix(a)
+      // (2^-62 fixed point) are produced here, so sampling needs no separate read
+      // of the states.  CDF order inside a tile is THREAD-major (thread, k, vector
+      // element): a 2^sbits block is one warp's 32 x (ITER * VPW) amplitudes when
+      // that product is 2^sbits, so a block sum is one warp reduction.  The
+      // sampler's Philox path maps element indices back through this geometry
+      // (sample_kernels.cuh tiled_phys).
+      uint64_t q = 0;
+#pragma unroll
+      for (int k = 0; k < ITER; ++k) {
+        const W w = *reinterpret_cast<const W*>(cur + (s0 ^ swz_((uint32_t)(k * RSTEP) << C)));
+        st_stream(reinterpret_cast<W*>(st + g0 + row_off((uint32_t)(k * RSTEP))), w);
+        const V* pv = reinterpret_cast<const V*>(&w);
+#pragma unroll
+        for (int e = 0; e < VPW; ++e) q += qfix(pv[e]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+      if ((tid & 31) == 0 && en.x < p.B - 1)
+        p.tsum[(size_t)en.x * p.tsum_stride + ((size_t)tile << (L - p.tsum_sbits)) + (tid >> 5)] = q;
+    } else if (FAST) {
 #pragma unroll
       for (int k = 0; k < ITER; ++k) {
         const W w = *reinterpret_cast<const W*>(cur + (s0 ^ swz_((uint32_t)(k * RSTEP) << C)));

@@ -87,6 +87,9 @@ struct PassParams {
   long long tiles;
   const int4* ent;           // [E] launch entries {row, src slot, dst slot, 0}
   int E;
+  uint64_t* tsum;            // generated last pass: sampler block sums in tile order (or null)
+  long long tsum_stride;     // blocks per trajectory row
+  int tsum_sbits;            // log2 amplitudes per sampler block
 };
 
 // ---- shared-memory swizzle: spreads the 32 lanes of a phase access over banks

@@ -36,7 +36,41 @@ struct SampleParams {
   uint64_t* total;         // [B]
   const int64_t* off;      // [B] shot offsets
   const int64_t* m;        // [B] shots
+  // tile-order CDF (block sums written by the last generated pass): element e =
+  // (tile, row, column) of that pass's geometry; 0 = plain index order
+  int tiled;
+  uint64_t tq;             // the pass's tile qubit mask
+  int tL, tC;              // its tile bits and contiguous low bits
+  int tT;                  // its threads per CTA (thread-major element order)
 };
+
+// Fixed-point probability of the fused (tile-order) block sums: must equal
+// gen_prelude.cuh qfix bit for bit.
+__device__ __forceinline__ uint64_t qfix(float2 a) {
+  return __float2ull_rn(__fmul_rn(__fmaf_rn(a.x, a.x, __fmul_rn(a.y, a.y)), 0x1p62f));
+}
+__device__ __forceinline__ uint64_t qfix(double2 a) {
+  return __double2ull_rn(__dmul_rn(__fma_rn(a.x, a.x, __dmul_rn(a.y, a.y)), 0x1p62));
+}
+// Physical basis index of tile-order element e.  Inside a tile the order is
+// thread-major, as the last pass's store loop walks it (gen_prelude.cuh run_pass):
+// thread t holds 16-B vectors k = 0..ITER-1 at row (t >> CPR) + k * RSTEP, column
+// (t & (2^CPR - 1)) * VPW, with VPW amplitudes per vector (c64: 2, c128: 1).
+template <typename V>
+__device__ __forceinline__ uint64_t tiled_phys(const SampleParams& p, uint64_t e) {
+  constexpr int VPW = sizeof(V) == 8 ? 2 : 1;
+  const int cpr = p.tC - (VPW == 2 ? 1 : 0);                 // log2 vectors per row
+  const uint64_t nmask = p.n >= 64 ? ~0ull : ((1ull << p.n) - 1);
+  const uint64_t lowm = (1ull << p.tC) - 1;
+  const uint64_t tile = e >> p.tL, internal = e & ((1ull << p.tL) - 1);
+  const uint64_t per_thread = (1ull << p.tL) / (uint64_t)p.tT;   // ITER * VPW
+  const uint64_t t = internal / per_thread, r = internal % per_thread;
+  const uint64_t k = r / VPW, ev = r % VPW;
+  const uint64_t rstep = (uint64_t)p.tT >> cpr;
+  const uint64_t row = (t >> cpr) + k * rstep;
+  const uint64_t col = (t & ((1ull << cpr) - 1)) * VPW + ev;
+  return pdep64(tile, ~p.tq & nmask) | pdep64(row, p.tq & ~lowm) | col;
+}
 
 // ---- blocksum: one warp per sample block, coalesced 16-B loads
 template <typename R>
@@ -279,8 +313,10 @@ __global__ void __launch_bounds__(256) sample_resolve(SampleParams p, const uint
 #pragma unroll
     for (int j = 0; j < EMAX; ++j) {
       q[j] = 0;
-      if (j < per && (uint32_t)(lane * per + j) < bsz)
-        q[j] = (uint64_t)__double2ull_rn(prob64(st[e0 + j]) * mul);
+      if (j < per && (uint32_t)(lane * per + j) < bsz) {
+        const uint64_t e = (uint64_t)(e0 + j);
+        q[j] = p.tiled ? qfix(st[tiled_phys<V>(p, e)]) : (uint64_t)__double2ull_rn(prob64(st[e]) * mul);
+      }
       lsum += q[j];
     }
     const uint64_t incl = warp_incl_scan_u64(lsum);
@@ -302,7 +338,7 @@ __global__ void __launch_bounds__(256) sample_resolve(SampleParams p, const uint
           if (!found && j < per && c > tg) { found = true; jj = j; }
         }
         const long long sh = (long long)(ch & 0xFFFFFFFFFFull) + s;
-        idx_out[p.off[b] + sh] = (uint64_t)(e0 + jj);
+        idx_out[p.off[b] + sh] = p.tiled ? tiled_phys<V>(p, (uint64_t)(e0 + jj)) : (uint64_t)(e0 + jj);
       }
     }
     pending &= ~members;

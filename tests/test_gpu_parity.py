@@ -311,3 +311,38 @@ def test_circuit_specialised_kernels_are_active(cfg, dtype):
     with Engine(c.n_qubits, dtype, batch_cap=1) as eng:
         eng.load(c)
         assert eng.info()["codegen"] == 1
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_fused_block_sums_philox_chi_square(fused, monkeypatch):
+    """Config 3 (20 q, c64, generated kernels, unitary mixtures): the last pass writes the
+    sampler's block sums in its tile order (no separate state read); Philox shots drawn on that
+    CDF must still follow |psi|^2 of the logical state, exactly like the index-order path."""
+    from scipy import stats
+    if not fused:
+        monkeypatch.setenv("PTSBE_NO_FUSED_SUMS", "1")
+    c = workloads.build(3, P.parse_circuit, P.parse_noise_model, P.attach_noise)
+    specs = P.presample_probabilistic(c, 30, 100, np.random.default_rng(1))[:2]
+    m = 400_000
+    with Engine(20, "c64", batch_cap=2) as eng:
+        prog = eng.load(c)
+        assert eng.info()["codegen"] == 1
+        eng.run(selection_matrix(prog, specs))
+        seeds = np.array([mix_seed(11, t) for t in range(2)], dtype=np.uint64)
+        out = eng.sample(np.full(2, m), N.RNG_PHILOX, rng_state=seeds)
+        for b in range(2):
+            probs = np.abs(eng.get_state(b).astype(np.complex128)) ** 2
+            lo, hi = out.offsets[b], out.offsets[b + 1]
+            idx = out.indices[lo:hi].astype(np.int64)
+            assert np.all(np.diff(idx) > 0)                  # ascending, distinct (ShotBatch order)
+            obs = np.zeros(probs.size)
+            obs[idx] = out.counts[lo:hi]
+            assert obs.sum() == m
+            assert np.all(probs[obs > 0] > 0)
+            # a 20-q random state is spread over ~10^6 outcomes (Porter-Thomas): test the
+            # marginals of the high and the low 10 qubits (1024 bins each, ~400 shots per bin),
+            # which a wrong tile-order -> basis-index mapping would scramble
+            for fold in (lambda v: v.reshape(1024, -1).sum(axis=1), lambda v: v.reshape(-1, 1024).sum(axis=0)):
+                o, exp = fold(obs), fold(probs) * m
+                p = stats.chisquare(o, exp * o.sum() / exp.sum()).pvalue
+                assert p > 0.01
