@@ -315,8 +315,16 @@ def main():
     bytes_per_launch = pass_bytes / max(pass_n, 1)
     avg_launch_ms = pass_ms / max(pass_n, 1)
     achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
+    traffic, traffic_src = None, None
+    tf = REPO / "profiles" / "pass_traffic_config4.json"
+    if tf.exists():   # ncu DRAM bytes per pass launch of the same workload (committed capture)
+        t = json.loads(tf.read_text())
+        if (t.get("config"), t.get("batch_per_gpu"), t.get("dtype"), t.get("launches")) == \
+                (args.config, B, args.dtype, prog.n_passes):
+            traffic, traffic_src = t["per_launch_dram_bytes"], t["source"]
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": None, "kernel": "pass_kernel", "peak_kind": peak_kind,
+                "traffic": traffic, "traffic_unit": "bytes/launch (dram read+write, ncu)", "traffic_source": traffic_src,
+                "kernel": "pass_kernel", "peak_kind": peak_kind,
                 "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_ms,
                 "pass_share_of_step": pass_ms / max(1e-9, e0.elapsed_time(e1)),
                 "per_pass_ms": [round(float(x) / K, 3) for x in pp_ms],

@@ -11,7 +11,8 @@ def f(r, k):
         return float("nan")
     u = units[h[k]]
     return v * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1, "Tbyte": 1e12,
-                "msecond": 1e-3, "usecond": 1e-6, "nsecond": 1e-9, "second": 1}.get(u, 1)
+                "msecond": 1e-3, "usecond": 1e-6, "nsecond": 1e-9, "second": 1, "ms": 1e-3, "us": 1e-6, "ns": 1e-9,
+                "s": 1}.get(u, 1)
 stall = [k for k in h if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")]
 print(f"{'kernel':16s} {'ms':>7s} {'GB':>6s} {'GB/s':>6s} {'dram%':>5s} {'issue%':>6s} {'warps%':>6s} {'inst(M)':>8s} {'bankc%':>6s}  top stalls")
 for r in rows[2:]:
