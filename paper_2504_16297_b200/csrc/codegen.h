@@ -243,6 +243,17 @@ struct Emitter {
     o << "ptg::g1p<" << k << ">(a, " << lit(d.re, d.im) << ");\n";
   }
 
+  // a[j] *= d for one register (literal d; 1 is skipped, +-1 / +-i specialised).
+  void dmul(int j, Cx d) {
+    if (d.re == 1.0 && d.im == 0.0) return;
+    o << "      ";
+    if (d.im == 0.0 && d.re == -1.0) o << "a[" << j << "] = ptg::pmul(a[" << j << "], ptg::bc<" << V << ">((" << R << ")-1));\n";
+    else if (d.re == 0.0 && (d.im == 1.0 || d.im == -1.0))
+      o << "a[" << j << "] = ptg::pmul(ptg::ix(a[" << j << "]), ptg::bc<" << V << ">((" << R << ")" << (d.im > 0 ? "1" : "-1")
+        << "));\n";
+    else o << "a[" << j << "] = ptg::cmul(" << lit(d.re, d.im) << ", a[" << j << "]);\n";
+  }
+
   // Emit one gate.  With `scaled`, a factor f is pulled out of the matrix
   // (M = f * M', M' applied) and returned; otherwise f = 1.
   Cx op(int kind, int k0, int k1, const double* m, bool scaled) {
@@ -478,14 +489,54 @@ inline std::string generate(const GenProgram& P) {
           k << "      uint64_t hw_[" << std::max(1, woff[ph + 1] - woff[ph]) << "];\n";
           for (int w = 0; w < woff[ph + 1] - woff[ph]; ++w) k << "      hw_[" << w << "] = hits[" << woff[ph] + w << "];\n";
         }
+        // Fast variant: diagonal gates of the phase are multiplied into one pending
+        // diagonal over the register group, deferred while it commutes with the ops
+        // that follow (ops on other bits; CX whose target it does not touch; sites
+        // are the identity here) and applied once -- a layer of k diagonal gates
+        // costs one complex multiply per amplitude instead of k/2.  The slow variant
+        // keeps them in place (a hit site's Pauli does not commute with them); both
+        // variants pull out the same pivot factors.
+        std::vector<Cx> pend(N, Cx{1.0, 0.0});
+        uint32_t pmask = 0;
+        const bool merge_diag = !slow && !std::getenv("PTSBE_NO_DIAG_MERGE");
+        auto flush = [&]() {
+          if (!pmask) return;
+          for (int j = 0; j < N; ++j) ke.dmul(j, pend[j]);
+          std::fill(pend.begin(), pend.end(), Cx{1.0, 0.0});
+          pmask = 0;
+        };
         for (int q = D.op_begin; q < D.op_begin + D.n_ops; ++q) {
           const DevOp& op = gp.ops[q];
           const int k1 = op.arity == 2 ? op.k1 : 0;
+          const uint32_t bits = (1u << op.k0) | (op.arity == 2 ? (1u << op.k1) : 0u);
           if (op.kind == 0) {
+            const int kind = P.kinds[op.ref];
+            const double* m = P.mats + (size_t)op.ref * 32;
+            if (merge_diag && (kind == 2 || kind == 3 || kind == 11)) {
+              Cx e[4];
+              if (kind == 2) {          // diag(d0, d1), pivot-scaled like Emitter::op
+                const Cx d0 = Emitter::at(m, 0, 0), d1 = Emitter::at(m, 1, 1);
+                if (scaled && cxabs(d0) > 0.0) { e[0] = {1.0, 0.0}; e[1] = cxdiv(d1, d0); f = cxmul(f, d0); }
+                else { e[0] = d0; e[1] = d1; }
+              } else if (kind == 3) {   // diag(1, m11)
+                e[0] = {1.0, 0.0}; e[1] = Emitter::at(m, 1, 1);
+              } else {                  // 2-qubit diagonal, local index (bit k0) << 1 | bit k1
+                for (int t = 0; t < 4; ++t) e[t] = Emitter::at(m, t, t);
+              }
+              for (int j = 0; j < N; ++j) {
+                const int loc = op.arity == 2 ? (((j >> op.k0) & 1) << 1) | ((j >> op.k1) & 1) : ((j >> op.k0) & 1);
+                pend[j] = cxmul(pend[j], e[loc]);
+              }
+              pmask |= bits;
+              continue;
+            }
+            const bool commutes = kind == 9 ? !((pmask >> op.k1) & 1u) : !(pmask & bits);
+            if (!commutes) flush();
             k << "      ";
-            f = cxmul(f, ke.op(P.kinds[op.ref], op.k0, k1, P.mats + (size_t)op.ref * 32, scaled));
+            f = cxmul(f, ke.op(kind, op.k0, k1, m, scaled));
             continue;
           }
+          if (!slow && (P.chans[P.site_chan[op.ref]].identity_mask & 1ull) == 0 && (pmask & bits)) flush();
           const ptsbe_channel& ch = P.chans[P.site_chan[op.ref]];
           const int si = site_i++;
           if (slow) {
@@ -527,6 +578,7 @@ inline std::string generate(const GenProgram& P) {
               << " * p.B + b) * p.tiles + tile] = s_; }\n";
           }
         }
+        flush();
         return f;
       };
       auto emit_block = [&](bool slow) {
