@@ -223,7 +223,9 @@ def main():
     specs = [specs_all[i] for i in ids]
     prog = compile_circuit(c, args.dtype, tile_bits=args.tile_bits)
     eng = Engine(c.n_qubits, args.dtype, batch_cap=B, device=local)
-    eng.load_program(prog)
+    t_load = time.perf_counter()
+    eng.load_program(prog)          # plans phases, generates + NVRTC-compiles the pass kernels
+    t_load = time.perf_counter() - t_load
     sel = selection_matrix(prog, specs)
     if args.no_errors:
         sel[:] = 0
@@ -338,7 +340,7 @@ def main():
         "config": {"workload": "config4 steane_blocks(4): 28 q, %d ops, %d sites" % (len(c.ops), len(c.sites)),
                    "batch_per_gpu": B, "shots_per_trajectory": SHOTS, "passes": prog.n_passes, "g_ref": prog.g_ref,
                    "rng": args.rng, "l2": "inputs larger than L2 (2 GiB states)", "parallelism": f"traj-dp{world}",
-                   "codegen": bool(eng.info()["codegen"])},
+                   "codegen": bool(eng.info()["codegen"]), "program_load_s": round(t_load, 2)},
         "trajectories_per_s": total_traj / (ms / 1e3),
         "traj_roofline_frac": (total_traj / (ms / 1e3)) / (hbm * 1e9 * world / traj_bytes),
         "roofline": roofline,

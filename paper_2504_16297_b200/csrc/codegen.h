@@ -23,6 +23,8 @@
 #include <cstdio>
 #include <map>
 #include <mutex>
+#include <atomic>
+#include <thread>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -421,6 +423,8 @@ inline std::string err_mask_fn(const GenPass& gp) {
 // stored state equals the true state after every pass.  Passes holding
 // renormalising (general) sites are never scaled: their per-site norms must
 // be measured in the true frame.
+constexpr const char* kSplit = "\n// @@ptsbe-pass@@\n";
+
 inline std::string generate(const GenProgram& P) {
   std::ostringstream o;
   Cx G{1.0, 0.0};
@@ -653,16 +657,19 @@ inline std::string generate(const GenProgram& P) {
   }
   o << kGenPrelude << "\n"
     << "#define GZERO_RE " << hexd(G.re) << "\n#define GZERO_IM " << hexd(G.im) << "\n";
-  for (auto& kt : kernels) o << kt;
+  for (auto& kt : kernels) o << kSplit << kt;   // compile() builds one NVRTC program per pass
   return o.str();
 }
 
 // ---------------------------------------------------------------- compile + cache
 struct Module {
-  CUmodule mod = nullptr;
+  std::vector<CUmodule> mods;
   std::vector<CUfunction> fns;
 };
 
+// One NVRTC program per pass (shared header: prelude + global-phase defines),
+// compiled on parallel host threads: program load time scales with the largest
+// pass instead of the sum (config 4: 12 passes).
 inline bool compile(const std::string& src, int n_passes, int dev, Module& out, std::string& err) {
   Api& A = api();
   if (!A.ok) { err = A.why; return false; }
@@ -673,29 +680,59 @@ inline bool compile(const std::string& src, int n_passes, int dev, Module& out, 
   auto key = std::make_pair(dev, src);
   auto it = cache.find(key);
   if (it != cache.end()) { out = it->second; return true; }
-  void* prog = nullptr;
-  if (A.create(&prog, src.c_str(), "ptsbe_gen.cu", 0, nullptr, nullptr) != 0) { err = "nvrtcCreateProgram failed"; return false; }
-  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "--device-as-default-execution-space"};
-  const int rc = A.compile(prog, 4, opts);
-  if (rc != 0) {
-    size_t n = 0;
-    A.log_size(prog, &n);
-    std::string log(n, '\0');
-    if (n) A.get_log(prog, &log[0]);
-    err = "NVRTC compile failed: " + log.substr(0, 2000);
-    A.destroy(&prog);
-    return false;
+  const std::string split(kSplit);
+  std::vector<std::string> parts;
+  size_t pos = src.find(split);
+  const std::string header = src.substr(0, pos);
+  while (pos != std::string::npos) {
+    const size_t next = src.find(split, pos + split.size());
+    parts.push_back(header + src.substr(pos + split.size(), next == std::string::npos ? std::string::npos
+                                                                                       : next - pos - split.size()));
+    pos = next;
   }
-  size_t n = 0;
-  A.cubin_size(prog, &n);
-  std::vector<char> cubin(n);
-  A.get_cubin(prog, cubin.data());
-  A.destroy(&prog);
+  if ((int)parts.size() != n_passes) { err = "generated source does not hold one kernel per pass"; return false; }
+  std::vector<std::vector<char>> cubins(parts.size());
+  std::vector<std::string> errs(parts.size());
+  auto build = [&](size_t i) {
+    void* prog = nullptr;
+    if (A.create(&prog, parts[i].c_str(), "ptsbe_gen.cu", 0, nullptr, nullptr) != 0) {
+      errs[i] = "nvrtcCreateProgram failed";
+      return;
+    }
+    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "--device-as-default-execution-space"};
+    if (A.compile(prog, 4, opts) != 0) {
+      size_t n = 0;
+      A.log_size(prog, &n);
+      std::string log(n, '\0');
+      if (n) A.get_log(prog, &log[0]);
+      errs[i] = "NVRTC compile failed: " + log.substr(0, 2000);
+    } else {
+      size_t n = 0;
+      A.cubin_size(prog, &n);
+      cubins[i].resize(n);
+      A.get_cubin(prog, cubins[i].data());
+    }
+    A.destroy(&prog);
+  };
+  {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    std::vector<std::thread> pool;
+    std::atomic<size_t> next{0};
+    for (unsigned t = 0; t < std::min<unsigned>(hw, (unsigned)parts.size()); ++t)
+      pool.emplace_back([&] {
+        for (size_t i; (i = next.fetch_add(1)) < parts.size();) build(i);
+      });
+    for (auto& th : pool) th.join();
+  }
+  for (auto& e : errs)
+    if (!e.empty()) { err = e; return false; }
   Module m;
-  if (A.module_load(&m.mod, cubin.data()) != CUDA_SUCCESS) { err = "cuModuleLoadData failed"; return false; }
   for (int i = 0; i < n_passes; ++i) {
+    CUmodule mod = nullptr;
+    if (A.module_load(&mod, cubins[i].data()) != CUDA_SUCCESS) { err = "cuModuleLoadData failed"; return false; }
+    m.mods.push_back(mod);
     CUfunction f = nullptr;
-    if (A.get_function(&f, m.mod, kernel_name(i).c_str()) != CUDA_SUCCESS) { err = "cuModuleGetFunction failed"; return false; }
+    if (A.get_function(&f, mod, kernel_name(i).c_str()) != CUDA_SUCCESS) { err = "cuModuleGetFunction failed"; return false; }
     A.func_set_attr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, 227 * 1024);
     m.fns.push_back(f);
   }
