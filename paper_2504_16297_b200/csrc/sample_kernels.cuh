@@ -310,12 +310,27 @@ __global__ void __launch_bounds__(256) sample_resolve(SampleParams p, const uint
     uint64_t q[EMAX];
     uint64_t lsum = 0;
     const long long e0 = (long long)cur * bsz + (long long)lane * per;
+    // tiled: this lane's elements are one thread's vectors of the last pass (fused
+    // sums need a block == one warp's amplitudes): element j = (k, ev) sits at
+    // base | PDEP(k * RSTEP onto the row bits) | ev -- one full PDEP per lane
+    constexpr int VPW_ = sizeof(V) == 8 ? 2 : 1;
+    uint64_t tbase = 0, rowmask = 0;
+    int lr = 0;
+    if (p.tiled) {
+      tbase = tiled_phys<V>(p, (uint64_t)e0);
+      rowmask = p.tq & ~((1ull << p.tC) - 1);
+      lr = 31 - __clz(p.tT >> (p.tC - (VPW_ == 2 ? 1 : 0)));
+    }
 #pragma unroll
     for (int j = 0; j < EMAX; ++j) {
       q[j] = 0;
       if (j < per && (uint32_t)(lane * per + j) < bsz) {
-        const uint64_t e = (uint64_t)(e0 + j);
-        q[j] = p.tiled ? qfix(st[tiled_phys<V>(p, e)]) : (uint64_t)__double2ull_rn(prob64(st[e]) * mul);
+        if (p.tiled) {
+          const uint64_t a = tbase | pdep64((uint64_t)(j / VPW_) << lr, rowmask) | (uint64_t)(j % VPW_);
+          q[j] = qfix(st[a]);
+        } else {
+          q[j] = (uint64_t)__double2ull_rn(prob64(st[e0 + j]) * mul);
+        }
       }
       lsum += q[j];
     }
