@@ -190,12 +190,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=CONFIG)
-    ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--batch", type=int, default=48)
     ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
     ap.add_argument("--seed", type=int, default=2024)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--rng", default="philox", choices=["philox", "pcg64"])
     ap.add_argument("--tile-bits", type=int, default=None, help="fused-pass tile qubits (default: planner's)")
+    ap.add_argument("--low-bits", type=int, default=None, help="contiguous low qubits per tile row (default: planner's)")
+    ap.add_argument("--search-iters", type=int, default=None, help="layout-search steps of the planner")
     ap.add_argument("--no-errors", action="store_true",
                     help="analysis only: zero every sampled Kraus selection (all trajectories noiseless)")
     args = ap.parse_args()
@@ -221,7 +223,8 @@ def main():
     # deterministic deal by trajectory id: rank r owns ids [r*per_rank, (r+1)*per_rank)
     ids = list(range(rank * per_rank, (rank + 1) * per_rank))
     specs = [specs_all[i] for i in ids]
-    prog = compile_circuit(c, args.dtype, tile_bits=args.tile_bits)
+    prog = compile_circuit(c, args.dtype, tile_bits=args.tile_bits, low_bits=args.low_bits,
+                           search_iters=args.search_iters)
     eng = Engine(c.n_qubits, args.dtype, batch_cap=B, device=local)
     t_load = time.perf_counter()
     eng.load_program(prog)          # plans phases, generates + NVRTC-compiles the pass kernels

@@ -51,7 +51,7 @@ def val(r, k):
         units[h[k]], 1)
 by = [val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum") for r in rows[2:]]
 json.dump({"per_launch_dram_bytes": sum(by) / len(by), "launches": len(by), "per_pass_dram_bytes": by,
-           "config": 4, "batch_per_gpu": 32, "dtype": "c64",
+           "config": 4, "batch_per_gpu": 48, "dtype": "c64",
            "source": f"ncu --set full of the {len(by)} pass launches of one bench step (gpurun tag {tag})"},
           open("profiles/pass_traffic_config4.json", "w"), indent=1)
 for name, src in (("bench_line", f"bench_{tag}.log"), ("bench_reference_line", f"bench_ref_{tag}.log")):
