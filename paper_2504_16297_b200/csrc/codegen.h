@@ -486,6 +486,7 @@ inline std::string generate(const GenProgram& P) {
       // table (same gate code, so the frame factor is unchanged).  Each variant is
       // a complete load -> ops -> store block: no amplitude register is live across
       // the CTA-uniform branch, so the join costs no register-shuffling moves.
+      int chk_lo = 0, chk_hi = 1 << 30;   // slow variant: site indices that are tested for hits
       auto emit_ops = [&](bool slow) {
         Cx f{1.0, 0.0};
         int site_i = 0;
@@ -543,7 +544,7 @@ inline std::string generate(const GenProgram& P) {
           if (!slow && (P.chans[P.site_chan[op.ref]].identity_mask & 1ull) == 0 && (pmask & bits)) flush();
           const ptsbe_channel& ch = P.chans[P.site_chan[op.ref]];
           const int si = site_i++;
-          if (slow) {
+          if (slow && si >= chk_lo && si < chk_hi) {
             // hit: this trajectory's outcome at the site is not 0 -> apply it from the table
             // 32-bit halves + immediate mask: one predicate-setting LOP3 per site on the no-hit path
             k << "      if (__builtin_expect(((uint32_t)(hw_[" << si / 64 << "] >> " << (si % 64 >= 32 ? 32 : 0)
@@ -569,7 +570,7 @@ inline std::string generate(const GenProgram& P) {
               k << "      }";
             }
             k << "\n";
-          } else if (!(ch.identity_mask & 1ull)) {   // outcome 0 is not the identity (e.g. damping K0)
+          } else if (!(ch.identity_mask & 1ull)) {   // outcome 0 is not the identity (e.g. damping K0): no hit here
             k << "      ";
             ke.op(P.kinds[ch.mat_base], op.k0, k1, P.mats + (size_t)ch.mat_base * 32, false);
           }
@@ -627,24 +628,52 @@ inline std::string generate(const GenProgram& P) {
       } else if (no_slow) {
         k << "    }\n";
       } else {
-        // the slow variant lives out of line (a non-inlined function per phase), so
-        // the hot straight-line code stays dense in the instruction cache
-        const std::string fname = "ptsbe_slow_" + std::to_string(pi) + "_" + std::to_string(ph);
-        k << "    } else {\n      " << fname
-          << "(p.mats, p.partials, p.B, p.tiles, p.gen_zero, cur, b, sel, tile, base, scale, red, active, hits);\n    }\n";
-        const std::string before = k.str();
-        emit_block(true);
-        const std::string all = k.str();
-        slow_fns << "__device__ __noinline__ void " << fname << "(const void* mats_, double* partials_, int B_, "
-                 << "long long tiles_, int gen_zero_, " << ke.V << "* cur, int b, const uint8_t* sel, long long tile, "
-                 << "uint64_t base, double scale, double* red, bool active, const uint64_t* hits) {\n"
-                 << "  typedef " << ke.V << " V;\n"
-                 << "  struct { const void* mats; double* partials; int B; long long tiles; int gen_zero; } p = "
-                 << "{mats_, partials_, B_, tiles_, gen_zero_};\n"
-                 << "  V a[" << N << "];\n"
-                 << all.substr(before.size()) << "}\n";
-        k.str(before);
-        k.seekp(0, std::ios_base::end);
+        // The slow variants live out of line (non-inlined functions), so the hot
+        // straight-line code stays dense in the instruction cache.  A phase with up to
+        // 64 sites also gets one variant per segment of 16 consecutive sites that
+        // tests only that segment: a trajectory whose hits in the phase fall in one
+        // segment (the common case) runs a function ~4x smaller than the full variant,
+        // which matters because slow code is instruction-fetch bound.
+        const std::string base_name = "ptsbe_slow_" + std::to_string(pi) + "_" + std::to_string(ph);
+        const char* args = "(p.mats, p.partials, p.B, p.tiles, p.gen_zero, cur, b, sel, tile, base, scale, red, active, "
+                           "hits)";
+        auto emit_variant = [&](const std::string& fname, int lo, int hi) {
+          const std::string before = k.str();
+          chk_lo = lo;
+          chk_hi = hi;
+          emit_block(true);
+          chk_lo = 0;
+          chk_hi = 1 << 30;
+          const std::string all = k.str();
+          slow_fns << "__device__ __noinline__ void " << fname << "(const void* mats_, double* partials_, int B_, "
+                   << "long long tiles_, int gen_zero_, " << ke.V << "* cur, int b, const uint8_t* sel, long long tile, "
+                   << "uint64_t base, double scale, double* red, bool active, const uint64_t* hits) {\n"
+                   << "  typedef " << ke.V << " V;\n"
+                   << "  struct { const void* mats; double* partials; int B; long long tiles; int gen_zero; } p = "
+                   << "{mats_, partials_, B_, tiles_, gen_zero_};\n"
+                   << "  V a[" << N << "];\n"
+                   << all.substr(before.size()) << "}\n";
+          k.str(before);
+          k.seekp(0, std::ios_base::end);
+        };
+        int nsites = 0;
+        for (int q = D.op_begin; q < D.op_begin + D.n_ops; ++q) nsites += gp.ops[q].kind == 1;
+        constexpr int SEG = 16;
+        const int nseg = (nsites + SEG - 1) / SEG;
+        static const bool no_seg = std::getenv("PTSBE_NO_SEGMENT_VARIANTS") != nullptr;   // A/B knob
+        k << "    } else {\n";
+        if (nsites <= 64 && nseg >= 2 && !no_seg) {
+          k << "      const uint64_t hw0_ = hits[" << woff[ph] << "];\n      ";
+          for (int sgi = 0; sgi < nseg; ++sgi) {
+            const uint64_t own = (sgi * SEG + SEG >= 64 ? ~0ull : ((1ull << (sgi * SEG + SEG)) - 1)) &
+                                 ~((1ull << (sgi * SEG)) - 1);
+            k << "if (!(hw0_ & 0x" << std::hex << ~own << std::dec << "ull)) " << base_name << "_s" << sgi << args
+              << ";\n      else ";
+            emit_variant(base_name + "_s" + std::to_string(sgi), sgi * SEG, sgi * SEG + SEG);
+          }
+        }
+        k << base_name << args << ";\n    }\n";
+        emit_variant(base_name, 0, 1 << 30);
       }
       F = cxmul(F, Fph);
       k << "      __syncthreads();\n";
