@@ -630,9 +630,9 @@ inline std::string generate(const GenProgram& P) {
       } else {
         // The slow variants live out of line (non-inlined functions), so the hot
         // straight-line code stays dense in the instruction cache.  A phase with up to
-        // 64 sites also gets one variant per segment of 16 consecutive sites that
+        // 64 sites also gets one variant per segment of 8 consecutive sites (PTSBE_SEG) that
         // tests only that segment: a trajectory whose hits in the phase fall in one
-        // segment (the common case) runs a function ~4x smaller than the full variant,
+        // segment (the common case) runs a function several times smaller than the full one,
         // which matters because slow code is instruction-fetch bound.
         const std::string base_name = "ptsbe_slow_" + std::to_string(pi) + "_" + std::to_string(ph);
         const char* args = "(p.mats, p.partials, p.B, p.tiles, p.gen_zero, cur, b, sel, tile, base, scale, red, active, "
@@ -658,7 +658,7 @@ inline std::string generate(const GenProgram& P) {
         };
         int nsites = 0;
         for (int q = D.op_begin; q < D.op_begin + D.n_ops; ++q) nsites += gp.ops[q].kind == 1;
-        constexpr int SEG = 16;
+        static const int SEG = std::getenv("PTSBE_SEG") ? std::max(1, std::atoi(std::getenv("PTSBE_SEG"))) : 8;
         const int nseg = (nsites + SEG - 1) / SEG;
         static const bool no_seg = std::getenv("PTSBE_NO_SEGMENT_VARIANTS") != nullptr;   // A/B knob
         k << "    } else {\n";
