@@ -57,3 +57,20 @@ def test_errors_without_gpu_are_loud(libptsbe):
         pytest.skip("GPU present")
     with pytest.raises(ExecutionError):
         Engine(4, "c128", 1)
+
+
+def test_host_only_codegen_plans_and_generates(libptsbe):
+    """ptsbe_create_host: load_program's validation, phase planning and kernel generation run
+    without a GPU; the source holds one kernel per pass with out-of-line slow variants."""
+    import paper_2504_16297_b200 as P
+    from paper_2504_16297_b200 import workloads
+    from paper_2504_16297_b200.engine import generated_source
+    from paper_2504_16297_b200.program import compile_circuit
+    c = workloads.build(4, P.parse_circuit, P.parse_noise_model, P.attach_noise)
+    prog = compile_circuit(c, "c64")
+    src = generated_source(prog, "c64")
+    kernels = re.findall(r'extern "C" __global__ void __launch_bounds__\(\d+, \d+\) (ptsbe_pass_\d+)', src)
+    assert kernels == [f"ptsbe_pass_{i}" for i in range(prog.n_passes)]
+    assert "__noinline__ void ptsbe_slow_" in src          # slow variants out of line
+    assert "struct Swz0" in src                            # per-pass shared-memory swizzle
+    assert src.count("// @@ptsbe-pass@@") == prog.n_passes  # one NVRTC program per pass
