@@ -351,7 +351,7 @@ def main():
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:   # CPU baseline on rank 0 at N=1 only
         r = cpu_port_rate(c, specs, budget_s=15.0, workers=1)
         line["cpu_baseline"] = {"value": r["shots_s"], "unit": "shots/s", "cores": 1, "kind": "port",
                                 "sample": f"{r['ops_timed']} ops of one trajectory's op stream + one 1e4-shot "
