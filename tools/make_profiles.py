@@ -7,6 +7,7 @@ from contextlib import redirect_stdout
 from pathlib import Path
 
 tag, out = sys.argv[1], sys.argv[2]
+fill_csv = sys.argv[3] if len(sys.argv) > 3 else None
 G = Path("gpurun_out")
 # launch list
 rows = list(csv.reader(open(G / f"launches_{tag}.csv")))
@@ -50,9 +51,24 @@ def val(r, k):
     return float(r[h[k]].replace(",", "")) * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1, "Tbyte": 1e12}.get(
         units[h[k]], 1)
 by = [val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum") for r in rows[2:]]
+names = [r[h["Kernel Name"]] for r in rows[2:]]
+# ncu occasionally reports -nan DRAM counters for a long kernel under --set full: fill those
+# from a targeted --metrics capture (optional 3rd argument: its --csv log)
+if fill_csv:
+    fill = collections.defaultdict(float)
+    hh = None
+    for r in csv.reader(open(fill_csv)):
+        if r and r[0] == "ID":
+            hh = {k: i for i, k in enumerate(r)}
+            continue
+        if hh and len(r) > 10 and r[hh["Metric Name"]].startswith("dram__bytes"):
+            fill[r[hh["Kernel Name"]]] += float(r[hh["Metric Value"]].replace(",", "")) * (
+                1 if r[hh["Metric Unit"]] == "byte" else {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[r[hh["Metric Unit"]]])
+    by = [fill[nm] if (b != b and nm in fill) else b for b, nm in zip(by, names)]
 json.dump({"per_launch_dram_bytes": sum(by) / len(by), "launches": len(by), "per_pass_dram_bytes": by,
            "config": 4, "batch_per_gpu": 48, "dtype": "c64",
-           "source": f"ncu --set full of the {len(by)} pass launches of one bench step (gpurun tag {tag})"},
+           "source": f"ncu --set full of the {len(by)} pass launches of one bench step (gpurun tag {tag})"
+                     + (f"; -nan counters refilled from a targeted --metrics capture" if fill_csv else "")},
           open("profiles/pass_traffic_config4.json", "w"), indent=1)
 for name, src in (("bench_line", f"bench_{tag}.log"), ("bench_reference_line", f"bench_ref_{tag}.log")):
     for line in open(G / src):
