@@ -327,6 +327,8 @@ def main():
         if (t.get("config"), t.get("batch_per_gpu"), t.get("dtype"), t.get("launches")) == \
                 (args.config, B, args.dtype, prog.n_passes):
             traffic, traffic_src = t["per_launch_dram_bytes"], t["source"]
+            if not traffic == traffic:   # nan counters: report none
+                traffic, traffic_src = None, None
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                 "traffic": traffic, "traffic_unit": "bytes/launch (dram read+write, ncu)", "traffic_source": traffic_src,
                 "kernel": "pass_kernel", "peak_kind": peak_kind,
