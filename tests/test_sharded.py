@@ -165,3 +165,29 @@ def test_virtual_shards_match_oracle(k, dtype):
             assert stats.chisquare(obs, exp).pvalue > 1e-3   # the reference's chi^2 level (test_execute.py:168-178)
     finally:
         vs.close()
+
+
+@pytest.mark.gpu
+def test_virtual_shards_match_unsharded_engine_at_28_qubits():
+    """sharded vs unsharded device runs at full size -- config 4 (28 q, c64) split
+    into 2 shards of 27 local qubits (global<->local swaps between segments) must reproduce the
+    unsharded engine's state for the same Kraus selections."""
+    from paper_2504_16297_b200 import workloads
+    from paper_2504_16297_b200.engine import Engine
+    from paper_2504_16297_b200.program import selection_matrix
+    from paper_2504_16297_b200.sharded import VirtualShards
+    c = workloads.build(4, P.parse_circuit, P.parse_noise_model, P.attach_noise)
+    specs = P.presample_probabilistic(c, 20, 100, np.random.default_rng(4))[1:2]
+    plan = plan_sharded(c, 1, dtype="c64")
+    assert plan.n_swaps >= 1
+    vs = VirtualShards(plan, "c64", batch_cap=1)
+    try:
+        vs.run(sharded_selection(plan, specs))
+        got = vs.logical_state(0).astype(np.complex128)
+    finally:
+        vs.close()
+    with Engine(28, "c64", batch_cap=1) as eng:
+        prog = eng.load(c)
+        eng.run(selection_matrix(prog, specs))
+        ref = eng.get_state(0).astype(np.complex128)
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-5
