@@ -144,8 +144,8 @@ inline uint32_t ins0_host(uint32_t p, int bit) {
 // Shared-memory wavefronts of one warp's phase loads (stores are symmetric) under
 // swizzle z: lanes 0..31 hold consecutive register groups.  16-B accesses (c128,
 // or c64 phases holding bit 0, which load amplitude pairs) are served per quarter
-// warp by distinct 16-B chunks of a 128-B line; 8-B accesses per warp by slot load
-// (>= 2).  Minimum = conflict free.
+// warp by distinct 16-B chunks of a 128-B line; 8-B accesses per half warp by
+// distinct 8-B slots.  Minimum = conflict free.
 inline int phase_wavefronts(const Swizzle& z, const DevPhase& D, int GB) {
   int pb[5];
   for (int q = 0; q < GB; ++q) pb[q] = (int)((D.pbits >> (5 * q)) & 31);
@@ -171,10 +171,12 @@ inline int phase_wavefronts(const Swizzle& z, const DevPhase& D, int GB) {
         }
         tot += mx;
       }
-    } else {
-      int cnt[16] = {0}, mx = 0;
-      for (int l = 0; l < 32; ++l) mx = std::max(mx, ++cnt[z(lanes[l] | off) & 15u]);
-      tot += std::max(2, mx);
+    } else {   // 8-B accesses: modelled per half warp (16 lanes on 16 distinct 8-B slots)
+      for (int hw = 0; hw < 2; ++hw) {
+        int cnt[16] = {0}, mx = 0;
+        for (int l = hw * 16; l < hw * 16 + 16; ++l) mx = std::max(mx, ++cnt[z(lanes[l] | off) & 15u]);
+        tot += mx;
+      }
     }
   }
   return tot;
