@@ -205,10 +205,12 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero, int p_begin = 0, int p
   std::vector<int> fpass(B, 0);
   const bool tree = from_zero && p_begin == 0 && p_end == P && P >= 2 && h->tree_enabled && !h->host_sel.empty();
   h->tsum_ok = false;
-  // (a sampler block must be exactly one warp's amplitudes of the last pass's tile)
+  // (a 512-amplitude sampler block must be the amplitudes of a warp or a half warp of
+  // the last pass's tile)
+  const long long per_thread = P >= 1 ? (1ll << h->passes[P - 1].L) /
+                                            gen::threads_for(h->passes[P - 1].L, h->passes[P - 1].gb, false) : 0;
   const bool fuse_sums = h->gen_active && !h->any_general && from_zero && p_begin == 0 && p_end == P && P >= 1 &&
-                         (32ll << h->passes[P - 1].L) / gen::threads_for(h->passes[P - 1].L, h->passes[P - 1].gb, false) ==
-                             (1ll << h->sbits) &&
+                         h->sbits == 9 && (per_thread * 32 == 512 || per_thread * 16 == 512) &&
                          !std::getenv("PTSBE_NO_FUSED_SUMS");
   if (tree) {
     for (int b = 0; b < B; ++b) {
@@ -937,11 +939,11 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
   std::vector<DevOp> dops;
   std::vector<DevPhase> dph;
   // GB = 0: per pass, 5-bit phases iff they need fewer phases than 4-bit ones and
-  // the 4-bit plan has >= 4 phases (fewer shared-memory round trips: bench config
-  // 4 went 1.00 M -> 1.05 M shots/s); otherwise 4.  A 5-bit group doubles the
-  // registers per thread and halves the threads (128 per CTA), which loses when
-  // it saves no phase, and on memory-bound passes with 2-3 phases (their loads
-  // and stores need the wider CTA).
+  // the 4-bit plan has >= 3 phases (PTSBE_GB5_MIN_PHASES; fewer shared-memory round
+  // trips: bench config 4 went 1.00 M -> 1.05 M shots/s, and with the bank-conflict
+  // swizzle model the 3-phase light passes stopped losing); otherwise 4.  A 5-bit
+  // group doubles the registers per thread and halves the threads (128 per CTA),
+  // which loses when it saves no phase.
   auto plan_all = [&](int GB) {
     dops.clear();
     dph.clear();
@@ -958,7 +960,8 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
           std::vector<DevOp> pops5;
           std::vector<DevPhase> pphs5;
           plan_phases(per_pass[p], P.L, pops5, pphs5, 5);
-          if (pphs5.size() < pphs.size() && pphs.size() >= 4) {
+          static const size_t min4 = std::getenv("PTSBE_GB5_MIN_PHASES") ? std::atoi(std::getenv("PTSBE_GB5_MIN_PHASES")) : 3;
+          if (pphs5.size() < pphs.size() && pphs.size() >= min4) {
             pops.swap(pops5);
             pphs.swap(pphs5);
             P.gb = 5;

@@ -434,10 +434,12 @@ __device__ __forceinline__ void run_pass(const PassParams& p, Sw swz_, TileBase 
       // Last pass of a unitary program: the sampler's block sums of q = qfix(a)
       // (2^-62 fixed point) are produced here, so sampling needs no separate read
       // of the states.  CDF order inside a tile is THREAD-major (thread, k, vector
-      // element): a 2^sbits block is one warp's 32 x (ITER * VPW) amplitudes when
-      // that product is 2^sbits, so a block sum is one warp reduction.  The
-      // sampler's Philox path maps element indices back through this geometry
-      // (sample_kernels.cuh tiled_phys).
+      // element): a 512-amplitude block is the amplitudes of 32 (4-bit phases) or
+      // 16 (5-bit phases) consecutive threads, so a block sum is one (half-)warp
+      // reduction.  The sampler's Philox path maps element indices back through
+      // this geometry (sample_kernels.cuh tiled_phys).
+      constexpr int PER_THREAD = ITER * VPW;
+      constexpr int LANES = 512 / PER_THREAD;        // 32 or 16 (engine checks)
       uint64_t q = 0;
 #pragma unroll
       for (int k = 0; k < ITER; ++k) {
@@ -448,9 +450,9 @@ __device__ __forceinline__ void run_pass(const PassParams& p, Sw swz_, TileBase 
         for (int e = 0; e < VPW; ++e) q += qfix(pv[e]);
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-      if ((tid & 31) == 0 && en.x < p.B - 1)
-        p.tsum[(size_t)en.x * p.tsum_stride + ((size_t)tile << (L - p.tsum_sbits)) + (tid >> 5)] = q;
+      for (int o = LANES / 2; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+      if ((tid & (LANES - 1)) == 0 && en.x < p.B - 1)
+        p.tsum[(size_t)en.x * p.tsum_stride + ((size_t)tile << (L - 9)) + tid / LANES] = q;
     } else if (FAST) {
 #pragma unroll
       for (int k = 0; k < ITER; ++k) {

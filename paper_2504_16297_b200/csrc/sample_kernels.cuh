@@ -310,9 +310,10 @@ __global__ void __launch_bounds__(256) sample_resolve(SampleParams p, const uint
     uint64_t q[EMAX];
     uint64_t lsum = 0;
     const long long e0 = (long long)cur * bsz + (long long)lane * per;
-    // tiled: this lane's elements are one thread's vectors of the last pass (fused
-    // sums need a block == one warp's amplitudes): element j = (k, ev) sits at
-    // base | PDEP(k * RSTEP onto the row bits) | ev -- one full PDEP per lane
+    // tiled: this lane's elements are one thread's vectors of the last pass, or an
+    // aligned half of them (fused sums need a block == the amplitudes of a warp or a
+    // half warp): element j = (k0 + k, ev) sits at base | PDEP(k * RSTEP onto the row
+    // bits) | ev, k0 aligned so the bits are disjoint -- one full PDEP per lane
     constexpr int VPW_ = sizeof(V) == 8 ? 2 : 1;
     uint64_t tbase = 0, rowmask = 0;
     int lr = 0;
