@@ -7,10 +7,14 @@
 // calls with compile-time register positions and literal matrix entries
 // (hex-float, so c128 stays bit-identical to the operator table and c64 gets
 // exactly the host's float rounding); cx / swap / x compile to register
-// renaming.  Noise sites stay data-driven: per phase, one CTA-uniform bit says
-// whether the trajectory takes any non-default outcome there; if so the phase
-// runs a second straight-line copy whose sites read their outcome and apply
-// its operator from the table (rare), otherwise the fast path.
+// renaming; consecutive diagonal gates merge into one deferred register-group
+// diagonal.  Noise sites stay data-driven: per phase, hit words say which sites
+// the trajectory takes a non-default outcome at; a phase without hits runs its
+// fast straight-line code, a phase with hits calls an out-of-line slow variant
+// (per 8-site segment) whose sites test their bit and apply the outcome's
+// operator from the table.  Per pass the generator also picks the register
+// width (4 or 5 bits), the shared-memory swizzle (bank-conflict model), and, for
+// the last pass of a unitary program, fuses the sampler's block sums.
 //
 // NVRTC and the driver API are reached without link-time dependencies
 // (dlopen + cudaGetDriverEntryPoint), so libptsbe.so still loads on hosts
