@@ -448,7 +448,12 @@ inline std::string generate(const GenProgram& P) {
     const int groups = 1 << (gp.L - GB);
     const int gloop = groups / threads;   // >= 1 when threads <= groups
     const bool all_active = threads <= groups;
-    const int min_blocks = threads <= 128 ? 3 : (threads <= 256 ? 2 : 1);
+    // 3 CTAs/SM (<= 80 registers, small spills) hide more latency on the compute-heavy
+    // 256-thread passes (config 4: -3 % on its two heaviest 4-bit passes); light
+    // passes keep 2 (their spills would cost more than the extra warps give)
+    int n_gates = 0;
+    for (const DevOp& op : gp.ops) n_gates += op.kind == 0;
+    const int min_blocks = threads <= 128 ? 3 : (threads <= 256 ? (n_gates >= 40 ? 3 : 2) : 1);
     const uint64_t nmask = P.n >= 64 ? ~0ull : ((1ull << P.n) - 1);
     const uint64_t comp = ~gp.qmask & nmask;
     const uint64_t hmask = gp.qmask & ~((1ull << gp.c) - 1);
