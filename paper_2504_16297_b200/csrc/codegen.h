@@ -505,16 +505,16 @@ inline std::string generate(const GenProgram& P) {
           k << "      uint64_t hw_[" << std::max(1, woff[ph + 1] - woff[ph]) << "];\n";
           for (int w = 0; w < woff[ph + 1] - woff[ph]; ++w) k << "      hw_[" << w << "] = hits[" << woff[ph] + w << "];\n";
         }
-        // Fast variant: diagonal gates of the phase are multiplied into one pending
+        // Diagonal gates of the phase are multiplied into one pending
         // diagonal over the register group, deferred while it commutes with the ops
         // that follow (ops on other bits; CX whose target it does not touch; sites
         // are the identity here) and applied once -- a layer of k diagonal gates
-        // costs one complex multiply per amplitude instead of k/2.  The slow variant
-        // keeps them in place (a hit site's Pauli does not commute with them); both
-        // variants pull out the same pivot factors.
+        // costs one complex multiply per amplitude instead of k/2.  Slow variants
+        // flush it before every tested site on its bits (a hit's Pauli does not
+        // commute with it); all variants pull out the same pivot factors.
         std::vector<Cx> pend(N, Cx{1.0, 0.0});
         uint32_t pmask = 0;
-        const bool merge_diag = !slow && !std::getenv("PTSBE_NO_DIAG_MERGE");
+        const bool merge_diag = !std::getenv("PTSBE_NO_DIAG_MERGE");
         auto flush = [&]() {
           if (!pmask) return;
           for (int j = 0; j < N; ++j) ke.dmul(j, pend[j]);
@@ -552,9 +552,13 @@ inline std::string generate(const GenProgram& P) {
             f = cxmul(f, ke.op(kind, op.k0, k1, m, scaled));
             continue;
           }
-          if (!slow && (P.chans[P.site_chan[op.ref]].identity_mask & 1ull) == 0 && (pmask & bits)) flush();
           const ptsbe_channel& ch = P.chans[P.site_chan[op.ref]];
           const int si = site_i++;
+          // a tested site (slow variant) may apply any outcome, a non-identity default
+          // acts here, a renormalising site reads every amplitude: the pending diagonal
+          // goes first
+          const bool checked = slow && si >= chk_lo && si < chk_hi;
+          if (ch.general || ((checked || !(ch.identity_mask & 1ull)) && (pmask & bits))) flush();
           if (slow && si >= chk_lo && si < chk_hi) {
             // hit: this trajectory's outcome at the site is not 0 -> apply it from the table
             // 32-bit halves + immediate mask: one predicate-setting LOP3 per site on the no-hit path
