@@ -453,7 +453,8 @@ inline std::string generate(const GenProgram& P) {
     // passes keep 2 (their spills would cost more than the extra warps give)
     int n_gates = 0;
     for (const DevOp& op : gp.ops) n_gates += op.kind == 0;
-    const int min_blocks = threads <= 128 ? 3 : (threads <= 256 ? (n_gates >= 40 ? 3 : 2) : 1);
+    static const int mb128 = std::getenv("PTSBE_GB5_MB") ? std::atoi(std::getenv("PTSBE_GB5_MB")) : 3;
+    const int min_blocks = threads <= 128 ? mb128 : (threads <= 256 ? (n_gates >= 40 ? 3 : 2) : 1);
     const uint64_t nmask = P.n >= 64 ? ~0ull : ((1ull << P.n) - 1);
     const uint64_t comp = ~gp.qmask & nmask;
     const uint64_t hmask = gp.qmask & ~((1ull << gp.c) - 1);
