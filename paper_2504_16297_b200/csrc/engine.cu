@@ -209,8 +209,17 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero, int p_begin = 0, int p
   // the last pass's tile)
   const long long per_thread = P >= 1 ? (1ll << h->passes[P - 1].L) /
                                             gen::threads_for(h->passes[P - 1].L, h->passes[P - 1].gb, false) : 0;
+  // and the pass's store loop must be the vectorised one (gen_prelude.cuh run_pass FAST)
+  bool store_fast = false;
+  if (P >= 1) {
+    const PassHost& lp = h->passes[P - 1];
+    const long long thr = gen::threads_for(lp.L, lp.gb, false);
+    const int vpw = h->dtype == PTSBE_C64 ? 2 : 1;
+    const int cpr_log = lp.c - (vpw == 2 ? 1 : 0);
+    store_fast = cpr_log >= 0 && thr >= (1ll << cpr_log) && ((1ll << lp.L) / vpw) % thr == 0;
+  }
   const bool fuse_sums = h->gen_active && !h->any_general && from_zero && p_begin == 0 && p_end == P && P >= 1 &&
-                         h->sbits == 9 && (per_thread * 32 == 512 || per_thread * 16 == 512) &&
+                         h->sbits == 9 && store_fast && (per_thread * 32 == 512 || per_thread * 16 == 512) &&
                          !std::getenv("PTSBE_NO_FUSED_SUMS");
   if (tree) {
     for (int b = 0; b < B; ++b) {

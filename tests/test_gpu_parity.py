@@ -313,8 +313,8 @@ def test_circuit_specialised_kernels_are_active(cfg, dtype):
         assert eng.info()["codegen"] == 1
 
 
-@pytest.mark.parametrize("fused", [True, False])
-def test_fused_block_sums_philox_chi_square(fused, monkeypatch):
+@pytest.mark.parametrize("fused,dtype", [(True, "c64"), (False, "c64"), (True, "c128"), (False, "c128")])
+def test_fused_block_sums_philox_chi_square(fused, dtype, monkeypatch):
     """Config 3 (20 q, c64, generated kernels, unitary mixtures): the last pass writes the
     sampler's block sums in its tile order (no separate state read); Philox shots drawn on that
     CDF must still follow |psi|^2 of the logical state, exactly like the index-order path."""
@@ -324,7 +324,7 @@ def test_fused_block_sums_philox_chi_square(fused, monkeypatch):
     c = workloads.build(3, P.parse_circuit, P.parse_noise_model, P.attach_noise)
     specs = P.presample_probabilistic(c, 30, 100, np.random.default_rng(1))[:2]
     m = 400_000
-    with Engine(20, "c64", batch_cap=2) as eng:
+    with Engine(20, dtype, batch_cap=2) as eng:
         prog = eng.load(c)
         assert eng.info()["codegen"] == 1
         eng.run(selection_matrix(prog, specs))
@@ -342,7 +342,11 @@ def test_fused_block_sums_philox_chi_square(fused, monkeypatch):
             # a 20-q random state is spread over ~10^6 outcomes (Porter-Thomas): test the
             # marginals of the high and the low 10 qubits (1024 bins each, ~400 shots per bin),
             # which a wrong tile-order -> basis-index mapping would scramble
+            # alpha = 1e-3 per test, the reference's level for its batched-fidelity chi^2
+            # (test_execute.py:168-178): 4 params x 2 trajectories x 2 marginals = 16 tests
+            # at 0.01 would fail by chance ~15 % of the time (seen: p = 0.007, c128, seed 11,
+            # trajectory 1; other seeds and 4x the shots give p = 0.2-0.98)
             for fold in (lambda v: v.reshape(1024, -1).sum(axis=1), lambda v: v.reshape(-1, 1024).sum(axis=0)):
                 o, exp = fold(obs), fold(probs) * m
                 p = stats.chisquare(o, exp * o.sum() / exp.sum()).pvalue
-                assert p > 0.01
+                assert p > 1e-3
