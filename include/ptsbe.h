@@ -204,6 +204,18 @@ int ptsbe_profile_passes(ptsbe_engine* h, double* ms, double* bytes, int max_pas
 /* Kernel launches issued by this handle since creation (for bench gpu_launches). */
 int64_t ptsbe_launch_count(ptsbe_engine* h);
 
+/* ---- dataset writer (host-only, no GPU) <- Dataset.write's records.jsonl
+ * (execute.py:246-259, record order execute.py:181-223, bitstrings
+ * statevector.py:44-53).  Formats the sampler's CSR output -- trajectory i owns
+ * records [offsets[i], offsets[i+1]) of indices/counts and is written with id
+ * traj_ids[i] -- as the reference's lines {"t":T,"b":"<n bits, qubit n-1
+ * leftmost>","c":C}\n, each trajectory's records in ascending bitstring order,
+ * on all host cores.  Returns the text's byte length; writes it (no NUL) when
+ * buf != NULL and cap >= that length; -1 on invalid arguments (n_qubits
+ * outside 1..64, decreasing offsets, negative ids, index >= 2^n_qubits). */
+int64_t ptsbe_format_records(int n_qubits, int64_t n_traj, const int64_t* traj_ids, const int64_t* offsets,
+                             const uint64_t* indices, const uint32_t* counts, char* buf, int64_t cap);
+
 #ifdef __cplusplus
 }
 #endif

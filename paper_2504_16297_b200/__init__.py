@@ -55,7 +55,7 @@ def __getattr__(name):
     # PTS) works on machines without the CUDA build
     import importlib
     lazy = {
-        "Dataset": "execute", "ShotRecord": "execute", "execute_all": "execute", "execute_naive": "execute",
+        "Dataset": "execute", "ShotRecord": "execute", "format_records": "execute", "execute_all": "execute", "execute_naive": "execute",
         "execute_trajectory": "execute", "manifest_core": "execute", "mix_seed": "execute",
         "prepare_state": "execute", "stream_rng": "execute", "throughput_report": "execute",
         "unique_fraction": "execute", "run_specs": "execute",

@@ -87,6 +87,8 @@ SIGNATURES = {
     "ptsbe_profile_passes": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
     "ptsbe_create_host": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "ptsbe_codegen_source": (C.c_int64, [C.c_void_p, C.c_char_p, C.c_size_t]),
+    "ptsbe_format_records": (C.c_int64, [C.c_int, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_int64]),
 }
 
 _lib = None

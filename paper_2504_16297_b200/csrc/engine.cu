@@ -18,6 +18,7 @@
 #include "sample_kernels.cuh"
 #include "codegen.h"
 #include "planner.h"
+#include "records.h"
 
 using namespace ptsbe;
 
@@ -1395,5 +1396,10 @@ int ptsbe_last_error(ptsbe_engine* h, char* buf, size_t len) {
 }
 
 int64_t ptsbe_launch_count(ptsbe_engine* h) { return h ? h->launches : 0; }
+
+int64_t ptsbe_format_records(int n_qubits, int64_t n_traj, const int64_t* traj_ids, const int64_t* offsets,
+                             const uint64_t* indices, const uint32_t* counts, char* buf, int64_t cap) {
+  return ptsbe_records::format(n_qubits, n_traj, traj_ids, offsets, indices, counts, buf, cap);
+}
 
 }  // extern "C"

@@ -6,6 +6,8 @@ shots in verification mode (device PCG64 replaying the reference's stream)
 exactly equal; Philox-mode histograms pass chi-square at p > 0.01.
 """
 
+import json
+
 import numpy as np
 import pytest
 
@@ -75,6 +77,12 @@ def test_execute_all_records_identical(golden, name, tmp_path):
     ds = P.execute_all(c, specs, parallelism=3, master_seed=case["dataset"]["master_seed"])
     ds.validate()
     assert [[r.trajectory_id, r.bitstring, r.count] for r in ds.records] == case["dataset"]["records"]
+    # records.jsonl through the native writer is the reference's json.dumps text
+    assert ds.packed is not None
+    ds.write(tmp_path)
+    want = "".join(json.dumps({"t": t, "b": b, "c": k}, separators=(",", ":")) + "\n"
+                   for t, b, k in case["dataset"]["records"])
+    assert (tmp_path / "records.jsonl").read_text() == want
     got = P.manifest_core(ds.manifest)
     for row_g, row_r in zip(got["trajectories"], core["trajectories"]):
         wg, wr = row_g.pop("realized_weight"), row_r.pop("realized_weight")
@@ -126,7 +134,7 @@ def test_bench20_state_and_shots(golden):
         assert out.counts_dict(0, 20) == g["counts_m1000_seed00"]
 
 
-def test_uneven_shots_zero_shots_and_annihilation():
+def test_uneven_shots_zero_shots_and_annihilation(tmp_path):
     c = P.attach_noise(P.parse_circuit("qubits 3\ngate h 0\ngate cx 0 1\ngate x 2\n"),
                        P.parse_noise_model("rule gate=x qubit=* channel=amplitude_damping(0.5)\n"
                                            "rule gate=* qubit=* channel=depolarizing(0.2)\n"))
@@ -145,6 +153,12 @@ def test_uneven_shots_zero_shots_and_annihilation():
     assert ds2.manifest["partial"]
     assert r[0]["status"] == "ok" and r[0]["emitted"] == 50
     assert r[1]["status"] == "annihilated" and r[1]["emitted"] == 0
+    for d, sub in ((ds, "a"), (ds2, "b")):    # native writer == per-record json path
+        assert d.packed is not None
+        d.write(tmp_path / sub / "native")
+        P.Dataset(d.manifest, d.records).write(tmp_path / sub / "json")
+        assert ((tmp_path / sub / "native" / "records.jsonl").read_bytes()
+                == (tmp_path / sub / "json" / "records.jsonl").read_bytes())
     with pytest.raises(P.AnnihilatedStateError):
         P.prepare_state(c2, P.TrajectorySpec(((0, 1),), 1))
 
