@@ -41,11 +41,28 @@ inline char* put_dec(char* p, uint64_t v) {
 // {"t":  ,"b":"  ","c":  }\n  -> 5 + 6 + 6 + 2 fixed bytes
 constexpr int64_t kFixed = 19;
 
+// byte value -> its 8 binary digits, most significant first
+struct BitChars {
+  char c[256][8];
+  BitChars() {
+    for (int b = 0; b < 256; ++b)
+      for (int j = 0; j < 8; ++j) c[b][j] = char('0' + ((b >> (7 - j)) & 1));
+  }
+};
+
+inline char* put_bits(char* p, int n, uint64_t v) {
+  static const BitChars tbl;
+  int j = n - 1;
+  for (; (j + 1) & 7; --j) *p++ = char('0' + ((v >> j) & 1u));   // leading n % 8 bits
+  for (; j >= 0; j -= 8) { std::memcpy(p, tbl.c[(v >> (j - 7)) & 0xff], 8); p += 8; }
+  return p;
+}
+
 inline char* put_record(char* p, uint64_t t, int n, uint64_t v, uint64_t c) {
   std::memcpy(p, "{\"t\":", 5); p += 5;
   p = put_dec(p, t);
   std::memcpy(p, ",\"b\":\"", 6); p += 6;
-  for (int j = n - 1; j >= 0; --j) *p++ = char('0' + ((v >> j) & 1u));
+  p = put_bits(p, n, v);
   std::memcpy(p, "\",\"c\":", 6); p += 6;
   p = put_dec(p, c);
   *p++ = '}';
