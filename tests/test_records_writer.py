@@ -103,3 +103,24 @@ def test_dataset_write_native_equals_json(tmp_path):
     a = (tmp_path / "a" / "records.jsonl").read_bytes()
     assert a == (tmp_path / "b" / "records.jsonl").read_bytes()
     assert Dataset.read(tmp_path / "b").records == recs
+
+
+def test_packed_records_sequence_equals_sorted_list():
+    from paper_2504_16297_b200.execute import PackedRecords
+    rng = np.random.default_rng(11)
+    n, n_traj = 12, 25
+    ids = np.arange(100, 100 + n_traj, dtype=np.int64)
+    off, idx, cnt = _csr(rng, n, n_traj, 40, shuffle=True)
+    want = []
+    for i in range(n_traj):
+        counts = {format(int(v), f"0{n}b"): int(c) for v, c in zip(idx[off[i]:off[i + 1]], cnt[off[i]:off[i + 1]])}
+        want.extend(ShotRecord(int(ids[i]), b, counts[b]) for b in sorted(counts))
+    pr = PackedRecords(n, ids, off, idx, cnt)
+    assert len(pr) == len(want)
+    assert list(pr) == want and pr == want
+    assert pr[0] == want[0] and pr[-1] == want[-1] and pr[3:9] == want[3:9]
+    with pytest.raises(IndexError):
+        pr[len(want)]
+    assert [r for r in pr if r.trajectory_id == 105] == [r for r in want if r.trajectory_id == 105]
+    ds = Dataset({"n_qubits": n, "trajectories": []}, pr, packed=(n, ids, off, idx, cnt))
+    assert ds.pooled_counts() == Dataset({}, want).pooled_counts()
