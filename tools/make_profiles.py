@@ -27,7 +27,7 @@ for r in rows:
 tot = sum(a[1] for a in agg.values())
 with open(f"{out}_launches_config4.txt", "w") as f:
     f.write("ncu --metrics gpu__time_duration.sum --clock-control none -c 600: python bench.py --steps 2 --warmup 3 "
-            "--no-cpu\nconfig 4 (28 q, c64), batch 32, shared-trunk schedule; per-launch device time (serialised, "
+            "--no-cpu\nconfig 4 (28 q, c64), batch 48, shared-trunk schedule; per-launch device time (serialised, "
             "cold cache: compare SHARES)\n")
     for k, a in sorted(agg.items(), key=lambda x: -x[1][1]):
         f.write(f"{k:48s} launches={a[0]:4d} total_ms={a[1]:10.2f} share={100 * a[1] / tot:5.1f}% "
