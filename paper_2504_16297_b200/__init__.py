@@ -58,7 +58,8 @@ def __getattr__(name):
         "Dataset": "execute", "ShotRecord": "execute", "format_records": "execute", "execute_all": "execute", "execute_naive": "execute",
         "execute_trajectory": "execute", "manifest_core": "execute", "mix_seed": "execute",
         "prepare_state": "execute", "stream_rng": "execute", "throughput_report": "execute",
-        "unique_fraction": "execute", "run_specs": "execute",
+        "unique_fraction": "execute", "run_specs": "execute", "dataset_from_output": "execute",
+        "execute_all_distributed": "distributed",
         "ComplexState": "statevector", "ShotBatch": "statevector", "apply_gate": "statevector",
         "apply_kraus_normalized": "statevector", "apply_matrix": "statevector", "init_zero": "statevector",
         "kraus_outcome_probability": "statevector", "sample_shots": "statevector",

@@ -88,3 +88,26 @@ def run_distributed(circuit, specs, master_seed: int = 0, dtype: str = "c128", r
     if rank != 0:
         return None
     return merge([(i, o) for i, o in gathered if o is not None])
+
+
+def execute_all_distributed(circuit, specs, master_seed: int = 0, meta: dict | None = None, *,
+                            dtype: str = "c128", rng: str = "pcg64", runner=None, group=None, device=None):
+    """``execute_all`` over all ranks: the merged Dataset on rank 0, ``None`` elsewhere.
+
+    Same rows, manifest and ``records.jsonl`` bytes as a single-process
+    ``execute_all`` of the same specs (ref ``execute.py:130-178``; output
+    independent of the worker count, ``execute.py:1-5``).
+    """
+    import time
+
+    from .execute import dataset_from_output, validate_spec
+
+    specs = list(specs)
+    for spec in specs:
+        validate_spec(circuit, spec)
+    start = time.perf_counter()
+    out = run_distributed(circuit, specs, master_seed, dtype, rng, runner=runner, group=group, device=device)
+    if out is None:
+        return None
+    return dataset_from_output(circuit, specs, out if specs else None, master_seed=master_seed, meta=meta,
+                               start=start)

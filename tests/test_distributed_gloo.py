@@ -15,8 +15,8 @@ import torch.multiprocessing as mp
 
 import paper_2504_16297_b200 as P
 from paper_2504_16297_b200 import workloads
-from paper_2504_16297_b200.distributed import deal, merge, run_distributed
-from paper_2504_16297_b200.execute import BatchOutput, mix_seed
+from paper_2504_16297_b200.distributed import deal, execute_all_distributed, merge, run_distributed
+from paper_2504_16297_b200.execute import BatchOutput, dataset_from_output, mix_seed
 
 
 def oracle_runner(c, specs, master_seed, dtype, rng, ids):
@@ -44,7 +44,7 @@ def _case():
     return c, specs
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, out_dir):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -52,6 +52,12 @@ def _worker(rank, world, port, q):
     out = run_distributed(c, specs, master_seed=5, runner=oracle_runner)
     if rank == 0:
         q.put((out.weights.tolist(), out.indices.tolist(), out.counts.tolist(), out.offsets.tolist()))
+    ds = execute_all_distributed(c, specs, master_seed=5, runner=oracle_runner)
+    if rank == 0:
+        rp, _ = ds.write(out_dir)
+        q.put((rp.read_bytes(), P.manifest_core(ds.manifest)))
+    else:
+        assert ds is None
     dist.barrier()
     dist.destroy_process_group()
 
@@ -65,7 +71,7 @@ def test_deal_covers_ids_once():
             assert max(sizes) - min(sizes) <= 1
 
 
-def test_world2_gloo_matches_single_process():
+def test_world2_gloo_matches_single_process(tmp_path):
     c, specs = _case()
     single = oracle_runner(c, specs, 5, "c128", "pcg64", list(range(len(specs))))
     with socket.socket() as s:
@@ -73,15 +79,25 @@ def test_world2_gloo_matches_single_process():
         port = s.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, str(tmp_path / "w2"))) for r in range(2)]
     for p in procs:
         p.start()
     w, idx, cnt, off = q.get(timeout=240)
+    records_w2, core_w2 = q.get(timeout=240)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
     assert w == single.weights.tolist()
     assert idx == single.indices.tolist() and cnt == single.counts.tolist() and off == single.offsets.tolist()
+    # the merged dataset's records.jsonl (native writer) and manifest equal a single-process run's,
+    # and the records equal the per-record json.dumps text
+    ds1 = dataset_from_output(c, specs, single, master_seed=5)
+    rp, _ = ds1.write(tmp_path / "w1")
+    assert rp.read_bytes() == records_w2
+    assert P.manifest_core(ds1.manifest) == core_w2
+    P.Dataset(ds1.manifest, list(ds1.records)).write(tmp_path / "json")
+    assert (tmp_path / "json" / "records.jsonl").read_bytes() == records_w2
+    assert sum(r["emitted"] for r in core_w2["trajectories"]) == core_w2["total_shots"] > 0
 
 
 def test_merge_rejects_gaps():
