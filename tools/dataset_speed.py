@@ -1,6 +1,7 @@
 """execute_all + Dataset.write on the GPU box: dataset path timing (native writer vs json.dumps lines).
    python tools/dataset_speed.py [CONFIG] [TRAJECTORIES]"""
 import json, sys, tempfile, time
+sys.path.insert(0, str(__import__("pathlib").Path(__file__).resolve().parents[1]))
 from pathlib import Path
 
 import numpy as np
