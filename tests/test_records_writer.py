@@ -124,3 +124,27 @@ def test_packed_records_sequence_equals_sorted_list():
     assert [r for r in pr if r.trajectory_id == 105] == [r for r in want if r.trajectory_id == 105]
     ds = Dataset({"n_qubits": n, "trajectories": []}, pr, packed=(n, ids, off, idx, cnt))
     assert ds.pooled_counts() == Dataset({}, want).pooled_counts()
+
+
+def test_packed_validate_matches_record_path():
+    from paper_2504_16297_b200.execute import PackedRecords
+    rng = np.random.default_rng(5)
+    n, n_traj = 9, 6
+    ids = np.arange(n_traj, dtype=np.int64)
+    off, idx, cnt = _csr(rng, n, n_traj, 20, shuffle=False)
+    per = [int(cnt[off[i]:off[i + 1]].sum()) for i in range(n_traj)]
+    rows = [{"id": i, "shots": per[i], "status": "ok"} for i in range(n_traj)]
+    man = {"n_qubits": n, "trajectories": rows}
+    pk = (n, ids, off, idx, cnt)
+    Dataset(man, PackedRecords(*pk), packed=pk).validate()
+    Dataset(man, list(PackedRecords(*pk))).validate()
+    bad = {"n_qubits": n, "trajectories": [dict(r, shots=r["shots"] + (i == 2)) for i, r in enumerate(rows)]}
+    for ds in (Dataset(bad, PackedRecords(*pk), packed=pk), Dataset(bad, list(PackedRecords(*pk)))):
+        with pytest.raises(ValidationError, match="trajectory 2"):
+            ds.validate()
+    with pytest.raises(ValidationError):
+        Dataset({"n_qubits": n + 1, "trajectories": rows}, PackedRecords(*pk), packed=pk).validate()
+    short = {"n_qubits": n, "trajectories": rows[:-1]}
+    if off[-1] > off[-2]:
+        with pytest.raises(ValidationError, match="unknown trajectory"):
+            Dataset(short, PackedRecords(*pk), packed=pk).validate()
