@@ -364,3 +364,17 @@ def test_fused_block_sums_philox_chi_square(fused, dtype, monkeypatch):
                 o, exp = fold(obs), fold(probs) * m
                 p = stats.chisquare(o, exp * o.sum() / exp.sum()).pvalue
                 assert p > 1e-3
+
+
+def test_execute_all_distributed_single_rank_equals_execute_all(tmp_path):
+    """World of one (no process group): the trajectory-parallel driver's Dataset is execute_all's."""
+    from paper_2504_16297_b200.distributed import execute_all_distributed
+    c = workloads.build(1, P.parse_circuit, P.parse_noise_model, P.attach_noise)
+    specs = P.presample_probabilistic(c, 200, 300, np.random.default_rng(9))[:20]
+    a = P.execute_all(c, specs, master_seed=3)
+    b = execute_all_distributed(c, specs, master_seed=3)
+    a.write(tmp_path / "a")
+    b.write(tmp_path / "b")
+    assert (tmp_path / "a" / "records.jsonl").read_bytes() == (tmp_path / "b" / "records.jsonl").read_bytes()
+    assert P.manifest_core(a.manifest) == P.manifest_core(b.manifest)
+    b.validate()
