@@ -148,3 +148,18 @@ def test_packed_validate_matches_record_path():
     if off[-1] > off[-2]:
         with pytest.raises(ValidationError, match="unknown trajectory"):
             Dataset(short, PackedRecords(*pk), packed=pk).validate()
+
+
+def test_packed_pooled_and_per_trajectory_counts():
+    from paper_2504_16297_b200.execute import PackedRecords
+    rng = np.random.default_rng(21)
+    n, n_traj = 6, 30                      # small n: many shared bitstrings across trajectories
+    ids = np.arange(n_traj, dtype=np.int64)
+    off, idx, cnt = _csr(rng, n, n_traj, 20, shuffle=True)
+    pr = PackedRecords(n, ids, off, idx, cnt)
+    packed = Dataset({}, pr, packed=(n, ids, off, idx, cnt))
+    plain = Dataset({}, list(pr))
+    a, b = packed.pooled_counts(), plain.pooled_counts()
+    assert a == b and list(a) == list(b)   # same keys in the same order
+    for t in (0, 7, 29, 99):
+        assert packed.counts_for(t) == plain.counts_for(t)
