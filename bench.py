@@ -8,9 +8,19 @@ the hot path); every trajectory t keeps seed mix_seed(seed, t).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
+The headline is complex128 -- the reference's own arithmetic
+(``statevector.py:18-32``); the complex64 engine (north_star's fp32 mode) is
+reported beside it under ``"c64"`` in the same line.
+
 value : shots/s of the whole job with inputs resident in HBM (device pointers)
 e2e   : the same through the C-ABI with host buffers (H2D of the outcome table,
         D2H of the CSR shot records inside the timed region)
+
+``--impl reference`` times the reference itself (``trajsim`` installed under
+``baseline/_ref``; the oracle port only if that install is missing) on the
+box's host cores: the op loop of ``prepare_state`` (``execute.py:85-97``) over
+a prefix of the same trajectories' op streams, one trajectory per thread, plus
+``sample_shots`` at m = 10^4, extrapolated per op kind to the whole stream.
 """
 
 from __future__ import annotations
@@ -32,6 +42,22 @@ sys.path.insert(0, str(REPO))
 
 CONFIG = 4
 SHOTS = 10_000
+# one metric string for both arms (the driver pairs the lines on it)
+METRIC = "shots/sec (config 4: 28-qubit QEC circuit, 1e4 shots/trajectory)"
+
+
+def metric_for(config: int) -> str:
+    return METRIC if config == 4 else f"shots/sec (config {config}, 1e4 shots/trajectory)"
+DTYPE_NAME = {"c128": "c128 (complex128, f64 arithmetic)", "c64": "c64 (complex64, f32 arithmetic)"}
+DEFAULT_BATCH = {"c128": 24, "c64": 48}
+
+
+def workload_config(config: int, world: int) -> dict:
+    """The workload description, identical in both arms."""
+    return {"workload": "config4 steane_blocks(4): 28 q, 390 ops, 560 sites, probabilistic PTS"
+            if config == 4 else f"config{config}",
+            "shots_per_trajectory": SHOTS, "parallelism": f"traj-dp{world}",
+            "l2": "inputs larger than L2 (2-4 GiB states)"}
 
 
 def peaks():
@@ -96,115 +122,230 @@ def dist_env():
     return rank, world, local
 
 
-def make_workload(config: int, n_traj: int, seed: int):
-    import paper_2504_16297_b200 as P
+def make_workload(config: int, n_traj: int, seed: int, api=None):
+    """Circuit + the first n_traj accepted probabilistic-PTS specs (cli.py:100 seeding).
+
+    ``api`` is the module whose parser / PTS runs (this package, or the reference
+    itself for the reference arm); both give identical specs (bit-exact PTS)."""
+    if api is None:
+        import paper_2504_16297_b200 as api
     from paper_2504_16297_b200 import workloads
-    from paper_2504_16297_b200.execute import stream_rng
-    c = workloads.build(config, P.parse_circuit, P.parse_noise_model, P.attach_noise)
-    rng = stream_rng(seed, 2**63)            # cli.py:100 convention
+    c = workloads.build(config, api.parse_circuit, api.parse_noise_model, api.attach_noise)
     specs = []
     nsamples = max(64, 3 * n_traj)
     while len(specs) < n_traj:
-        specs = P.presample_probabilistic(c, nsamples, SHOTS, rng)
+        specs = api.presample_probabilistic(c, nsamples, SHOTS, api.stream_rng(seed, 2**63))
         nsamples *= 2
-        rng = stream_rng(seed, 2**63)
     return c, specs[:n_traj]
 
 
-def cpu_port_rate(c, specs, budget_s: float, workers: int = 1):
-    """Oracle (numpy restatement of the reference hot path) on a bounded prefix.
+# ---------------------------------------------------------------- reference CPU path
 
-    Times ``k`` ops of the op stream per trajectory (mix of gates and sites, as
-    execute.py:85-97 applies them) plus one sample_shots at the full m, and
-    extrapolates per-trajectory time = t_op * G_ref + t_sample.
-    """
-    from concurrent.futures import ThreadPoolExecutor
+def load_reference():
+    """The reference package from baseline/_ref (unmodified install), else None."""
+    ref_dir = REPO / "baseline" / "_ref"
+    if not (ref_dir / "trajsim" / "__init__.py").exists():
+        return None
+    if str(ref_dir) not in sys.path:
+        sys.path.insert(0, str(ref_dir))
+    try:
+        import trajsim
+        import trajsim.statevector as sv
+    except Exception:   # noqa: BLE001 -- a broken install falls back to the port
+        return None
+    sv.MAX_QUBITS = max(sv.MAX_QUBITS, 30)   # lifts the 24-q cap (SURVEY Appendix A fact 9)
+    return trajsim
 
+
+def reference_op_stream(ref, circuit, spec):
+    """prepare_state's op loop (execute.py:85-97) as (category, thunk(state) -> state) items."""
+    sv = ref.statevector
+    chosen = dict(spec.selections)
+    by_pos = circuit.sites_by_position()
+    out = []
+    for pos, op in enumerate(circuit.ops):
+        out.append((("gate", len(op.targets), False), lambda s, op=op: sv.apply_gate(s, op)))
+        for site in by_pos.get(pos, ()):
+            k = chosen.get(site.site_id, 0)
+            ch = circuit.channels[site.channel_id]
+            mix = ch.unitary_mixture()
+            if mix is not None:
+                out.append((("site", len(site.targets), False),
+                            lambda s, m=mix.unitaries[k], t=site.targets: sv.apply_matrix(s, m, t)))
+            else:
+                out.append((("site", len(site.targets), True),
+                            lambda s, m=ch.kraus_ops[k], t=site.targets: sv.apply_kraus_normalized(s, m, t)[0]))
+    return out
+
+
+def port_op_stream(circuit, spec):
+    """Same loop on the oracle port (only if the reference install is missing)."""
     from oracle import engine as O
-    n = c.n_qubits
-    g_ref = len(c.ops) + len(c.sites)
-
-    def one(spec):
-        psi = O.zero_state(n)
-        t0 = time.perf_counter()
-        done = 0
-        for mat, targets, general in O.op_stream(c, spec.selections):
+    n = circuit.n_qubits
+    out = []
+    for mat, targets, general in O.op_stream(circuit, spec.selections):
+        def f(psi, mat=mat, targets=targets, general=general):
             psi = O.apply_local(psi, mat, targets, n)
             if general:
-                r = float(np.sum(np.abs(psi) ** 2))
-                psi = psi / np.sqrt(r)
-            done += 1
-            if time.perf_counter() - t0 > budget_s * 0.6:
-                break
-        t_op = (time.perf_counter() - t0) / done
-        t1 = time.perf_counter()
-        psi /= np.linalg.norm(psi)
-        O.sample(psi, SHOTS, np.random.default_rng(0), n)
-        t_s = time.perf_counter() - t1
-        return t_op, t_s, done
+                psi = psi / np.sqrt(float(np.sum(np.abs(psi) ** 2)))
+            return psi
+        out.append((("op", len(targets), general), f))
+    return out
 
-    with ThreadPoolExecutor(max_workers=workers) as pool:
-        res = list(pool.map(one, specs[:workers]))
-    t_op = float(np.mean([r[0] for r in res]))
-    t_s = float(np.mean([r[1] for r in res]))
-    per_traj = t_op * g_ref + t_s
-    traj_s = workers / per_traj
-    return {"traj_s": traj_s, "shots_s": traj_s * SHOTS, "t_op_s": t_op, "t_sample_s": t_s,
-            "ops_timed": int(sum(r[2] for r in res)), "g_ref": g_ref}
+
+class CpuReference:
+    """The reference's CPU path on host threads, one trajectory per thread.
+
+    Every step each worker applies the next ``ops_per_step`` entries of its
+    trajectory's op stream (a prefix: encode h / cx gates and their noise
+    sites), timing each by kind (gate / site, arity, renormalising); the last
+    step also draws the trajectory's 10^4 shots with the reference's
+    ``sample_shots``.  Per-trajectory time = sum over the FULL stream of the
+    per-kind mean op time + the sample time; throughput = workers / that.
+    """
+
+    def __init__(self, config: int, seed: int, workers: int | None = None):
+        self.ref = load_reference()
+        api = self.ref
+        if api is None:
+            import paper_2504_16297_b200 as api
+        cores = os.cpu_count() or 1
+        try:
+            import psutil
+            avail = psutil.virtual_memory().available
+        except Exception:   # noqa: BLE001
+            avail = 64 << 30
+        self.c, specs = make_workload(config, max(cores, 1), seed, api=api)
+        n = self.c.n_qubits
+        state_b = (1 << n) * 16
+        mem_workers = max(1, int(avail * 0.7 // (5 * state_b)))   # state + result + numpy temporaries
+        self.workers = workers or max(1, min(cores, mem_workers, len(specs)))
+        self.kind = "reference" if self.ref is not None else "port"
+        self.specs = specs[: self.workers]
+        self.cores = cores
+        self.seed = seed
+        if self.ref is not None:
+            self.streams = [reference_op_stream(self.ref, self.c, s) for s in self.specs]
+        else:
+            self.streams = [port_op_stream(self.c, s) for s in self.specs]
+        self.states = None
+        self.pos = [0] * self.workers
+        self.times: dict = {}
+        self.t_sample: list = []
+        self.blas_limit = None
+        if self.workers > 1:     # one BLAS thread per worker: the workers are the parallelism
+            try:
+                from threadpoolctl import threadpool_limits
+                self.blas_limit = threadpool_limits(1)
+            except Exception:   # noqa: BLE001
+                pass
+
+    def _zero(self):
+        n = self.c.n_qubits
+        if self.ref is not None:
+            return self.ref.statevector.init_zero(n)
+        from oracle import engine as O
+        return O.zero_state(n)
+
+    def step(self, ops_per_step: int, timed: bool, sample: bool = False) -> float:
+        from concurrent.futures import ThreadPoolExecutor
+        if self.states is None:
+            self.states = [self._zero() for _ in range(self.workers)]
+
+        def work(w):
+            rec = []
+            st = self.states[w]
+            stream = self.streams[w]
+            for _ in range(ops_per_step):
+                cat, f = stream[self.pos[w] % len(stream)]
+                t0 = time.perf_counter()
+                st = f(st)
+                rec.append((cat, time.perf_counter() - t0))
+                self.pos[w] += 1
+            ts = None
+            if sample:
+                t0 = time.perf_counter()
+                if self.ref is not None:
+                    self.ref.statevector.sample_shots(st, SHOTS, self.ref.stream_rng(self.seed, w))
+                else:
+                    from oracle import engine as O
+                    O.sample(st / np.linalg.norm(st), SHOTS, np.random.default_rng(w), self.c.n_qubits)
+                ts = time.perf_counter() - t0
+            self.states[w] = st
+            return rec, ts
+
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(max_workers=self.workers) as pool:
+            res = list(pool.map(work, range(self.workers)))
+        wall = time.perf_counter() - t0
+        if timed:
+            for rec, ts in res:
+                for cat, dt in rec:
+                    self.times.setdefault(cat, []).append(dt)
+                if ts is not None:
+                    self.t_sample.append(ts)
+        return wall
+
+    def estimate(self) -> dict:
+        """Extrapolated per-trajectory time over the full op stream and the resulting rates."""
+        all_t = [t for v in self.times.values() for t in v]
+        mean_all = float(np.mean(all_t)) if all_t else float("nan")
+        per_cat = {cat: float(np.mean(v)) for cat, v in self.times.items()}
+        full = self.streams[0]
+        t_prep = 0.0
+        for cat, _f in full:
+            # an untimed kind: nearest timed kind of the same arity, else the overall mean
+            t = per_cat.get(cat)
+            if t is None:
+                same = [v for k, v in per_cat.items() if k[1] == cat[1]]
+                t = float(np.mean(same)) if same else mean_all
+            t_prep += t
+        t_s = float(np.mean(self.t_sample)) if self.t_sample else 0.0
+        per_traj = t_prep + t_s
+        traj_s = self.workers / per_traj
+        kinds = {f"{k[0]}{k[1]}q{'_renorm' if k[2] else ''}": [len(v), round(float(np.mean(v)), 4)]
+                 for k, v in self.times.items()}
+        return {"traj_s": traj_s, "shots_s": traj_s * SHOTS, "per_traj_s": per_traj, "t_sample_s": t_s,
+                "ops_timed": len(all_t), "g_ref": len(full), "kinds": kinds}
+
+    def sample_text(self, est: dict) -> str:
+        src = ("trajsim (baseline/_ref, unmodified; MAX_QUBITS raised to 30)" if self.ref is not None
+               else "oracle port (reference install missing)")
+        return (f"{src}: {est['ops_timed']} timed ops of the prepare_state op loop (prefix of each "
+                f"trajectory's stream: 1q/2q gates and noise sites, complex128) + sample_shots(m=1e4) on "
+                f"{self.workers} threads (one trajectory each, {self.cores} host cores), extrapolated per op "
+                f"kind to the full stream of G_ref={est['g_ref']} ops; per-kind [count, mean s]: {est['kinds']}")
 
 
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    c, specs = make_workload(args.config, 8, args.seed)
-    import psutil
-    cores = os.cpu_count() or 1
-    mem = psutil.virtual_memory().available
-    state_b = (1 << c.n_qubits) * 16
-    workers = max(1, min(cores, int(mem * 0.3 // (4 * state_b)), 4))
-    vals = []
-    for _ in range(args.warmup and 0):
-        pass
-    for step in range(max(1, args.steps)):
-        r = cpu_port_rate(c, specs, budget_s=max(4.0, 20.0 / max(1, args.steps)), workers=workers)
-        vals.append(r["shots_s"])
-    v = float(np.median(vals))
-    line = {"impl": "reference", "metric": "shots/sec (config 4, 28 q, 1e4 shots/trajectory)", "value": v,
-            "unit": "shots/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64)",
-            "data": "synthetic",
-            "config": {"workload": "config4 steane_blocks(4): 28 q, 390 ops, 560 sites, 1e4 shots/traj"},
-            "trajectories_per_s": r["traj_s"],
-            "cpu_baseline": {"value": v, "unit": "shots/s", "cores": workers, "kind": "port",
-                             "sample": f"{r['ops_timed']} ops of the op stream + one 1e4-shot sample per "
-                                       f"trajectory on {workers} threads, extrapolated to G_ref={r['g_ref']} ops"},
+    cpu = CpuReference(args.config, args.seed)
+    ops = max(1, args.ops_per_step)
+    for _ in range(args.warmup):             # real warm-up: the same work, untimed
+        cpu.step(ops, timed=False)
+    walls = []
+    for i in range(max(1, args.steps)):
+        walls.append(cpu.step(ops, timed=True, sample=(i == max(1, args.steps) - 1)))
+    est = cpu.estimate()
+    v = est["shots_s"]
+    line = {"impl": "reference", "metric": metric_for(args.config), "value": v, "unit": "shots/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(walls)),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": DTYPE_NAME["c128"],
+            "data": "synthetic (PTS-sampled Kraus selections of a generated circuit)",
+            "config": workload_config(args.config, world),
+            "trajectories_per_s": est["traj_s"],
+            "cpu_baseline": {"value": v, "unit": "shots/s", "cores": cpu.workers, "kind": cpu.kind,
+                             "sample": cpu.sample_text(est)},
             "e2e": {"value": v, "unit": "shots/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=CONFIG)
-    ap.add_argument("--batch", type=int, default=48)
-    ap.add_argument("--dtype", default="c64", choices=["c64", "c128"])
-    ap.add_argument("--seed", type=int, default=2024)
-    ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--rng", default="philox", choices=["philox", "pcg64"])
-    ap.add_argument("--tile-bits", type=int, default=None, help="fused-pass tile qubits (default: planner's)")
-    ap.add_argument("--low-bits", type=int, default=None, help="contiguous low qubits per tile row (default: planner's)")
-    ap.add_argument("--search-iters", type=int, default=None, help="layout-search steps of the planner")
-    ap.add_argument("--no-errors", action="store_true",
-                    help="analysis only: zero every sampled Kraus selection (all trajectories noiseless)")
-    args = ap.parse_args()
-    if args.impl == "reference":
-        run_reference(args)
-        return
+# ---------------------------------------------------------------- device path
 
+def run_engine_leg(args, dtype: str, batch: int, c, specs_for, dev, world, rank, local, with_e2e=True):
+    """Time K steps of one engine (dtype) on this rank; returns the measurements."""
     import torch
     import torch.distributed as dist
 
@@ -213,19 +354,12 @@ def main():
     from paper_2504_16297_b200.execute import mix_seed
     from paper_2504_16297_b200.program import compile_circuit, selection_matrix
 
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    B, W, K = args.batch, args.warmup, args.steps
+    B, W, K = batch, args.warmup, args.steps
     per_rank = (W + K) * B
-    c, specs_all = make_workload(args.config, per_rank * world, args.seed)
-    # deterministic deal by trajectory id: rank r owns ids [r*per_rank, (r+1)*per_rank)
-    ids = list(range(rank * per_rank, (rank + 1) * per_rank))
-    specs = [specs_all[i] for i in ids]
-    prog = compile_circuit(c, args.dtype, tile_bits=args.tile_bits, low_bits=args.low_bits,
+    ids, specs = specs_for(per_rank)
+    prog = compile_circuit(c, dtype, tile_bits=args.tile_bits, low_bits=args.low_bits,
                            search_iters=args.search_iters)
-    eng = Engine(c.n_qubits, args.dtype, batch_cap=B, device=local)
+    eng = Engine(c.n_qubits, dtype, batch_cap=B, device=local)
     t_load = time.perf_counter()
     eng.load_program(prog)          # plans phases, generates + NVRTC-compiles the pass kernels
     t_load = time.perf_counter() - t_load
@@ -239,7 +373,6 @@ def main():
     else:
         rng_mode = N.RNG_PCG64
         rng_words = np.stack([pcg64_state_words(mix_seed(args.seed, t)) for t in ids])
-    dev = torch.device("cuda", local)
     # value path: inputs resident in HBM
     d_sel = torch.from_numpy(sel).to(dev)
     d_shots = torch.from_numpy(shots).to(dev)
@@ -287,78 +420,155 @@ def main():
     pass_ms, pass_n, pass_bytes = eng.profile_read()
     pp_ms, pp_bytes = eng.profile_passes()
     eng.profile(False)
-    ms = max_over_ranks(e0.elapsed_time(e1))
+    step_ms = e0.elapsed_time(e1)
+    ms = max_over_ranks(step_ms)
     total_traj = K * B * world
-    value = total_traj * SHOTS / (ms / 1e3)
+    out = {"prog": prog, "eng_info": eng.info(), "t_load": t_load, "ms": ms, "value": total_traj * SHOTS / (ms / 1e3),
+           "traj_s": total_traj / (ms / 1e3), "launches": launches, "clocks": clk.summary(),
+           "pass_ms": pass_ms, "pass_n": pass_n, "pass_bytes": pass_bytes, "pp_ms": pp_ms, "pp_bytes": pp_bytes,
+           "step_ms_local": step_ms, "total_traj": total_traj}
 
-    # e2e: host buffers through the C ABI, copies inside the timed region
-    sel_host = np.ascontiguousarray(sel)
-    barrier()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    h2d = d2h = 0
-    for i in range(W, W + K):
-        lo = i * B
-        w, st = eng.run(sel_host[lo:lo + B])
-        out = eng.sample(shots[lo:lo + B], rng_mode, rng_state=rng_words[lo:lo + B].reshape(-1))
-        h2d += sel_host[lo:lo + B].nbytes + shots[lo:lo + B].nbytes + rng_words[lo:lo + B].nbytes
-        d2h += w.nbytes + st.nbytes + out.indices.nbytes + out.counts.nbytes + 8 * B
-    t1.record(stream)
-    barrier()
-    ms_e2e = max_over_ranks(t0.elapsed_time(t1))
-    e2e = total_traj * SHOTS / (ms_e2e / 1e3)
+    if with_e2e:
+        # e2e: host buffers through the C ABI, copies inside the timed region
+        sel_host = np.ascontiguousarray(sel)
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        h2d = d2h = 0
+        for i in range(W, W + K):
+            lo = i * B
+            w, st = eng.run(sel_host[lo:lo + B])
+            o = eng.sample(shots[lo:lo + B], rng_mode, rng_state=rng_words[lo:lo + B].reshape(-1))
+            h2d += sel_host[lo:lo + B].nbytes + shots[lo:lo + B].nbytes + rng_words[lo:lo + B].nbytes
+            d2h += w.nbytes + st.nbytes + o.indices.nbytes + o.counts.nbytes + 8 * B
+        t1.record(stream)
+        barrier()
+        ms_e2e = max_over_ranks(t0.elapsed_time(t1))
+        out["e2e"] = {"value": total_traj * SHOTS / (ms_e2e / 1e3), "unit": "shots/s",
+                      "h2d_bytes_per_step": h2d // K, "d2h_bytes_per_step": d2h // K}
+    eng.close()
+    del d_sel, d_shots, d_rng, d_w, d_s, d_idx, d_cnt, d_nu
+    torch.cuda.empty_cache()
+    return out
+
+
+def roofline_of(leg, dtype: str, batch: int, config: int, K: int):
+    hbm, peak_kind = peaks()
+    # algorithmic bytes: one read + one write of every state each pass launch processes
+    # (2 * E * 2^n * s; E = trajectories + shared trunk in the launch), summed by the engine
+    bytes_per_launch = leg["pass_bytes"] / max(leg["pass_n"], 1)
+    avg_launch_ms = leg["pass_ms"] / max(leg["pass_n"], 1)
+    achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
+    traffic, traffic_src = None, None
+    tf = REPO / "profiles" / f"pass_traffic_config{config}_{dtype}.json"
+    if tf.exists():   # ncu DRAM bytes per pass launch of the same workload (committed capture)
+        t = json.loads(tf.read_text())
+        if (t.get("config"), t.get("batch_per_gpu"), t.get("dtype"), t.get("launches")) == \
+                (config, batch, dtype, leg["prog"].n_passes):
+            traffic, traffic_src = t["per_launch_dram_bytes"], t["source"]
+            if not traffic == traffic:   # nan counters: report none
+                traffic, traffic_src = None, None
+    return {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+            "traffic": traffic, "traffic_unit": "bytes/launch (dram read+write, ncu)", "traffic_source": traffic_src,
+            "kernel": "ptsbe_pass_<p> (circuit-specialised fused pass kernels, NVRTC sm_100a)",
+            "peak_kind": peak_kind, "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_ms,
+            "pass_share_of_step": leg["pass_ms"] / max(1e-9, leg["step_ms_local"]),
+            "per_pass_ms": [round(float(x) / K, 3) for x in leg["pp_ms"]],
+            "per_pass_gbs": [round(float(b) / max(float(m), 1e-9) / 1e6, 1)
+                             for m, b in zip(leg["pp_ms"], leg["pp_bytes"])]}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=CONFIG)
+    ap.add_argument("--batch", type=int, default=None, help="trajectories per step (default per dtype)")
+    ap.add_argument("--dtype", default="c128", choices=["c64", "c128"], help="headline arithmetic")
+    ap.add_argument("--secondary", default="c64", choices=["c64", "c128", "none"],
+                    help="second engine reported in the same line")
+    ap.add_argument("--seed", type=int, default=2024)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ops-per-step", type=int, default=1, help="reference arm: ops per worker per step")
+    ap.add_argument("--rng", default="philox", choices=["philox", "pcg64"])
+    ap.add_argument("--tile-bits", type=int, default=None, help="fused-pass tile qubits (default: planner's)")
+    ap.add_argument("--low-bits", type=int, default=None, help="contiguous low qubits per tile row (default: planner's)")
+    ap.add_argument("--search-iters", type=int, default=None, help="layout-search steps of the planner")
+    ap.add_argument("--no-errors", action="store_true",
+                    help="analysis only: zero every sampled Kraus selection (all trajectories noiseless)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    W, K = args.warmup, args.steps
+    legs = [args.dtype] + ([args.secondary] if args.secondary not in ("none", args.dtype) else [])
+    batches = {d: (args.batch if (args.batch and d == args.dtype) else DEFAULT_BATCH[d]) for d in legs}
+    need = max(batches.values()) * (W + K) * world
+    c, specs_all = make_workload(args.config, need, args.seed)
+
+    def specs_for(per_rank):
+        # deterministic deal by trajectory id: rank r owns ids [r*per_rank, (r+1)*per_rank)
+        ids = list(range(rank * per_rank, (rank + 1) * per_rank))
+        return ids, [specs_all[i] for i in ids]
+
+    res = {}
+    for d in legs:
+        res[d] = run_engine_leg(args, d, batches[d], c, specs_for, dev, world, rank, local)
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
-    hbm, peak_kind = peaks()
+    hbm, _ = peaks()
+    head = res[args.dtype]
+    B = batches[args.dtype]
     amp = 8 if args.dtype == "c64" else 16
-    # algorithmic bytes: one read + one write of every state each pass launch processes
-    # (2 * E * 2^n * s; E = trajectories + shared trunk in the launch), summed by the engine
-    bytes_per_launch = pass_bytes / max(pass_n, 1)
-    avg_launch_ms = pass_ms / max(pass_n, 1)
-    achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
-    traffic, traffic_src = None, None
-    tf = REPO / "profiles" / "pass_traffic_config4.json"
-    if tf.exists():   # ncu DRAM bytes per pass launch of the same workload (committed capture)
-        t = json.loads(tf.read_text())
-        if (t.get("config"), t.get("batch_per_gpu"), t.get("dtype"), t.get("launches")) == \
-                (args.config, B, args.dtype, prog.n_passes):
-            traffic, traffic_src = t["per_launch_dram_bytes"], t["source"]
-            if not traffic == traffic:   # nan counters: report none
-                traffic, traffic_src = None, None
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": traffic, "traffic_unit": "bytes/launch (dram read+write, ncu)", "traffic_source": traffic_src,
-                "kernel": "pass_kernel", "peak_kind": peak_kind,
-                "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_ms,
-                "pass_share_of_step": pass_ms / max(1e-9, e0.elapsed_time(e1)),
-                "per_pass_ms": [round(float(x) / K, 3) for x in pp_ms],
-                "per_pass_gbs": [round(float(b) / max(float(m), 1e-9) / 1e6, 1) for m, b in zip(pp_ms, pp_bytes)]}
+    prog = head["prog"]
     traj_bytes = prog.n_passes * 2 * (1 << c.n_qubits) * amp + (1 << c.n_qubits) * amp + 16 * SHOTS
     line = {
-        "metric": "shots/sec (config 4: 28 q QEC, 1e4 shots/trajectory)", "value": value, "unit": "shots/s",
-        "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "c64 (f32 complex)" if args.dtype == "c64" else "c128 (f64 complex)",
+        "metric": metric_for(args.config), "value": head["value"], "unit": "shots/s",
+        "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": head["ms"] / K, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": DTYPE_NAME[args.dtype],
         "data": "synthetic (PTS-sampled Kraus selections of a generated circuit)",
-        "config": {"workload": "config4 steane_blocks(4): 28 q, %d ops, %d sites" % (len(c.ops), len(c.sites)),
-                   "batch_per_gpu": B, "shots_per_trajectory": SHOTS, "passes": prog.n_passes, "g_ref": prog.g_ref,
-                   "rng": args.rng, "l2": "inputs larger than L2 (2 GiB states)", "parallelism": f"traj-dp{world}",
-                   "codegen": bool(eng.info()["codegen"]), "program_load_s": round(t_load, 2)},
-        "trajectories_per_s": total_traj / (ms / 1e3),
-        "traj_roofline_frac": (total_traj / (ms / 1e3)) / (hbm * 1e9 * world / traj_bytes),
-        "roofline": roofline,
-        "e2e": {"value": e2e, "unit": "shots/s", "h2d_bytes_per_step": h2d // K, "d2h_bytes_per_step": d2h // K},
-        "gpu_launches": launches,
-        "clocks": clk.summary(),
+        "config": workload_config(args.config, world),
+        "engine": {"batch_per_gpu": B, "passes": prog.n_passes, "g_ref": prog.g_ref, "rng": args.rng,
+                   "codegen": bool(head["eng_info"]["codegen"]), "program_load_s": round(head["t_load"], 2),
+                   "trajectories_timed": head["total_traj"]},
+        "trajectories_per_s": head["traj_s"],
+        "traj_roofline_frac": head["traj_s"] / (hbm * 1e9 * world / traj_bytes),
+        "roofline": roofline_of(head, args.dtype, B, args.config, K),
+        "e2e": head["e2e"],
+        "gpu_launches": head["launches"],
+        "clocks": head["clocks"],
     }
-    if not args.no_cpu and world == 1:   # CPU baseline on rank 0 at N=1 only
-        r = cpu_port_rate(c, specs, budget_s=15.0, workers=1)
-        line["cpu_baseline"] = {"value": r["shots_s"], "unit": "shots/s", "cores": 1, "kind": "port",
-                                "sample": f"{r['ops_timed']} ops of one trajectory's op stream + one 1e4-shot "
-                                          f"sample (complex128 numpy, as the reference), extrapolated to "
-                                          f"G_ref={r['g_ref']} ops"}
+    for d in legs[1:]:
+        r = res[d]
+        rf = roofline_of(r, d, batches[d], args.config, K)
+        line[d] = {"value": r["value"], "unit": "shots/s", "ms_per_step": r["ms"] / K,
+                   "trajectories_per_s": r["traj_s"], "e2e": r["e2e"], "batch_per_gpu": batches[d],
+                   "passes": r["prog"].n_passes, "gpu_launches": r["launches"], "clocks": r["clocks"],
+                   "roofline": {k: rf[k] for k in ("achieved", "peak", "frac", "traffic", "avg_launch_ms",
+                                                   "per_pass_ms", "per_pass_gbs", "pass_share_of_step")}}
+    if not args.no_cpu and world == 1:   # CPU baseline on rank 0 at N=1 only (bounded sample)
+        cpu = CpuReference(args.config, args.seed)
+        cpu.step(1, timed=False)
+        for i in range(2):
+            cpu.step(2, timed=True, sample=(i == 1))
+        est = cpu.estimate()
+        line["cpu_baseline"] = {"value": est["shots_s"], "unit": "shots/s", "cores": cpu.workers,
+                                "kind": cpu.kind, "sample": cpu.sample_text(est)}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -60,6 +60,8 @@ typedef enum { PTSBE_C64 = 0, PTSBE_C128 = 1 } ptsbe_dtype;
 #define PTSBE_DEVICE_PTRS 0x1u  /* pointer arguments are device pointers */
 #define PTSBE_ZERO_VECTOR 0x4u  /* ptsbe_run_range from pass 0: start from the all-zero vector
                                    instead of |0...0> (every shard but shard 0) */
+#define PTSBE_CONTINUE    0x8u  /* ptsbe_run_range from pass 0: apply the passes to the states as
+                                   they are (set_state / a previous range) instead of |0...0> */
 #define PTSBE_NO_SYNC     0x2u  /* do not synchronise the stream before returning
                                    (only meaningful with PTSBE_DEVICE_PTRS) */
 
@@ -189,6 +191,9 @@ int ptsbe_device_memory(int device, uint64_t* free_bytes, uint64_t* total_bytes)
 int ptsbe_synchronize(ptsbe_engine* h);
 void* ptsbe_stream(ptsbe_engine* h);            /* cudaStream_t of the handle */
 int ptsbe_info(ptsbe_engine* h, int64_t* out, int n);  /* {n, dtype, cap, n_passes, tile_bits, ...} */
+/* Pass p of the loaded program: {tile bits L, contiguous low bits c, register bits per
+ * phase, phases, ops, renormalising slots, threads per CTA, generated (1) / generic (0)}. */
+int ptsbe_pass_info(ptsbe_engine* h, int p, int64_t* out, int n);
 int ptsbe_last_error(ptsbe_engine* h, char* buf, size_t len);
 /* Per-launch timing of the fused-pass kernel: when enabled, every pass launch
  * is bracketed by CUDA events on the handle's stream; profile_read syncs and

@@ -30,6 +30,7 @@ PTSBE_C128 = 1
 PTSBE_DEVICE_PTRS = 0x1
 PTSBE_NO_SYNC = 0x2
 PTSBE_ZERO_VECTOR = 0x4
+PTSBE_CONTINUE = 0x8
 
 RNG_PCG64 = 0
 RNG_PHILOX = 1
@@ -79,6 +80,7 @@ SIGNATURES = {
     "ptsbe_synchronize": (C.c_int, [C.c_void_p]),
     "ptsbe_stream": (C.c_void_p, [C.c_void_p]),
     "ptsbe_info": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int]),
+    "ptsbe_pass_info": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int]),
     "ptsbe_last_error": (C.c_int, [C.c_void_p, C.c_char_p, C.c_size_t]),
     "ptsbe_launch_count": (C.c_int64, [C.c_void_p]),
     "ptsbe_profile": (C.c_int, [C.c_void_p, C.c_int]),

@@ -1135,7 +1135,8 @@ int ptsbe_apply_program(ptsbe_engine* h, const uint8_t* sel, int B, double* out_
 
 int ptsbe_run_range(ptsbe_engine* h, const uint8_t* sel, int B, int pass_begin, int pass_end, double* out_weight,
                     int32_t* out_status, uint32_t flags) {
-  return run_common(h, sel, B, out_weight, out_status, flags, pass_begin == 0, pass_begin, pass_end);
+  return run_common(h, sel, B, out_weight, out_status, flags, pass_begin == 0 && !(flags & PTSBE_CONTINUE),
+                    pass_begin, pass_end);
 }
 
 int ptsbe_exchange_half(ptsbe_engine* h, int b, int bit, int value, void* buf, int unpack) {
@@ -1392,6 +1393,16 @@ int ptsbe_last_error(ptsbe_engine* h, char* buf, size_t len) {
   if (!buf || len == 0) return PTSBE_ERR_VALIDATION;
   const std::string& s = h ? h->err : std::string("null handle");
   std::snprintf(buf, len, "%s", s.c_str());
+  return 0;
+}
+
+int ptsbe_pass_info(ptsbe_engine* h, int p, int64_t* out, int n) {
+  if (!h || !out) return PTSBE_ERR_VALIDATION;
+  if (p < 0 || p >= (int)h->passes.size()) return fail(h, PTSBE_ERR_VALIDATION, "pass %d out of range", p);
+  const PassHost& P = h->passes[p];
+  const int64_t thr = h->gen_active ? gen::threads_for(P.L, P.gb, P.n_slots > 0) : std::max(32, 1 << std::max(0, P.L - 4));
+  const int64_t vals[] = {P.L, P.c, P.gb, P.n_phases, P.n_ops, P.n_slots, thr, h->gen_active ? 1 : 0};
+  for (int i = 0; i < n && i < (int)(sizeof vals / sizeof vals[0]); ++i) out[i] = vals[i];
   return 0;
 }
 

@@ -84,7 +84,7 @@ def run_distributed(circuit, specs, master_seed: int = 0, dtype: str = "c128", r
     if world == 1:
         return merge([(ids, local)])
     gathered = [None] * world if rank == 0 else None
-    dist.gather_object((ids, local), gathered, dst=0, group=group)
+    dist.gather_object((ids, local), gathered, dst=dist.get_global_rank(group, 0) if group else 0, group=group)
     if rank != 0:
         return None
     return merge([(i, o) for i, o in gathered if o is not None])

@@ -230,6 +230,12 @@ class Engine:
         self.lib.ptsbe_profile_passes(self.h, _ptr(ms), _ptr(by), n)
         return ms[:n], by[:n]
 
+    def pass_info(self, p: int) -> dict:
+        out = np.zeros(8, dtype=np.int64)
+        self._check(self.lib.ptsbe_pass_info(self.h, int(p), _ptr(out), out.size), "ptsbe_pass_info")
+        keys = ("L", "c", "gb", "n_phases", "n_ops", "n_slots", "threads", "codegen")
+        return dict(zip(keys, (int(v) for v in out)))
+
     def info(self) -> dict:
         out = np.zeros(11, dtype=np.int64)
         self._check(self.lib.ptsbe_info(self.h, _ptr(out), out.size), "ptsbe_info")
@@ -255,12 +261,14 @@ def pcg64_state_words(seed_or_rng) -> np.ndarray:
 def _engine_sharding_methods():
     """Sharding primitives on Engine (ptsbe_run_range / exchange_half / norm_totals)."""
 
-    def run_range(self, sel, pass_begin: int, pass_end: int, zero_vector: bool = False):
+    def run_range(self, sel, pass_begin: int, pass_end: int, zero_vector: bool = False, continue_: bool = False):
+        """Passes [pass_begin, pass_end); from pass 0 the states start at |0...0> (or the zero
+        vector) unless ``continue_``, which applies the range to the states as they are."""
         sel = np.ascontiguousarray(sel, dtype=np.uint8)
         B = sel.shape[0]
         w = np.empty(B, dtype=np.float64)
         s = np.empty(B, dtype=np.int32)
-        flags = N.PTSBE_ZERO_VECTOR if zero_vector else 0
+        flags = (N.PTSBE_ZERO_VECTOR if zero_vector else 0) | (N.PTSBE_CONTINUE if continue_ else 0)
         self._check(self.lib.ptsbe_run_range(self.h, _ptr(sel), B, int(pass_begin), int(pass_end), _ptr(w),
                                              _ptr(s), flags), "ptsbe_run_range")
         return w, s

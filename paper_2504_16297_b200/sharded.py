@@ -242,10 +242,14 @@ class DistributedShards:
                     send = self.backend.half_buffer()
                     recv = self.backend.half_buffer()
                     self.backend.exchange_half(b, l, v, send, unpack=False)
+                    self.backend.before_send()
                     reqs = dist.batch_isend_irecv([dist.P2POp(dist.isend, send, partner, self.group),
                                                    dist.P2POp(dist.irecv, recv, partner, self.group)])
                     for r in reqs:
                         r.wait()
+                    # NCCL's wait() only orders torch's current stream; the unpack runs on the
+                    # engine's own stream, so it must not start before the receive landed
+                    self.backend.after_recv()
                     self.backend.exchange_half(b, l, v, recv, unpack=True)
 
     def sample(self, shots, seeds):
@@ -254,16 +258,18 @@ class DistributedShards:
         import torch.distributed as dist
         shots = np.asarray(shots, dtype=np.int64)
         B = shots.size
-        mine = torch.tensor(self.backend.norm_totals(B).astype(np.int64))
+        # collectives on the backend's device (an NCCL-only group cannot reduce CPU tensors)
+        mine = torch.tensor(self.backend.norm_totals(B).astype(np.int64), device=self.backend.comm_device())
         allt = [torch.zeros_like(mine) for _ in range(self.world)]
         dist.all_gather(allt, mine, group=self.group)
-        totals = np.stack([t.numpy().astype(np.uint64) for t in allt], axis=1)
+        totals = np.stack([t.cpu().numpy().astype(np.uint64) for t in allt], axis=1)
         split = np.stack([_split_shots(totals[b], int(shots[b]), int(seeds[b])) for b in range(B)])
         keys = np.array([mix_seed(int(seeds[b]), self.rank) for b in range(B)], dtype=np.uint64)
         local = self.backend.sample(split[:, self.rank], keys)      # list of (local idx, counts)
         mapped = [(physical_to_logical(np.full(ix.size, self.rank), ix, self.plan), ct) for ix, ct in local]
         gathered = [None] * self.world if self.rank == 0 else None
-        dist.gather_object(mapped, gathered, dst=0, group=self.group)
+        dist.gather_object(mapped, gathered, dst=dist.get_global_rank(self.group, 0) if self.group else 0,
+                           group=self.group)
         if self.rank != 0:
             return None
         result = []
@@ -296,6 +302,18 @@ class EngineShardBackend:
 
     def run_range(self, sel, p0, p1, zero_vector=False):
         self.engine.run_range(sel, p0, p1, zero_vector=zero_vector)
+
+    def comm_device(self):
+        import torch
+        return torch.device("cuda", self.engine.device)
+
+    def before_send(self):
+        # the pack ran on the engine's stream; torch's stream (NCCL's) must see it
+        self.engine.synchronize()
+
+    def after_recv(self):
+        import torch
+        torch.cuda.current_stream(self.comm_device()).synchronize()
 
     def exchange_half(self, b, bit, value, buf, unpack):
         self.engine.exchange_half(b, bit, value, buf.data_ptr(), unpack)

@@ -139,8 +139,8 @@ def kraus_outcome_probability(state: ComplexState, kraus: np.ndarray, targets) -
     """||K psi||^2 without changing the state (ref ``statevector.py:129-133``)."""
     kraus = np.asarray(kraus)
     _check_targets(state.n_qubits, targets, kraus.shape[0])
-    _eng, w, st = _run_single(state, kraus, targets, general=True)
-    return w if st == N.TRAJ_OK else w  # annihilated outcomes still report their norm^2
+    _eng, w, _st = _run_single(state, kraus, targets, general=True)
+    return w   # reported for annihilating outcomes too (the reference returns the raw norm^2)
 
 
 def apply_kraus_normalized(state: ComplexState, kraus: np.ndarray, targets):

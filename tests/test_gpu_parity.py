@@ -238,8 +238,10 @@ def test_config3_20q_against_oracle():
         with Engine(20, dtype, batch_cap=2) as eng:
             prog = eng.load(c)
             w, st = eng.run(selection_matrix(prog, specs))
-            for b, s in enumerate(specs[:1]):
+            assert len(specs) == 2
+            for b, s in enumerate(specs):
                 ref, rw = O.prepare(c, s.selections)
+                assert st[b] == 0 and w[b] == pytest.approx(rw, rel=TOL[dtype], abs=0)
                 assert rel(eng.get_state(b).astype(np.complex128), ref) <= TOL[dtype]
 
 

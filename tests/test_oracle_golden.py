@@ -52,3 +52,26 @@ def test_oracle_dataset_records(golden, name):
     for t, row in enumerate(rows):
         recs += [[t, b, row["counts"][b]] for b in sorted(row["counts"])]
     assert recs == case["dataset"]["records"]
+
+
+def test_coset_oracle_equals_full_state_oracle():
+    """oracle.apply_on_cosets (the 28-q pass-parity checker) equals apply_local on the full
+    state, restricted to the sampled cosets, for 1q/2q ops inside a scattered qubit set."""
+    rng = np.random.default_rng(0)
+    n = 10
+    psi = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    qubits = [0, 1, 4, 7, 9]
+    items = []
+    for _ in range(12):
+        k = int(rng.integers(1, 3))
+        t = [int(x) for x in rng.choice(qubits, size=k, replace=False)]
+        m = rng.normal(size=(1 << k, 1 << k)) + 1j * rng.normal(size=(1 << k, 1 << k))
+        items.append((m, t))
+    full = psi.copy()
+    for m, t in items:
+        full = O.apply_local(full, m, t, n)
+    rest = [q for q in range(n) if q not in qubits]
+    pats = np.array([0, 3, 17, 31])
+    idx = O.scatter_bits(pats, rest)[:, None] | O.scatter_bits(np.arange(1 << len(qubits)), qubits)[None, :]
+    got = O.apply_on_cosets(psi[idx], items, qubits)
+    assert np.allclose(got, full[idx], rtol=1e-13, atol=1e-13)

@@ -33,6 +33,15 @@ class NumpyShard:
     def half_buffer(self):
         return torch.empty(1 << (self.nl - 1), dtype=torch.complex128)
 
+    def comm_device(self):
+        return torch.device("cpu")
+
+    def before_send(self):
+        pass
+
+    def after_recv(self):
+        pass
+
     def run_range(self, sel, p0, p1, zero_vector=False):
         prog = self.plan.program
         for b in range(sel.shape[0]):
