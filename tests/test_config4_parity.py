@@ -105,6 +105,15 @@ def check_pass(prev, cur, items, qubits, idx, tol, phase_free=True):
     return err
 
 
+def coset_norms(state, qubits):
+    """Norm^2 of every coset of the qubit set (float64)."""
+    n = state.size.bit_length() - 1
+    t = (np.abs(state.astype(np.complex128)) ** 2).reshape((2,) * n)
+    axes_q = [n - 1 - q for q in qubits]
+    rest = [a for a in range(n) if a not in axes_q]
+    return np.transpose(t, rest + axes_q).reshape(1 << len(rest), -1).sum(axis=1)
+
+
 def random_state(n, dtype, seed=0):
     rng = np.random.default_rng(seed)
     psi = rng.standard_normal(1 << n) + 1j * rng.standard_normal(1 << n)
@@ -138,9 +147,14 @@ def test_every_bench_pass_against_oracle_random_input(config4, dtype):
             idx = coset_rows(c.n_qubits, qs, COSETS[dtype], rng)
             for b in range(3):
                 check_pass(prev[b], cur[b], oracle_items(c, prog, p, selections[b]), qs, idx, TOL[dtype])
-                # unitary pass: the whole state's norm is kept
-                n2 = float(np.vdot(cur[b], cur[b]).real)
+                # unitary pass: the whole state's norm is kept (accumulated in float64)
+                n2 = float(np.sum(np.abs(cur[b].astype(np.complex128)) ** 2))
                 assert abs(n2 - 1.0) <= (1e-5 if dtype == "c64" else 1e-12)
+            if dtype == "c64":
+                # every coset of Q keeps its norm (the pass is unitary inside each coset): a
+                # full-state check of the tile addressing, not only the sampled cosets
+                a0, a1 = coset_norms(prev[2], qs), coset_norms(cur[2], qs)
+                assert np.max(np.abs(a1 - a0)) <= 1e-5 * max(float(a0.max()), 1e-30)
             prev = cur
 
 
