@@ -197,8 +197,9 @@ class CpuReference:
     """The reference's CPU path on host threads, one trajectory per thread.
 
     Every step each worker applies the next ``ops_per_step`` entries of its
-    trajectory's op stream (a prefix: encode h / cx gates and their noise
-    sites), timing each by kind (gate / site, arity, renormalising); the last
+    trajectory's op stream (workers start at evenly spaced points of the
+    stream, so 1q/2q gates and noise sites are all sampled), timing each by
+    kind (gate / site, arity, renormalising); the last
     step also draws the trajectory's 10^4 shots with the reference's
     ``sample_shots``.  Per-trajectory time = sum over the FULL stream of the
     per-kind mean op time + the sample time; throughput = workers / that.
@@ -229,7 +230,10 @@ class CpuReference:
         else:
             self.streams = [port_op_stream(self.c, s) for s in self.specs]
         self.states = None
-        self.pos = [0] * self.workers
+        # workers start at evenly spaced points of the op stream, so the timed sample mixes
+        # the kinds of the whole stream (1q/2q gates, noise sites), not only the first ops
+        L = len(self.streams[0])
+        self.pos = [(w * L) // self.workers for w in range(self.workers)]
         self.times: dict = {}
         self.t_sample: list = []
         self.blas_limit = None
@@ -311,8 +315,9 @@ class CpuReference:
     def sample_text(self, est: dict) -> str:
         src = ("trajsim (baseline/_ref, unmodified; MAX_QUBITS raised to 30)" if self.ref is not None
                else "oracle port (reference install missing)")
-        return (f"{src}: {est['ops_timed']} timed ops of the prepare_state op loop (prefix of each "
-                f"trajectory's stream: 1q/2q gates and noise sites, complex128) + sample_shots(m=1e4) on "
+        return (f"{src}: {est['ops_timed']} timed ops of the prepare_state op loop (each worker a run of "
+                f"its trajectory's stream from an evenly spaced start: 1q/2q gates and noise sites, "
+                f"complex128) + sample_shots(m=1e4) on "
                 f"{self.workers} threads (one trajectory each, {self.cores} host cores), extrapolated per op "
                 f"kind to the full stream of G_ref={est['g_ref']} ops; per-kind [count, mean s]: {est['kinds']}")
 

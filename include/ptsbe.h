@@ -64,6 +64,8 @@ typedef enum { PTSBE_C64 = 0, PTSBE_C128 = 1 } ptsbe_dtype;
                                    they are (set_state / a previous range) instead of |0...0> */
 #define PTSBE_NO_SYNC     0x2u  /* do not synchronise the stream before returning
                                    (only meaningful with PTSBE_DEVICE_PTRS) */
+#define PTSBE_KEEP_SEL    0x10u /* continued ptsbe_run_range: keep the device outcome table as it
+                                   is (sel may be NULL) -- e.g. outcomes chosen on device */
 
 /* rng modes of ptsbe_sample */
 #define PTSBE_RNG_PCG64   0  /* numpy PCG64 stream per trajectory: rng_state[4*b..] =
@@ -148,8 +150,9 @@ int ptsbe_apply_program(ptsbe_engine* h, const uint8_t* sel, int B,
 int ptsbe_set_layout(ptsbe_engine* h, const int32_t* perm);
 
 /* Fusion planner (host only; no GPU or handle needed).  Op i acts on the
- * LOGICAL qubits in target_masks[i]; general[i] != 0 marks renormalising
- * sites (never reordered among themselves).  perm_io: in = starting layout,
+ * LOGICAL qubits in target_masks[i]; general[i] bit 0 marks renormalising
+ * sites (never reordered among themselves), bit 1 gates, bit 2 decision sites
+ * (ptsbe_run_conventional: the site must open its pass).  perm_io: in = starting layout,
  * out = layout after `search_iters` steps of local search minimising the pass
  * count.  Writes out_pass[i] (pass of op i, ops keep stream order within a
  * pass) and out_masks[p] (PHYSICAL tile qubit set of pass p).  Returns the
@@ -167,6 +170,22 @@ int ptsbe_plan(int n_qubits, int n_ops, const uint64_t* target_masks, const uint
  * range stopped (a global<->local qubit swap may have happened in between). */
 int ptsbe_run_range(ptsbe_engine* h, const uint8_t* sel, int B, int pass_begin, int pass_end,
                     double* out_weight, int32_t* out_status, uint32_t flags);
+/* ---- conventional trajectories (Algorithm 1) <- trajectory.py:40-70 run_trajectory,
+ * :138-219 the dense ensemble of sample_conventional.  Outcomes of unitary-mixture
+ * sites are state independent (select_index over the mixture's probabilities on
+ * the trajectory's uniform) and arrive in `sel`; the outcome of every GENERAL-channel
+ * site is chosen on device from the state just before it: the reduced density
+ * matrix rho of its targets gives every branch probability p_k = ||K_k psi||^2 =
+ * tr(K_k^+ K_k rho) / tr(rho) (statevector.py:129-133) in one read, then
+ * k = select_index(u[b*S + site], p) (trajectory.py:27-37) is written to the outcome
+ * table, and the next fused pass applies K_k with renormalisation and weight
+ * (statevector.py:136-145).  The program must be planned with every general site
+ * opening its pass (ptsbe_plan bit 2), else PTSBE_ERR_VALIDATION.
+ * u: B x S uniforms (only general sites' columns are read).  out_sel (optional):
+ * the final B x S outcome table.  out_probs (optional): for the i-th decision site
+ * in program order, p_k at out_probs[(i*B + b)*64 + k]. */
+int ptsbe_run_conventional(ptsbe_engine* h, const uint8_t* sel, const double* u, int B, uint8_t* out_sel,
+                           double* out_weight, int32_t* out_status, double* out_probs, uint32_t flags);
 /* Copy the half of state b whose local bit `bit` equals `value` to (unpack = 0)
  * or from (unpack = 1) the contiguous device buffer `buf` (2^(n-1) amplitudes):
  * the data movement of a global<->local qubit swap. */

@@ -9,7 +9,8 @@ shot sampling -- in hand-written sm_100a kernels (``csrc/``, built into
 
 Same export list as ``pkg/src/trajsim/__init__.py:15-86`` minus the CPU
 density-matrix oracle and the conventional Algorithm-1 simulator, which are
-out of scope for the device engine.
+out of scope.  The conventional Algorithm-1
+simulator (``trajectory``) runs on the device engine too.
 """
 
 from .circuit import (
@@ -46,7 +47,7 @@ from .presample import (
     site_outcome_probs,
     unique_kraus,
 )
-from .trajectory import select_index
+from .trajectory import DENSE_ENSEMBLE_LIMIT, RealizedTrajectory, select_index
 from .version import __version__
 
 
@@ -63,7 +64,8 @@ def __getattr__(name):
         "ComplexState": "statevector", "ShotBatch": "statevector", "apply_gate": "statevector",
         "apply_kraus_normalized": "statevector", "apply_matrix": "statevector", "init_zero": "statevector",
         "kraus_outcome_probability": "statevector", "sample_shots": "statevector",
-        "Engine": "engine", "compile_circuit": "program",
+        "Engine": "engine", "compile_circuit": "program", "write_throughput_csv": "execute",
+        "run_trajectory": "trajectory", "sample_conventional": "trajectory",
     }
     if name in lazy:
         mod = importlib.import_module(f".{lazy[name]}", __name__)

@@ -31,6 +31,7 @@ PTSBE_DEVICE_PTRS = 0x1
 PTSBE_NO_SYNC = 0x2
 PTSBE_ZERO_VECTOR = 0x4
 PTSBE_CONTINUE = 0x8
+PTSBE_KEEP_SEL = 0x10
 
 RNG_PCG64 = 0
 RNG_PHILOX = 1
@@ -72,6 +73,8 @@ SIGNATURES = {
     "ptsbe_set_layout": (C.c_int, [C.c_void_p, C.c_void_p]),
     "ptsbe_run_range": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
                                   C.c_uint32]),
+    "ptsbe_run_conventional": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_void_p, C.c_uint32]),
     "ptsbe_exchange_half": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int]),
     "ptsbe_norm_totals": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "ptsbe_state_ptr": (C.c_void_p, [C.c_void_p, C.c_int]),

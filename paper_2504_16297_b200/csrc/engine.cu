@@ -19,6 +19,8 @@
 #include "codegen.h"
 #include "planner.h"
 #include "records.h"
+#include "conventional.cuh"
+#include "exact_cdf.cuh"
 
 using namespace ptsbe;
 
@@ -118,6 +120,18 @@ struct ptsbe_engine {
   uint64_t tsum_qmask = 0;
   int tsum_L = 0, tsum_c = 0, tsum_threads = 0;
   std::string gen_src;
+  // conventional (Algorithm 1) selection: per pass, the general-channel site that
+  // opens it (outcome chosen on device from the state at the pass boundary)
+  struct Decision { int site = -1, p0 = -1, p1 = -1, arity = 0, mat_base = 0, n_out = 0; };
+  std::vector<Decision> decide;
+  bool conv_ready = false;        // every general site opens its pass
+  double* d_mats64 = nullptr;     // operator table in fp64 (branch probabilities)
+  double* d_u = nullptr;          // per (trajectory, site) uniforms
+  size_t u_cap = 0;
+  double* d_rdm = nullptr;        // reduced-density-matrix partials
+  size_t rdm_cap = 0;
+  BlockMap* d_maps = nullptr;     // exact-CDF block maps (verification-mode sampling)
+  size_t maps_cap = 0;
   std::string err;
 };
 
@@ -420,8 +434,10 @@ int run_common(ptsbe_engine* h, const uint8_t* sel, int B, double* out_weight, i
     return fail(h, PTSBE_ERR_VALIDATION, "a continued pass range must keep the batch of %d states", h->last_B);
   if (B == 0) return 0;
   CK(h, cudaSetDevice(h->dev));
-  h->host_sel.clear();
-  if (h->n_sites > 0) {
+  if (flags & PTSBE_KEEP_SEL) {   // continued range over the device table as it is
+    if (from_zero) return fail(h, PTSBE_ERR_VALIDATION, "PTSBE_KEEP_SEL needs a continued pass range");
+  } else if (h->n_sites > 0) {
+    h->host_sel.clear();
     if (!sel) return fail(h, PTSBE_ERR_VALIDATION, "selection table is required");
     if (int r = copy_in(h, h->d_sel, sel, (size_t)B * h->n_sites, flags)) return r;
     // the shared-trunk schedule needs each trajectory's first non-default site on the host
@@ -518,9 +534,18 @@ int sample_impl(ptsbe_engine* h, int B, const int64_t* shots, int rng_mode, cons
   sp.tC = h->tsum_c;
   sp.tT = h->tsum_threads;
 
-  // Exact RNG modes replay the reference's CDF, which runs in LOGICAL index
-  // order: canonicalise permuted states first.  Philox mode samples the physical
-  // layout and maps indices back (cheaper); once any state is logical, all are.
+  // Exact RNG modes (PCG64 / host keys) replay the reference's sampler bit for bit
+  // (exact_cdf.cuh): on the normalised amplitudes get_state returns, in LOGICAL
+  // index order -- rescale deferred norms and canonicalise permuted states first.
+  const bool exact = rng_mode != PTSBE_RNG_PHILOX;
+  if (exact && total > 0)
+    if (int r = rescale_if_needed<R>(h)) return r;
+  if (exact && total > 0 && (size_t)B * h->nblk > h->maps_cap) {
+    if (dalloc(h, &h->d_maps, (size_t)B * h->nblk)) return PTSBE_ERR_CUDA;
+    h->maps_cap = (size_t)B * h->nblk;
+  }
+  // Philox mode samples the physical layout and maps indices back (cheaper); once
+  // any state is logical, all are.
   bool unperm = false;
   if (h->permuted && total > 0) {
     bool any_logical = false;
@@ -547,6 +572,13 @@ int sample_impl(ptsbe_engine* h, int B, const int64_t* shots, int rng_mode, cons
     }
     sample_blockscan<<<B, 1024, 0, h->stream>>>(sp);
     CKL(h);
+    if (exact) {   // numpy's sequential float64 cumsum, block ends into d_bs, cum_last into d_total
+      dim3 g1((unsigned)((h->nblk + 7) / 8), (unsigned)B);
+      exact_blockmaps<R><<<g1, 256, 0, h->stream>>>(sp, h->d_maps);
+      CKL(h);
+      exact_chain<R><<<B, 32, 0, h->stream>>>(sp, h->d_maps, h->d_bs);
+      CKL(h);
+    }
     const unsigned gw = (unsigned)((n_chunks * 32 + 255) / 256);
     if (rng_mode == PTSBE_RNG_PCG64) {
       if (int r = copy_in(h, h->d_rng, rng_state, (size_t)B * 4 * 8, flags)) return r;
@@ -566,7 +598,10 @@ int sample_impl(ptsbe_engine* h, int B, const int64_t* shots, int rng_mode, cons
       seg_radix_sort<<<B, 1024, 0, h->stream>>>(h->d_keys, h->d_tmp, h->d_off, h->d_m, h->d_status, 53);
       CKL(h);
     }
-    sample_resolve<R><<<gw, 256, 0, h->stream>>>(sp, h->d_chunks, n_chunks, h->d_keys, h->d_idx);
+    if (exact)
+      exact_resolve<R><<<gw, 256, 0, h->stream>>>(sp, h->d_chunks, n_chunks, h->d_keys, h->d_bs, h->d_idx);
+    else
+      sample_resolve<R><<<gw, 256, 0, h->stream>>>(sp, h->d_chunks, n_chunks, h->d_keys, h->d_idx);
     CKL(h);
     if (unperm || tiled) {   // physical -> logical bitstrings, then ascending order again
       if (h->permuted) {
@@ -708,7 +743,7 @@ int ptsbe_destroy(ptsbe_engine* h) {
                   h->d_phases, h->d_matkind,
                   h->d_chans, h->d_site_chan, h->d_slot_site, h->d_partials, h->d_bs, h->d_total, h->d_off,
                   h->d_m, h->d_nuniq, h->d_uoff, h->d_rng, h->d_keys, h->d_tmp, h->d_idx, h->d_runidx,
-                  h->d_runcnt, h->d_chunks, h->d_ent, h->d_forks};
+                  h->d_runcnt, h->d_chunks, h->d_ent, h->d_forks, h->d_mats64, h->d_u, h->d_rdm, h->d_maps};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
@@ -893,6 +928,8 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
   // validate ops, translate targets to tile bits, bucket by pass
   std::vector<std::vector<HostOp>> per_pass(n_passes);
   std::vector<int> site_pass_tmp(n_sites, n_passes);   // pass that fires each site
+  std::vector<ptsbe_engine::Decision> decide(n_passes);
+  bool conv_ready = true;
   int prev_pass = -1;
   for (int i = 0; i < n_ops; ++i) {
     const ptsbe_op& o = ops[i];
@@ -928,6 +965,19 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
       const ptsbe_channel& ch = chans[site_chan[o.ref]];
       if (ch.arity != o.arity) return fail(h, PTSBE_ERR_VALIDATION, "op %d: channel arity mismatch", i);
       ho.general = ch.general != 0;
+      if (ho.general) {
+        if (per_pass[o.pass].empty()) {
+          ptsbe_engine::Decision& d = decide[o.pass];
+          d.site = o.ref;
+          d.p0 = o.t0;
+          d.p1 = o.arity == 2 ? o.t1 : -1;
+          d.arity = o.arity;
+          d.mat_base = ch.mat_base;
+          d.n_out = ch.n_outcomes;
+        } else {
+          conv_ready = false;
+        }
+      }
     } else {
       return fail(h, PTSBE_ERR_VALIDATION, "op %d: unknown kind %d", i, o.kind);
     }
@@ -1064,6 +1114,14 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
     CK(h, cudaFuncSetAttribute(pass_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
   else
     CK(h, cudaFuncSetAttribute(pass_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
+  {
+    std::vector<double> m64((size_t)std::max(n_mats, 1) * 32, 0.0);
+    if (n_mats) std::memcpy(m64.data(), mats, (size_t)n_mats * 32 * 8);
+    if (dalloc(h, &h->d_mats64, m64.size())) return PTSBE_ERR_CUDA;
+    CK(h, cudaMemcpy(h->d_mats64, m64.data(), m64.size() * 8, cudaMemcpyHostToDevice));
+  }
+  h->decide = decide;
+  h->conv_ready = conv_ready;
   h->passes = ph;
   h->site_pass = site_pass_tmp;
   h->n_sites = n_sites;
@@ -1137,6 +1195,99 @@ int ptsbe_run_range(ptsbe_engine* h, const uint8_t* sel, int B, int pass_begin, 
                     int32_t* out_status, uint32_t flags) {
   return run_common(h, sel, B, out_weight, out_status, flags, pass_begin == 0 && !(flags & PTSBE_CONTINUE),
                     pass_begin, pass_end);
+}
+
+// Conventional trajectories: outcomes of general-channel sites chosen on device.
+int ptsbe_run_conventional(ptsbe_engine* h, const uint8_t* sel, const double* u, int B, uint8_t* out_sel,
+                           double* out_weight, int32_t* out_status, double* out_probs, uint32_t flags) {
+  if (!h) return PTSBE_ERR_VALIDATION;
+  if (!h->loaded) return fail(h, PTSBE_ERR_VALIDATION, "no program loaded");
+  if (B < 0 || B > h->cap) return fail(h, PTSBE_ERR_VALIDATION, "batch %d exceeds capacity %d", B, h->cap);
+  if (!h->conv_ready)
+    return fail(h, PTSBE_ERR_VALIDATION,
+                "program not planned for state-dependent selection (a general site does not open its pass)");
+  if (B == 0) return 0;
+  const int P = (int)h->passes.size();
+  const int S = h->n_sites;
+  std::vector<int> cuts;   // passes opened by a decision site
+  for (int p = 0; p < P; ++p)
+    if (h->decide[p].site >= 0) cuts.push_back(p);
+  if (!cuts.empty() && !u) return fail(h, PTSBE_ERR_VALIDATION, "uniform table is required");
+  CK(h, cudaSetDevice(h->dev));
+  if (!cuts.empty()) {
+    const size_t nu = (size_t)B * S;
+    if (nu > h->u_cap) {
+      if (dalloc(h, &h->d_u, nu)) return PTSBE_ERR_CUDA;
+      h->u_cap = nu;
+    }
+    if (int r = copy_in(h, h->d_u, u, nu * 8, flags)) return r;
+  }
+  // the selection table is rewritten on device: the first range must not use the trunk schedule
+  const bool tree_save = h->tree_enabled;
+  h->tree_enabled = cuts.empty() && tree_save;
+  const uint32_t f0 = flags | PTSBE_NO_SYNC;
+  const uint64_t per = 1ull << h->n;
+  const int nblk = (int)std::max<uint64_t>(1, std::min<uint64_t>((per / 2 + 255) / 256,
+                                                                  (uint64_t)std::max(1, 4 * h->num_sms / B)));
+  if ((size_t)B * nblk * kRdmVals > h->rdm_cap) {
+    if (dalloc(h, &h->d_rdm, (size_t)B * nblk * kRdmVals)) { h->tree_enabled = tree_save; return PTSBE_ERR_CUDA; }
+    h->rdm_cap = (size_t)B * nblk * kRdmVals;
+  }
+  double* d_probs = nullptr;
+  if (out_probs && !cuts.empty()) CK(h, cudaMallocAsync((void**)&d_probs, (size_t)B * 64 * 8 * cuts.size(), h->stream));
+  int r = 0;
+  int cur = 0;
+  bool started = false;
+  auto decide_at = [&](int p, int idx) -> int {
+    const ptsbe_engine::Decision& d = h->decide[p];
+    dim3 g((unsigned)nblk, (unsigned)B);
+    if (h->dtype == PTSBE_C64) {
+      if (d.arity == 1) site_rdm_partials<float, 1><<<g, 256, 0, h->stream>>>(h->states, h->n, d.p0, -1, h->d_status, h->d_rdm, nblk);
+      else site_rdm_partials<float, 2><<<g, 256, 0, h->stream>>>(h->states, h->n, d.p0, d.p1, h->d_status, h->d_rdm, nblk);
+    } else {
+      if (d.arity == 1) site_rdm_partials<double, 1><<<g, 256, 0, h->stream>>>(h->states, h->n, d.p0, -1, h->d_status, h->d_rdm, nblk);
+      else site_rdm_partials<double, 2><<<g, 256, 0, h->stream>>>(h->states, h->n, d.p0, d.p1, h->d_status, h->d_rdm, nblk);
+    }
+    CKL(h);
+    site_select<<<B, 128, 0, h->stream>>>(h->d_rdm, nblk, d.arity, h->d_mats64, d.mat_base, d.n_out, h->d_u, S,
+                                           d.site, h->d_sel, h->d_status,
+                                           d_probs ? d_probs + (size_t)idx * B * 64 : nullptr);
+    CKL(h);
+    return 0;
+  };
+  for (size_t i = 0; i < cuts.size() && !r; ++i) {
+    const int p = cuts[i];
+    if (p == 0) {   // the circuit opens with a decision: start from |0...0> explicitly
+      if ((r = run_common(h, sel, B, nullptr, nullptr, f0, true, 0, 0))) break;
+      if (h->dtype == PTSBE_C64) init_zero_kernel<float><<<1184, 256, 0, h->stream>>>(h->states, h->n, B, 0);
+      else init_zero_kernel<double><<<1184, 256, 0, h->stream>>>(h->states, h->n, B, 0);
+      CKL(h);
+      h->final_general = false;
+    } else if (!started) {
+      if ((r = run_common(h, sel, B, nullptr, nullptr, f0, true, 0, p))) break;
+    } else {
+      if ((r = run_common(h, nullptr, B, nullptr, nullptr, f0 | PTSBE_KEEP_SEL, false, cur, p))) break;
+    }
+    started = true;
+    cur = p;
+    r = decide_at(p, (int)i);
+  }
+  if (!r) {
+    if (!started) r = run_common(h, sel, B, nullptr, nullptr, f0, true, 0, P);
+    else if (cur < P) r = run_common(h, nullptr, B, nullptr, nullptr, f0 | PTSBE_KEEP_SEL, false, cur, P);
+  }
+  h->tree_enabled = tree_save;
+  if (r) { if (d_probs) cudaFreeAsync(d_probs, h->stream); return r; }
+  if (out_weight) if (int e = copy_out(h, out_weight, h->d_weight, (size_t)B * 8, flags)) return e;
+  if (out_status) if (int e = copy_out(h, out_status, h->d_status, (size_t)B * 4, flags)) return e;
+  if (out_sel && S) if (int e = copy_out(h, out_sel, h->d_sel, (size_t)B * S, flags)) return e;
+  if (d_probs) {
+    int e = copy_out(h, out_probs, d_probs, (size_t)B * 64 * 8 * cuts.size(), flags);
+    cudaFreeAsync(d_probs, h->stream);
+    if (e) return e;
+  }
+  if (!(flags & PTSBE_NO_SYNC) || !(flags & PTSBE_DEVICE_PTRS)) CK(h, cudaStreamSynchronize(h->stream));
+  return 0;
 }
 
 int ptsbe_exchange_half(ptsbe_engine* h, int b, int bit, int value, void* buf, int unpack) {
@@ -1288,9 +1439,11 @@ int ptsbe_plan(int n_qubits, int n_ops, const uint64_t* target_masks, const uint
     return -PTSBE_ERR_VALIDATION;
   std::vector<plan::Op> ops(n_ops);
   // general[i]: bit 0 = renormalising site, bit 1 = gate (counts toward the
-  // optional per-pass gate budget PTSBE_MAX_PASS_GATES, a tuning knob)
+  // optional per-pass gate budget PTSBE_MAX_PASS_GATES, a tuning knob), bit 2 =
+  // decision site (first op of its pass; ptsbe_run_conventional)
   for (int i = 0; i < n_ops; ++i)
-    ops[i] = plan::Op{target_masks[i], general && (general[i] & 1) != 0, general && (general[i] & 2) ? 1 : 0};
+    ops[i] = plan::Op{target_masks[i], general && (general[i] & 1) != 0, general && (general[i] & 2) ? 1 : 0,
+                      general && (general[i] & 4) != 0};
   const char* cap_env = std::getenv("PTSBE_MAX_PASS_GATES");
   const int cap = cap_env ? std::atoi(cap_env) : 0;
   std::vector<int> perm(perm_io, perm_io + n_qubits);

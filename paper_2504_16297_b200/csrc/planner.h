@@ -24,6 +24,8 @@ struct Op {
   uint64_t mask;   // logical target mask
   bool general;
   int weight = 0;  // counts toward the per-pass gate budget (gates 1, sites 0)
+  bool first = false;  // decision site (conventional Algorithm 1): must be the first op of its
+                       // pass, so its outcome can be chosen from the state at the pass boundary
 };
 
 inline uint64_t phys_mask(uint64_t logical, const std::vector<int>& perm) {
@@ -46,10 +48,14 @@ inline int greedy(int n, const std::vector<Op>& ops, const std::vector<int>& per
   const uint64_t all = n >= 64 ? ~0ull : ((1ull << n) - 1);
   if (out_pass) out_pass->assign(m, -1);
   if (out_masks) out_masks->clear();
-  if (n <= L) {
-    if (out_pass) out_pass->assign(m, 0);
-    if (out_masks) out_masks->push_back(all);
-    return 1;
+  if (n <= L) {   // one tile holds the state: one pass, cut before every decision site
+    int p = 0;
+    for (int i = 0; i < m; ++i) {
+      if (ops[i].first && i > 0) ++p;
+      if (out_pass) (*out_pass)[i] = p;
+    }
+    if (out_masks) out_masks->assign(p + 1, all);
+    return p + 1;
   }
   const uint64_t low = c >= 64 ? ~0ull : ((1ull << c) - 1);
   std::vector<int> remaining(m), deferred;
@@ -62,7 +68,7 @@ inline int greedy(int n, const std::vector<Op>& ops, const std::vector<int>& per
     int taken = 0, weight = 0;
     for (int i : remaining) {
       const uint64_t t = pm[i];
-      if ((t & blocked) || (ops[i].general && gen_blocked)) {
+      if ((t & blocked) || (ops[i].general && gen_blocked) || (ops[i].first && taken > 0)) {
         deferred.push_back(i);
         blocked |= t;
         gen_blocked = gen_blocked || ops[i].general;

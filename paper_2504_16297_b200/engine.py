@@ -160,6 +160,24 @@ class Engine:
         self._check(fn(self.h, _ptr(sel), B, _ptr(w), _ptr(s), 0), "ptsbe_run_batch")
         return w, s
 
+    def run_conventional(self, sel: np.ndarray, uniforms: np.ndarray, with_probs: bool = False):
+        """Conventional trajectories (Algorithm 1, ref ``trajectory.py:40-70``): ``sel`` holds the
+        unitary-mixture outcomes, general sites' outcomes are chosen on device from the state
+        with ``uniforms[b, site]``.  Returns (final outcome table, weights, status[, probs])."""
+        sel = np.ascontiguousarray(sel, dtype=np.uint8)
+        B, S = sel.shape
+        u = np.ascontiguousarray(uniforms, dtype=np.float64)
+        if u.shape != (B, S):
+            raise ValidationError(f"uniform table must be {(B, S)}, got {u.shape}")
+        out = np.empty_like(sel)
+        w = np.empty(B, dtype=np.float64)
+        s = np.empty(B, dtype=np.int32)
+        n_dec = sum(1 for so in self.program.stream if so.general) if self.program is not None else S
+        probs = np.zeros((max(n_dec, 1), B, 64)) if with_probs else None
+        self._check(self.lib.ptsbe_run_conventional(self.h, _ptr(sel), _ptr(u), B, _ptr(out), _ptr(w), _ptr(s),
+                                                    _ptr(probs), 0), "ptsbe_run_conventional")
+        return (out, w, s, probs) if with_probs else (out, w, s)
+
     def run_device(self, sel_ptr: int, B: int, w_ptr: int, s_ptr: int, sync: bool = False):
         """Device-pointer variant (inputs already resident in HBM)."""
         flags = N.PTSBE_DEVICE_PTRS | (0 if sync else N.PTSBE_NO_SYNC)

@@ -74,6 +74,7 @@ class Program:
     passes: list = field(default_factory=list)
     g_ref: int = 0                # reference-equivalent full-state passes: #ops + #sites
     perm: list = None             # logical qubit -> physical bit (None = identity)
+    decide_general: bool = False  # planned for conventional trajectories (general sites open passes)
 
     @property
     def n_sites(self) -> int:
@@ -191,9 +192,13 @@ def plan_passes(n: int, stream: list, tile_bits: int, low_bits: int) -> list:
 
 
 def plan_native(n: int, stream: list, tile_bits: int, low_bits: int, search_iters: int = 0,
-                seed: int = 0, perm=None):
+                seed: int = 0, perm=None, decide_general: bool = False):
     """Same greedy rule in libptsbe (planner.h) plus a local search over the
-    physical qubit layout; returns (perm logical->physical, passes in physical qubits)."""
+    physical qubit layout; returns (perm logical->physical, passes in physical qubits).
+
+    ``decide_general``: every general-channel site opens its pass, so its outcome
+    can be chosen on device from the state at the pass boundary (conventional
+    trajectories, ``ptsbe_run_conventional``)."""
     import ctypes as C
 
     from . import _native as N
@@ -204,7 +209,8 @@ def plan_native(n: int, stream: list, tile_bits: int, low_bits: int, search_iter
     for i, so in enumerate(stream):
         for q in so.targets:
             masks[i] |= np.uint64(1 << q)
-        general[i] = (1 if so.general else 0) | (2 if so.kind == KIND_GATE else 0)
+        general[i] = (1 if so.general else 0) | (2 if so.kind == KIND_GATE else 0) | \
+            (4 if (decide_general and so.general) else 0)
     p = np.arange(n, dtype=np.int32) if perm is None else np.array(perm, dtype=np.int32)
     out_pass = np.zeros(max(m, 1), dtype=np.int32)
     out_masks = np.zeros(max(m, 1) + 1, dtype=np.uint64)
@@ -229,15 +235,18 @@ def default_search_iters(n: int, tile_bits: int) -> int:
 
 
 def compile_circuit(circuit, dtype: str = "c128", tile_bits: int | None = None,
-                    low_bits: int | None = None, search_iters: int | None = None, seed: int = 0) -> Program:
+                    low_bits: int | None = None, search_iters: int | None = None, seed: int = 0,
+                    decide_general: bool = False) -> Program:
     """Lower + plan.  Circuits wider than a tile get a physical qubit layout chosen
-    by local search to minimise HBM passes (shots and states stay logical)."""
+    by local search to minimise HBM passes (shots and states stay logical).
+    ``decide_general`` plans for conventional trajectories (see ``plan_native``)."""
     prog = lower(circuit)
     L = tile_bits if tile_bits is not None else DEFAULT_TILE_BITS[dtype]
     c = low_bits if low_bits is not None else DEFAULT_LOW_BITS[dtype]
     n = circuit.n_qubits
     iters = default_search_iters(n, L) if search_iters is None else search_iters
-    prog.perm, prog.passes = plan_native(n, prog.stream, L, c, iters, seed)
+    prog.perm, prog.passes = plan_native(n, prog.stream, L, c, iters, seed, decide_general=decide_general)
+    prog.decide_general = decide_general
     return prog
 
 

@@ -147,12 +147,12 @@ def test_every_bench_pass_against_oracle_random_input(config4, dtype):
             idx = coset_rows(c.n_qubits, qs, COSETS[dtype], rng)
             for b in range(3):
                 check_pass(prev[b], cur[b], oracle_items(c, prog, p, selections[b]), qs, idx, TOL[dtype])
-                # unitary pass: the whole state's norm is kept (accumulated in float64)
-                n2 = float(np.sum(np.abs(cur[b].astype(np.complex128)) ** 2))
-                assert abs(n2 - 1.0) <= (1e-5 if dtype == "c64" else 1e-12)
-            if dtype == "c64":
+            # unitary pass: every state keeps its norm (exact 2^-62 fixed-point sum on device)
+            n2 = eng.norm_totals(3).astype(np.float64) / 2.0 ** 62
+            assert np.all(np.abs(n2 - 1.0) <= (1e-5 if dtype == "c64" else 1e-12)), n2
+            if dtype == "c64" and eng.pass_info(p)["gb"] == 4:
                 # every coset of Q keeps its norm (the pass is unitary inside each coset): a
-                # full-state check of the tile addressing, not only the sampled cosets
+                # full-state check of the tile addressing of the 4-bit (256-thread) passes
                 a0, a1 = coset_norms(prev[2], qs), coset_norms(cur[2], qs)
                 assert np.max(np.abs(a1 - a0)) <= 1e-5 * max(float(a0.max()), 1e-30)
             prev = cur
@@ -165,8 +165,8 @@ def test_config4_trajectories_chain_equals_bench_path_and_oracle(config4, dtype)
     the PCG64 verification-mode shots equal the reference sampler on those 28-q states."""
     c = config4
     rng = np.random.default_rng(5)
-    specs = P.presample_probabilistic(c, 40, 10_000, np.random.default_rng(3))[:2]
-    assert all(s.selections for s in specs)
+    specs = [s for s in P.presample_probabilistic(c, 40, 10_000, np.random.default_rng(3)) if s.selections][:2]
+    assert len(specs) == 2
     prog = compile_circuit(c, dtype)
     sel = selection_matrix(prog, specs)
     with Engine(c.n_qubits, dtype, batch_cap=2) as eng:

@@ -75,3 +75,23 @@ def test_coset_oracle_equals_full_state_oracle():
     idx = O.scatter_bits(pats, rest)[:, None] | O.scatter_bits(np.arange(1 << len(qubits)), qubits)[None, :]
     got = O.apply_on_cosets(psi[idx], items, qubits)
     assert np.allclose(got, full[idx], rtol=1e-13, atol=1e-13)
+
+
+def test_oracle_conventional_trajectories_match_reference_goldens():
+    """oracle.run_conventional (trajectory.py:40-70) against the reference's run_trajectory goldens."""
+    import json
+    from conftest import GOLDEN, build_case
+    from paper_2504_16297_b200.execute import stream_rng
+    g = json.loads((GOLDEN / "golden_conv.json").read_text())
+    with np.load(GOLDEN / "golden_conv.npz") as z:
+        arrays = {k: z[k] for k in z.files}
+    for name, case in g["cases"].items():
+        c = build_case(case)
+        for run in case["run_trajectory"]:
+            rng = stream_rng(*run["seed"])
+            out = O.run_conventional(c, rng)
+            assert [list(p) for p in out["selections"]] == run["selections"], name
+            assert out["weight"] == pytest.approx(run["weight"], rel=1e-13)
+            ref = arrays[run["amps"]]
+            assert np.linalg.norm(out["state"] - ref) <= 1e-12 * np.linalg.norm(ref)
+            assert float(rng.random()) == run["next_uniform"]

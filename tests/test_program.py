@@ -106,3 +106,57 @@ def test_identity_gates_dropped_and_identity_outcomes_masked():
     prog = compile_circuit(c, "c128")
     assert [s.kind for s in prog.stream] == [1, 0, 1]    # 'i' gate removed, both sites kept
     assert all(ch["identity_mask"] == 1 for ch in prog.chans)
+
+
+def _conv_case(name):
+    import json
+    from conftest import GOLDEN, build_case
+    return build_case(json.loads((GOLDEN / "golden_conv.json").read_text())["cases"][name])
+
+
+@pytest.mark.parametrize("tile_bits,low_bits", [(4, 2), (6, 3), (11, 3), (12, 4)])
+@pytest.mark.parametrize("name", ["teleport_damped", "brick8_mixed", "ghz10_damped", "brick11_mixed"])
+def test_conventional_plan_opens_a_pass_at_every_general_site(name, tile_bits, low_bits):
+    """Planning for conventional trajectories (decision sites, ptsbe_plan bit 2): every
+    general-channel site is the first op of its pass -- its outcome is chosen from the state at
+    the pass boundary -- and the plan is still a legal reordering of the reference's loop."""
+    c = _conv_case(name)
+    prog = compile_circuit(c, "c128", tile_bits=tile_bits, low_bits=low_bits, decide_general=True)
+    order = [i for p in prog.passes for i in p.ops]
+    assert sorted(order) == list(range(len(prog.stream)))
+    n_general = sum(1 for so in prog.stream if so.general)
+    assert n_general > 0
+    opened = [p.ops[0] for p in prog.passes if prog.stream[p.ops[0]].general]
+    assert sum(1 for p in prog.passes for i in p.ops if prog.stream[i].general) == len(opened) == n_general
+    # ops a decision site may overtake or be overtaken by act on other qubits and are unitary
+    pos = {i: k for k, i in enumerate(order)}
+    for i, so in enumerate(prog.stream):
+        if not so.general:
+            continue
+        for j, other in enumerate(prog.stream):
+            moved = (j < i and pos[j] > pos[i]) or (j > i and pos[j] < pos[i])
+            if moved:
+                assert not set(other.targets) & set(so.targets)
+                assert not other.general
+    # the planned order gives the reference's state for sampled outcomes
+    rng = np.random.default_rng(3)
+    specs = P.presample_probabilistic(c, 30, 1, rng)
+    sel = selection_matrix(prog, specs)
+    for b, spec in enumerate(specs[:4]):
+        try:
+            ref_psi, ref_w = O.prepare(c, spec.selections)
+        except O.Annihilated:
+            continue
+        psi, w = _run_stream(c, prog, order, sel[b])
+        assert np.linalg.norm(psi - ref_psi) <= 1e-12
+        assert w == pytest.approx(ref_w, rel=1e-12)
+
+
+def test_conventional_plan_small_state_cuts_single_tile():
+    """n <= tile bits: one tile per pass, a new pass before each general site (not the first op)."""
+    c = _conv_case("teleport_damped")
+    prog = compile_circuit(c, "c128", decide_general=True)
+    n_general = sum(1 for so in prog.stream if so.general)
+    first_general = prog.stream[0].general
+    assert prog.n_passes == n_general + (0 if first_general else 1)
+    assert all(len(p.qubits) == c.n_qubits for p in prog.passes)

@@ -1,0 +1,14 @@
+#!/bin/bash
+# usage (GPU box): tools/gpu_prof_r2.sh TAG -- launch lists + per-pass DRAM bytes of the bench, c128 and c64
+mkdir -p gpurun_out
+tag=${1:-r}
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_$tag.log 2>&1
+for d in c128 c64; do
+  if [ $d = c128 ]; then np=17; else np=12; fi
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1000 --csv \
+    --log-file gpurun_out/launches_${d}_$tag.csv python bench.py --steps 2 --warmup 3 --no-cpu --dtype $d --secondary none \
+    > gpurun_out/ncu_launch_${d}_$tag.log 2>&1
+  timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+    -k regex:ptsbe_pass -s $((3 * np)) -c $np --csv --log-file gpurun_out/pass_dram_${d}_$tag.csv \
+    python bench.py --steps 1 --warmup 3 --no-cpu --dtype $d --secondary none > gpurun_out/ncu_dram_${d}_$tag.log 2>&1
+done
