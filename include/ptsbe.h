@@ -64,6 +64,12 @@ typedef enum { PTSBE_C64 = 0, PTSBE_C128 = 1 } ptsbe_dtype;
                                    they are (set_state / a previous range) instead of |0...0> */
 #define PTSBE_NO_SYNC     0x2u  /* do not synchronise the stream before returning
                                    (only meaningful with PTSBE_DEVICE_PTRS) */
+#define PTSBE_DEFER_NORMS 0x20u /* ptsbe_run_range of ONE pass of a shard: leave the shard-local
+                                   norms of its renormalising sites for ptsbe_slot_norms /
+                                   ptsbe_finalize_norms (shards of one process) */
+#define PTSBE_SHARDED     0x40u /* ptsbe_run_range of a shard in an NCCL shard group
+                                   (ptsbe_shard_init): norms of renormalising sites are
+                                   all-reduced over the group on the engine stream */
 #define PTSBE_KEEP_SEL    0x10u /* continued ptsbe_run_range: keep the device outcome table as it
                                    is (sel may be NULL) -- e.g. outcomes chosen on device */
 
@@ -193,6 +199,29 @@ int ptsbe_exchange_half(ptsbe_engine* h, int b, int bit, int value, void* buf, i
 /* Exact 2^-62 fixed-point sum of |a|^2 of each of the first B states (the
  * sampler's CDF total), for splitting shots across shards. */
 int ptsbe_norm_totals(ptsbe_engine* h, int B, uint64_t* out_totals);
+/* NCCL shard group (one shard per rank, one rank per GPU; `nccl_id` = 128 bytes from
+ * ptsbe_nccl_unique_id on rank 0, broadcast by the caller).  NCCL is loaded at run time. */
+int ptsbe_nccl_unique_id(void* out128);
+int ptsbe_shard_init(ptsbe_engine* h, const void* nccl_id, int rank, int nranks);
+/* Swap global bits gbits[j] (bits of the shard index = rank) with local bits lbits[j],
+ * j < nswap <= 3, for the first B states: ONE all-to-all of 2^nswap parts per group of
+ * shards (grouped ncclSend/ncclRecv on a comm stream, chunked and double-buffered so
+ * the part packing overlaps the transfer; persistent buffers <= 2 GiB). */
+int ptsbe_shard_swap(ptsbe_engine* h, int B, int nswap, const int32_t* gbits, const int32_t* lbits);
+/* The same exchange between the D = 2^k shards of ONE process on one device
+ * (handles hs[s] hold shard s): pairwise in-place part swaps, no buffers. */
+int ptsbe_shard_swap_local(ptsbe_engine* const* hs, int D, int B, int nswap, const int32_t* gbits,
+                           const int32_t* lbits);
+/* Cross-shard norms for PTSBE_DEFER_NORMS runs: shard-local norm^2 of the pending pass's
+ * renormalising slots (out[j*B + b], j < *out_slots <= 64), then the caller's sums
+ * over all shards finalise weights / status / stored norms on every shard. */
+int ptsbe_slot_norms(ptsbe_engine* h, int B, double* out, int* out_slots);
+int ptsbe_finalize_norms(ptsbe_engine* h, int B, const double* sums);
+/* Realized weights and status of the first B rows (after a run / finalize). */
+int ptsbe_get_weights(ptsbe_engine* h, int B, double* out_weight, int32_t* out_status);
+/* Amplitudes of state b at `count` PHYSICAL basis indices (normalised; verification of
+ * states too large to download). */
+int ptsbe_gather_amplitudes(ptsbe_engine* h, int b, const uint64_t* idx, int64_t count, void* out);
 /* Device address of state b (exchange buffers, debugging). */
 void* ptsbe_state_ptr(ptsbe_engine* h, int b);
 

@@ -32,6 +32,8 @@ PTSBE_NO_SYNC = 0x2
 PTSBE_ZERO_VECTOR = 0x4
 PTSBE_CONTINUE = 0x8
 PTSBE_KEEP_SEL = 0x10
+PTSBE_DEFER_NORMS = 0x20
+PTSBE_SHARDED = 0x40
 
 RNG_PCG64 = 0
 RNG_PHILOX = 1
@@ -75,6 +77,14 @@ SIGNATURES = {
                                   C.c_uint32]),
     "ptsbe_run_conventional": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
                                          C.c_void_p, C.c_void_p, C.c_uint32]),
+    "ptsbe_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "ptsbe_shard_init": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int]),
+    "ptsbe_shard_swap": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
+    "ptsbe_shard_swap_local": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
+    "ptsbe_slot_norms": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
+    "ptsbe_finalize_norms": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "ptsbe_get_weights": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
+    "ptsbe_gather_amplitudes": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p]),
     "ptsbe_exchange_half": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int]),
     "ptsbe_norm_totals": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "ptsbe_state_ptr": (C.c_void_p, [C.c_void_p, C.c_int]),

@@ -21,6 +21,8 @@
 #include "records.h"
 #include "conventional.cuh"
 #include "exact_cdf.cuh"
+#include "shard.cuh"
+#include "nccl_api.h"
 
 using namespace ptsbe;
 
@@ -132,6 +134,19 @@ struct ptsbe_engine {
   size_t rdm_cap = 0;
   BlockMap* d_maps = nullptr;     // exact-CDF block maps (verification-mode sampling)
   size_t maps_cap = 0;
+  // state sharding (shard.cuh): NCCL communicator of the shard group, exchange buffers,
+  // cross-shard Kraus norms
+  ncclComm_t comm = nullptr;
+  int shard_rank = 0, shard_nranks = 1;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t xev[4] = {nullptr, nullptr, nullptr, nullptr};
+  void* xbuf = nullptr;
+  size_t xbuf_bytes = 0;
+  double* d_slotsum = nullptr;    // per (slot, row) shard-local norm^2 of renormalising sites
+  size_t slotsum_cap = 0;
+  uint32_t run_flags = 0;         // flags of the current run_common call (launch_passes reads them)
+  int pending_pass = -1;          // PTSBE_DEFER_NORMS: pass whose slot norms await the global sums
+  int pending_ent = 0, pending_E = 0;
   std::string err;
 };
 
@@ -367,10 +382,31 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero, int p_begin = 0, int p
       h->ev_bytes.push_back(by);
     }
     if (ph.n_slots > 0) {
-      norm_finalize<<<E, 256, 0, h->stream>>>(h->d_partials, ph.n_slots, p.B, p.tiles,
-                                              h->d_slot_site + ph.slot_begin, h->d_nst, h->d_weight,
-                                              h->d_status, h->d_fail, p.ent);
-      CKL(h);
+      if (h->run_flags & (PTSBE_DEFER_NORMS | PTSBE_SHARDED)) {
+        // sharded state: the norms of renormalising sites are sums over every shard
+        norm_slot_sums<<<E, 256, 0, h->stream>>>(h->d_partials, ph.n_slots, p.B, p.tiles, p.ent, h->d_status,
+                                                 h->d_slotsum);
+        CKL(h);
+        if (h->run_flags & PTSBE_DEFER_NORMS) {   // the caller adds the shards' sums (ptsbe_finalize_norms)
+          h->pending_pass = (int)pi;
+          h->pending_ent = ent_begin[pi];
+          h->pending_E = E;
+        } else {
+          if (!h->comm) return fail(h, PTSBE_ERR_VALIDATION, "PTSBE_SHARDED needs ptsbe_shard_init");
+          const ncclResult_t nr = nccl::api().all_reduce(h->d_slotsum, h->d_slotsum, (size_t)ph.n_slots * p.B,
+                                                         ncclFloat64, ncclSum, h->comm, h->stream);
+          if (nr != ncclSuccess) return fail(h, PTSBE_ERR_NCCL, "ncclAllReduce: %s", nccl::api().error_string(nr));
+          norm_finalize_sums<<<(E + 127) / 128, 128, 0, h->stream>>>(h->d_slotsum, ph.n_slots, p.B,
+                                                                     h->d_slot_site + ph.slot_begin, h->d_nst,
+                                                                     h->d_weight, h->d_status, h->d_fail, p.ent, E);
+          CKL(h);
+        }
+      } else {
+        norm_finalize<<<E, 256, 0, h->stream>>>(h->d_partials, ph.n_slots, p.B, p.tiles,
+                                                h->d_slot_site + ph.slot_begin, h->d_nst, h->d_weight,
+                                                h->d_status, h->d_fail, p.ent);
+        CKL(h);
+      }
     }
     prev_general = ph.n_slots > 0;
   }
@@ -433,7 +469,13 @@ int run_common(ptsbe_engine* h, const uint8_t* sel, int B, double* out_weight, i
   if (p_begin > 0 && B != h->last_B)
     return fail(h, PTSBE_ERR_VALIDATION, "a continued pass range must keep the batch of %d states", h->last_B);
   if (B == 0) return 0;
+  if ((flags & PTSBE_DEFER_NORMS) && p_end - p_begin != 1)
+    return fail(h, PTSBE_ERR_VALIDATION, "PTSBE_DEFER_NORMS runs one pass at a time");
+  if (h->pending_pass >= 0)
+    return fail(h, PTSBE_ERR_VALIDATION, "pass %d still waits for its global norms (ptsbe_finalize_norms)",
+                h->pending_pass);
   CK(h, cudaSetDevice(h->dev));
+  h->run_flags = flags;
   if (flags & PTSBE_KEEP_SEL) {   // continued range over the device table as it is
     if (from_zero) return fail(h, PTSBE_ERR_VALIDATION, "PTSBE_KEEP_SEL needs a continued pass range");
   } else if (h->n_sites > 0) {
@@ -743,10 +785,14 @@ int ptsbe_destroy(ptsbe_engine* h) {
                   h->d_phases, h->d_matkind,
                   h->d_chans, h->d_site_chan, h->d_slot_site, h->d_partials, h->d_bs, h->d_total, h->d_off,
                   h->d_m, h->d_nuniq, h->d_uoff, h->d_rng, h->d_keys, h->d_tmp, h->d_idx, h->d_runidx,
-                  h->d_runcnt, h->d_chunks, h->d_ent, h->d_forks, h->d_mats64, h->d_u, h->d_rdm, h->d_maps};
+                  h->d_runcnt, h->d_chunks, h->d_ent, h->d_forks, h->d_mats64, h->d_u, h->d_rdm, h->d_maps, h->xbuf, h->d_slotsum};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : h->xev)
+    if (e) cudaEventDestroy(e);
+  if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
+  if (h->comm && nccl::api().ok) nccl::api().comm_destroy(h->comm);
   if (h->stream) cudaStreamDestroy(h->stream);
   delete h;
   return 0;
@@ -1109,6 +1155,13 @@ int ptsbe_load_program(ptsbe_engine* h, const ptsbe_op* ops, int n_ops, const do
     if (dalloc(h, &h->d_partials, need)) return PTSBE_ERR_CUDA;
     h->partial_cap = need;
   }
+  size_t need_ss = 1;
+  for (auto& P : ph) need_ss = std::max(need_ss, (size_t)P.n_slots * (h->cap + 1));
+  if (need_ss > h->slotsum_cap) {
+    if (dalloc(h, &h->d_slotsum, need_ss)) return PTSBE_ERR_CUDA;
+    h->slotsum_cap = need_ss;
+  }
+  h->pending_pass = -1;
   const int max_smem = 227 * 1024;
   if (h->dtype == PTSBE_C64)
     CK(h, cudaFuncSetAttribute(pass_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
@@ -1333,6 +1386,296 @@ int ptsbe_norm_totals(ptsbe_engine* h, int B, uint64_t* out_totals) {
   sample_blockscan<<<B, 1024, 0, h->stream>>>(sp);
   CKL(h);
   CK(h, cudaMemcpyAsync(out_totals, h->d_total, (size_t)B * 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+// ---- state sharding (shard.cuh) --------------------------------------------------
+
+extern "C++" {
+namespace {
+int part_map(ptsbe_engine* h, int nswap, const int32_t* gbits, const int32_t* lbits, int nglobal, PartMap* m,
+             uint32_t* gmask) {
+  if (nswap < 1 || nswap > 3 || !gbits || !lbits)
+    return fail(h, PTSBE_ERR_VALIDATION, "a swap exchanges 1..3 qubit pairs, got %d", nswap);
+  m->kp = nswap;
+  m->lmask = 0;
+  *gmask = 0;
+  for (int j = 0; j < nswap; ++j) {
+    if (lbits[j] < 0 || lbits[j] >= h->n || ((m->lmask >> lbits[j]) & 1) || gbits[j] < 0 || gbits[j] >= nglobal ||
+        ((*gmask >> gbits[j]) & 1))
+      return fail(h, PTSBE_ERR_VALIDATION, "bad swap pair %d: global bit %d, local bit %d", j, gbits[j], lbits[j]);
+    m->lbit[j] = lbits[j];
+    m->lmask |= 1ull << lbits[j];
+    *gmask |= 1u << gbits[j];
+  }
+  for (int j = 0; j < nswap; ++j) m->lsort[j] = m->lbit[j];
+  std::sort(m->lsort, m->lsort + nswap);
+  if (h->permuted) return fail(h, PTSBE_ERR_VALIDATION, "sharded exchange needs an unpermuted engine layout");
+  return 0;
+}
+
+// shard index with the swapped global bits spelling c (pair j <-> bit j of c)
+inline int shard_with(int s, const int32_t* gbits, int nswap, uint32_t c) {
+  for (int j = 0; j < nswap; ++j) s = (s & ~(1 << gbits[j])) | (int)(((c >> j) & 1u) << gbits[j]);
+  return s;
+}
+inline uint32_t spelled(int s, const int32_t* gbits, int nswap) {
+  uint32_t c = 0;
+  for (int j = 0; j < nswap; ++j) c |= (uint32_t)((s >> gbits[j]) & 1) << j;
+  return c;
+}
+}  // namespace
+}  // extern "C++"
+
+int ptsbe_nccl_unique_id(void* out) {
+  if (!out) return PTSBE_ERR_VALIDATION;
+  nccl::Api& A = nccl::api();
+  if (!A.ok) return PTSBE_ERR_NCCL;
+  ncclUniqueId id;
+  if (A.get_unique_id(&id) != ncclSuccess) return PTSBE_ERR_NCCL;
+  std::memcpy(out, &id, sizeof id);
+  return 0;
+}
+
+int ptsbe_shard_init(ptsbe_engine* h, const void* nccl_id, int rank, int nranks) {
+  if (!h || !nccl_id) return PTSBE_ERR_VALIDATION;
+  if (nranks < 1 || (nranks & (nranks - 1)) || rank < 0 || rank >= nranks)
+    return fail(h, PTSBE_ERR_VALIDATION, "shard group of %d ranks (rank %d): need a power of two", nranks, rank);
+  nccl::Api& A = nccl::api();
+  if (!A.ok) return fail(h, PTSBE_ERR_NCCL, "NCCL unavailable: %s", A.why.c_str());
+  CK(h, cudaSetDevice(h->dev));
+  if (h->comm) { A.comm_destroy(h->comm); h->comm = nullptr; }
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_id, sizeof id);
+  const ncclResult_t r = A.comm_init_rank(&h->comm, nranks, id, rank);
+  if (r != ncclSuccess) { h->comm = nullptr; return fail(h, PTSBE_ERR_NCCL, "ncclCommInitRank: %s", A.error_string(r)); }
+  h->shard_rank = rank;
+  h->shard_nranks = nranks;
+  if (!h->comm_stream) CK(h, cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
+  for (auto& e : h->xev)
+    if (!e) CK(h, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return 0;
+}
+
+extern "C++" {
+template <typename V>
+static int shard_swap_impl(ptsbe_engine* h, int B, const PartMap& m, const int32_t* gbits, int nswap) {
+  const int s = h->shard_rank;
+  const uint32_t own = spelled(s, gbits, nswap);
+  const int P = (1 << nswap) - 1;                 // parts that travel
+  const uint64_t part_len = 1ull << (h->n - nswap);
+  const size_t amp = sizeof(V);
+  // chunk: <= 512 MiB of sends per round, double-buffered sends + receives
+  uint64_t CH = std::max<uint64_t>(1, std::min<uint64_t>(part_len, (512ull << 20) / ((uint64_t)P * amp)));
+  if (const char* e = std::getenv("PTSBE_SHARD_CHUNK"))   // test knob: force many chunks
+    CH = std::max<uint64_t>(1, std::min<uint64_t>(CH, (uint64_t)std::atoll(e)));
+  // test knob (1-rank group, one GPU): every part goes to this rank itself -- exercises
+  // the pack / grouped send-recv / unpack pipeline; the state must come back unchanged
+  const bool self_test = h->shard_nranks == 1 && std::getenv("PTSBE_SHARD_SELF_TEST");
+  const size_t need = 4ull * P * CH * amp;
+  if (need > h->xbuf_bytes) {
+    if (h->xbuf) cudaFree(h->xbuf);
+    h->xbuf = nullptr;
+    h->xbuf_bytes = 0;
+    CK(h, cudaMalloc(&h->xbuf, need));
+    h->xbuf_bytes = need;
+  }
+  V* sendb[2] = {(V*)h->xbuf, (V*)h->xbuf + (size_t)P * CH};
+  V* recvb[2] = {(V*)h->xbuf + 2ull * P * CH, (V*)h->xbuf + 3ull * P * CH};
+  nccl::Api& A = nccl::api();
+  const uint64_t nch = (part_len + CH - 1) / CH;
+  const long long iters = (long long)B * (long long)nch;
+  const unsigned grid = (unsigned)std::min<uint64_t>((CH + 255) / 256, 4u * (unsigned)h->num_sms);
+  auto region = [&](long long it, int b) {
+    V* st = reinterpret_cast<V*>(h->states) + ((size_t)b << h->n);
+    return st;
+  };
+  auto pack = [&](long long it) -> int {
+    const int b = (int)(it / (long long)nch);
+    const uint64_t j0 = (uint64_t)(it % (long long)nch) * CH, len = std::min<uint64_t>(CH, part_len - j0);
+    int slot = 0;
+    for (uint32_t c = 0; c <= (uint32_t)P; ++c) {
+      if (c == own) continue;
+      part_copy<V><<<grid, 256, 0, h->stream>>>(region(it, b), sendb[it & 1] + (size_t)slot * CH, m, c, j0, len, 0);
+      CKL(h);
+      ++slot;
+    }
+    CK(h, cudaEventRecord(h->xev[it & 1], h->stream));              // packed
+    CK(h, cudaStreamWaitEvent(h->comm_stream, h->xev[it & 1], 0));
+    ncclResult_t r = A.group_start();
+    slot = 0;
+    for (uint32_t c = 0; c <= (uint32_t)P && r == ncclSuccess; ++c) {
+      if (c == own) continue;
+      const int peer = self_test ? s : shard_with(s, gbits, nswap, c);
+      r = A.send(sendb[it & 1] + (size_t)slot * CH, (size_t)len * amp, ncclInt8, peer, h->comm, h->comm_stream);
+      if (r == ncclSuccess)
+        r = A.recv(recvb[it & 1] + (size_t)slot * CH, (size_t)len * amp, ncclInt8, peer, h->comm, h->comm_stream);
+      ++slot;
+    }
+    const ncclResult_t r2 = A.group_end();
+    if (r != ncclSuccess || r2 != ncclSuccess)
+      return fail(h, PTSBE_ERR_NCCL, "ncclSend/ncclRecv: %s", A.error_string(r != ncclSuccess ? r : r2));
+    CK(h, cudaEventRecord(h->xev[2 + (it & 1)], h->comm_stream));    // received
+    return 0;
+  };
+  auto unpack = [&](long long it) -> int {
+    const int b = (int)(it / (long long)nch);
+    const uint64_t j0 = (uint64_t)(it % (long long)nch) * CH, len = std::min<uint64_t>(CH, part_len - j0);
+    CK(h, cudaStreamWaitEvent(h->stream, h->xev[2 + (it & 1)], 0));
+    int slot = 0;
+    for (uint32_t c = 0; c <= (uint32_t)P; ++c) {
+      if (c == own) continue;
+      part_copy<V><<<grid, 256, 0, h->stream>>>(region(it, b), recvb[it & 1] + (size_t)slot * CH, m, c, j0, len, 1);
+      CKL(h);
+      ++slot;
+    }
+    return 0;
+  };
+  // pack(i+1) overlaps the transfer of chunk i; buffers of i+1 were freed when unpack(i-1)
+  // waited for their transfer
+  for (long long it = 0; it < iters; ++it) {
+    if (int r = pack(it)) return r;
+    if (it > 0)
+      if (int r = unpack(it - 1)) return r;
+  }
+  if (iters > 0)
+    if (int r = unpack(iters - 1)) return r;
+  h->tsum_ok = false;
+  CK(h, cudaStreamSynchronize(h->stream));
+  return 0;
+}
+}  // extern "C++"
+
+int ptsbe_shard_swap(ptsbe_engine* h, int B, int nswap, const int32_t* gbits, const int32_t* lbits) {
+  if (!h) return PTSBE_ERR_VALIDATION;
+  if (!h->comm) return fail(h, PTSBE_ERR_VALIDATION, "no shard group: call ptsbe_shard_init first");
+  if (B < 1 || B > h->cap) return fail(h, PTSBE_ERR_VALIDATION, "batch %d outside [1, %d]", B, h->cap);
+  int nglobal = 0;
+  while ((1 << nglobal) < h->shard_nranks) ++nglobal;
+  if (h->shard_nranks == 1 && std::getenv("PTSBE_SHARD_SELF_TEST")) nglobal = 3;
+  PartMap m;
+  uint32_t gmask = 0;
+  if (int r = part_map(h, nswap, gbits, lbits, nglobal, &m, &gmask)) return r;
+  CK(h, cudaSetDevice(h->dev));
+  return h->dtype == PTSBE_C64 ? shard_swap_impl<float2>(h, B, m, gbits, nswap)
+                               : shard_swap_impl<double2>(h, B, m, gbits, nswap);
+}
+
+int ptsbe_shard_swap_local(ptsbe_engine* const* hs, int D, int B, int nswap, const int32_t* gbits,
+                           const int32_t* lbits) {
+  if (!hs || D < 2 || (D & (D - 1))) return PTSBE_ERR_VALIDATION;
+  ptsbe_engine* h0 = hs[0];
+  if (!h0) return PTSBE_ERR_VALIDATION;
+  int nglobal = 0;
+  while ((1 << nglobal) < D) ++nglobal;
+  PartMap m;
+  uint32_t gmask = 0;
+  if (int r = part_map(h0, nswap, gbits, lbits, nglobal, &m, &gmask)) return r;
+  for (int s = 0; s < D; ++s) {
+    if (!hs[s] || hs[s]->dev != h0->dev || hs[s]->n != h0->n || hs[s]->dtype != h0->dtype || hs[s]->permuted)
+      return fail(h0, PTSBE_ERR_VALIDATION, "shard %d: engines must share device, width, dtype and layout", s);
+    if (B < 1 || B > hs[s]->cap) return fail(h0, PTSBE_ERR_VALIDATION, "batch %d exceeds shard %d", B, s);
+  }
+  CK(h0, cudaSetDevice(h0->dev));
+  for (int s = 0; s < D; ++s) CK(h0, cudaStreamSynchronize(hs[s]->stream));
+  const uint64_t part_len = 1ull << (h0->n - nswap);
+  const unsigned grid = (unsigned)std::min<uint64_t>((part_len + 255) / 256, 8u * (unsigned)h0->num_sms);
+  for (int s = 0; s < D; ++s) {
+    const uint32_t own = spelled(s, gbits, nswap);
+    for (uint32_t c = 0; c < (1u << nswap); ++c) {
+      const int peer = shard_with(s, gbits, nswap, c);
+      if (c == own || peer < s) continue;                // each pair once
+      for (int b = 0; b < B; ++b) {
+        if (h0->dtype == PTSBE_C64) {
+          float2* a = reinterpret_cast<float2*>(hs[s]->states) + ((size_t)b << h0->n);
+          float2* q = reinterpret_cast<float2*>(hs[peer]->states) + ((size_t)b << h0->n);
+          part_swap<float2><<<grid, 256, 0, h0->stream>>>(a, q, m, c, own, part_len);
+        } else {
+          double2* a = reinterpret_cast<double2*>(hs[s]->states) + ((size_t)b << h0->n);
+          double2* q = reinterpret_cast<double2*>(hs[peer]->states) + ((size_t)b << h0->n);
+          part_swap<double2><<<grid, 256, 0, h0->stream>>>(a, q, m, c, own, part_len);
+        }
+        CKL(h0);
+      }
+    }
+  }
+  CK(h0, cudaStreamSynchronize(h0->stream));
+  for (int s = 0; s < D; ++s) hs[s]->tsum_ok = false;
+  return 0;
+}
+
+int ptsbe_slot_norms(ptsbe_engine* h, int B, double* out, int* out_slots) {
+  if (!h || !out || !out_slots) return PTSBE_ERR_VALIDATION;
+  if (h->pending_pass < 0) return fail(h, PTSBE_ERR_VALIDATION, "no pass waits for its norms");
+  if (B != h->last_B) return fail(h, PTSBE_ERR_VALIDATION, "batch %d, the pending pass ran %d", B, h->last_B);
+  const int ns = h->passes[h->pending_pass].n_slots;
+  const int Bst = h->cap + 1;
+  CK(h, cudaSetDevice(h->dev));
+  for (int j = 0; j < ns; ++j)
+    CK(h, cudaMemcpyAsync(out + (size_t)j * B, h->d_slotsum + (size_t)j * Bst, (size_t)B * 8, cudaMemcpyDeviceToHost,
+                          h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  *out_slots = ns;
+  return 0;
+}
+
+int ptsbe_finalize_norms(ptsbe_engine* h, int B, const double* sums) {
+  if (!h || !sums) return PTSBE_ERR_VALIDATION;
+  if (h->pending_pass < 0) return fail(h, PTSBE_ERR_VALIDATION, "no pass waits for its norms");
+  if (B != h->last_B) return fail(h, PTSBE_ERR_VALIDATION, "batch %d, the pending pass ran %d", B, h->last_B);
+  const PassHost& ph = h->passes[h->pending_pass];
+  const int Bst = h->cap + 1;
+  CK(h, cudaSetDevice(h->dev));
+  for (int j = 0; j < ph.n_slots; ++j)
+    CK(h, cudaMemcpyAsync(h->d_slotsum + (size_t)j * Bst, sums + (size_t)j * B, (size_t)B * 8, cudaMemcpyHostToDevice,
+                          h->stream));
+  norm_finalize_sums<<<(h->pending_E + 127) / 128, 128, 0, h->stream>>>(
+      h->d_slotsum, ph.n_slots, Bst, h->d_slot_site + ph.slot_begin, h->d_nst, h->d_weight, h->d_status, h->d_fail,
+      h->d_ent + h->pending_ent, h->pending_E);
+  CKL(h);
+  h->pending_pass = -1;
+  CK(h, cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int ptsbe_get_weights(ptsbe_engine* h, int B, double* out_weight, int32_t* out_status) {
+  if (!h) return PTSBE_ERR_VALIDATION;
+  if (B < 0 || B > h->cap) return fail(h, PTSBE_ERR_VALIDATION, "batch %d exceeds capacity %d", B, h->cap);
+  CK(h, cudaSetDevice(h->dev));
+  if (out_weight) CK(h, cudaMemcpyAsync(out_weight, h->d_weight, (size_t)B * 8, cudaMemcpyDeviceToHost, h->stream));
+  if (out_status) CK(h, cudaMemcpyAsync(out_status, h->d_status, (size_t)B * 4, cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int ptsbe_gather_amplitudes(ptsbe_engine* h, int b, const uint64_t* idx, int64_t count, void* out) {
+  if (!h || (count > 0 && (!idx || !out))) return PTSBE_ERR_VALIDATION;
+  if (b < 0 || b >= h->cap) return fail(h, PTSBE_ERR_VALIDATION, "state %d out of range", b);
+  if (count <= 0) return 0;
+  const uint64_t nmask = (1ull << h->n) - 1;
+  for (int64_t i = 0; i < count; ++i)
+    if (idx[i] & ~nmask) return fail(h, PTSBE_ERR_VALIDATION, "index %llu outside 2^%d", (unsigned long long)idx[i], h->n);
+  CK(h, cudaSetDevice(h->dev));
+  int r = h->dtype == PTSBE_C64 ? rescale_if_needed<float>(h) : rescale_if_needed<double>(h);
+  if (r) return r;
+  uint64_t* d_idx = nullptr;
+  void* d_out = nullptr;
+  CK(h, cudaMallocAsync((void**)&d_idx, (size_t)count * 8, h->stream));
+  CK(h, cudaMallocAsync(&d_out, (size_t)count * h->amp_bytes, h->stream));
+  CK(h, cudaMemcpyAsync(d_idx, idx, (size_t)count * 8, cudaMemcpyHostToDevice, h->stream));
+  const unsigned g = (unsigned)std::min<int64_t>((count + 255) / 256, 4096);
+  const size_t off = (size_t)b << h->n;
+  if (h->dtype == PTSBE_C64)
+    gather_amps<float2><<<g, 256, 0, h->stream>>>(reinterpret_cast<const float2*>(h->states) + off, d_idx, count,
+                                                  reinterpret_cast<float2*>(d_out));
+  else
+    gather_amps<double2><<<g, 256, 0, h->stream>>>(reinterpret_cast<const double2*>(h->states) + off, d_idx, count,
+                                                   reinterpret_cast<double2*>(d_out));
+  CKL(h);
+  CK(h, cudaMemcpyAsync(out, d_out, (size_t)count * h->amp_bytes, cudaMemcpyDeviceToHost, h->stream));
+  CK(h, cudaFreeAsync(d_idx, h->stream));
+  CK(h, cudaFreeAsync(d_out, h->stream));
   CK(h, cudaStreamSynchronize(h->stream));
   return 0;
 }

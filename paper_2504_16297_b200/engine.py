@@ -209,6 +209,14 @@ class Engine:
                                    C.c_void_p(idx_ptr), C.c_void_p(cnt_ptr), C.c_void_p(nuniq_ptr), flags)
         self._check(st, "ptsbe_sample")
 
+    def gather(self, b: int, phys_idx) -> np.ndarray:
+        """Normalised amplitudes of state b at PHYSICAL basis indices."""
+        idx = np.ascontiguousarray(phys_idx, dtype=np.uint64)
+        out = np.empty(idx.size, dtype=self.np_dtype)
+        self._check(self.lib.ptsbe_gather_amplitudes(self.h, int(b), _ptr(idx), idx.size, _ptr(out)),
+                    "ptsbe_gather_amplitudes")
+        return out
+
     def get_state(self, b: int = 0) -> np.ndarray:
         out = np.empty(1 << self.n, dtype=self.np_dtype)
         self._check(self.lib.ptsbe_get_state(self.h, b, _ptr(out), 0), "ptsbe_get_state")
@@ -262,6 +270,24 @@ class Engine:
         return dict(zip(keys, (int(v) for v in out)))
 
 
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for ptsbe_shard_init (rank 0 makes it, the caller broadcasts it)."""
+    lib = N.load_library()
+    buf = C.create_string_buffer(128)
+    N.check(lib, None, lib.ptsbe_nccl_unique_id(buf), "ptsbe_nccl_unique_id")
+    return buf.raw
+
+
+def shard_swap_local(engines, B: int, pairs) -> None:
+    """Global<->local swap between the shards of one process (engines[s] holds shard s)."""
+    lib = N.load_library()
+    arr = (C.c_void_p * len(engines))(*[e.h.value for e in engines])
+    g = np.array([p[0] for p in pairs], dtype=np.int32)
+    lb = np.array([p[1] for p in pairs], dtype=np.int32)
+    N.check(lib, engines[0].h, lib.ptsbe_shard_swap_local(arr, len(engines), int(B), len(pairs), _ptr(g), _ptr(lb)),
+            "ptsbe_shard_swap_local")
+
+
 def pcg64_state_words(seed_or_rng) -> np.ndarray:
     """(state_hi, state_lo, inc_hi, inc_lo) of a numpy PCG64 stream, for RNG_PCG64."""
     if isinstance(seed_or_rng, np.random.Generator):
@@ -279,14 +305,19 @@ def pcg64_state_words(seed_or_rng) -> np.ndarray:
 def _engine_sharding_methods():
     """Sharding primitives on Engine (ptsbe_run_range / exchange_half / norm_totals)."""
 
-    def run_range(self, sel, pass_begin: int, pass_end: int, zero_vector: bool = False, continue_: bool = False):
+    def run_range(self, sel, pass_begin: int, pass_end: int, zero_vector: bool = False, continue_: bool = False,
+                  defer_norms: bool = False, sharded: bool = False):
         """Passes [pass_begin, pass_end); from pass 0 the states start at |0...0> (or the zero
-        vector) unless ``continue_``, which applies the range to the states as they are."""
+        vector) unless ``continue_``, which applies the range to the states as they are.
+        ``defer_norms``: one pass of a shard whose renormalising norms are summed over the
+        shards by the caller (slot_norms / finalize_norms); ``sharded``: a shard of an NCCL
+        group (shard_init), norms all-reduced inside the engine."""
         sel = np.ascontiguousarray(sel, dtype=np.uint8)
         B = sel.shape[0]
         w = np.empty(B, dtype=np.float64)
         s = np.empty(B, dtype=np.int32)
-        flags = (N.PTSBE_ZERO_VECTOR if zero_vector else 0) | (N.PTSBE_CONTINUE if continue_ else 0)
+        flags = (N.PTSBE_ZERO_VECTOR if zero_vector else 0) | (N.PTSBE_CONTINUE if continue_ else 0) | \
+            (N.PTSBE_DEFER_NORMS if defer_norms else 0) | (N.PTSBE_SHARDED if sharded else 0)
         self._check(self.lib.ptsbe_run_range(self.h, _ptr(sel), B, int(pass_begin), int(pass_end), _ptr(w),
                                              _ptr(s), flags), "ptsbe_run_range")
         return w, s
@@ -300,7 +331,38 @@ def _engine_sharding_methods():
         self._check(self.lib.ptsbe_norm_totals(self.h, int(B), _ptr(out)), "ptsbe_norm_totals")
         return out
 
+    def shard_init(self, nccl_id: bytes, rank: int, nranks: int):
+        buf = C.create_string_buffer(bytes(nccl_id), 128)
+        self._check(self.lib.ptsbe_shard_init(self.h, buf, int(rank), int(nranks)), "ptsbe_shard_init")
+
+    def shard_swap(self, B: int, pairs):
+        g = np.array([p[0] for p in pairs], dtype=np.int32)
+        lb = np.array([p[1] for p in pairs], dtype=np.int32)
+        self._check(self.lib.ptsbe_shard_swap(self.h, int(B), len(pairs), _ptr(g), _ptr(lb)), "ptsbe_shard_swap")
+
+    def slot_norms(self, B: int) -> np.ndarray:
+        """(slots, B) shard-local norm^2 of the pending pass's renormalising sites."""
+        out = np.zeros((64, B), dtype=np.float64)
+        n = C.c_int()
+        self._check(self.lib.ptsbe_slot_norms(self.h, int(B), _ptr(out), C.byref(n)), "ptsbe_slot_norms")
+        return out[: n.value].copy()
+
+    def finalize_norms(self, B: int, sums: np.ndarray):
+        a = np.ascontiguousarray(sums, dtype=np.float64)
+        self._check(self.lib.ptsbe_finalize_norms(self.h, int(B), _ptr(a)), "ptsbe_finalize_norms")
+
+    def get_weights(self, B: int):
+        w = np.empty(B, dtype=np.float64)
+        s = np.empty(B, dtype=np.int32)
+        self._check(self.lib.ptsbe_get_weights(self.h, int(B), _ptr(w), _ptr(s)), "ptsbe_get_weights")
+        return w, s
+
     Engine.run_range = run_range
+    Engine.shard_init = shard_init
+    Engine.shard_swap = shard_swap
+    Engine.slot_norms = slot_norms
+    Engine.finalize_norms = finalize_norms
+    Engine.get_weights = get_weights
     Engine.exchange_half = exchange_half
     Engine.norm_totals = norm_totals
 

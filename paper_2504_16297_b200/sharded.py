@@ -10,11 +10,20 @@ index):
   shard runs the same fused passes on its own amplitudes (the global bits are
   spectators), so a segment is just a pass range of an ordinary program
   compiled for ``n - k`` qubits (``ptsbe_run_range``);
-* between segments a global qubit is **swapped** with a local one: each shard
-  exchanges the half of its amplitudes whose local bit differs from its
-  global bit with the partner shard ``s ^ (1 << g)`` (``ptsbe_exchange_half``:
-  pack -> send/recv -> unpack).  The victim local qubit is the one used
-  furthest in the future (Belady), so swaps are rare;
+* between segments the global qubits the next op needs are **swapped** with
+  local ones (the local qubit used furthest in the future, Belady) -- all
+  pairs due together in ONE all-to-all of 2^k' parts per shard group
+  (``ptsbe_shard_swap``: grouped ``ncclSend``/``ncclRecv`` on a comm stream,
+  chunked and double-buffered so part packing overlaps the NVLink transfer;
+  ``ptsbe_shard_swap_local`` swaps parts in place between the shards of one
+  process);
+* renormalising (general) Kraus sites: the realized weight is a ratio of norms
+  of the WHOLE state, so each shard reduces its slot norms and the sums are
+  added over the shards -- ``ncclAllReduce`` on the engine stream inside
+  ``ptsbe_run_range(PTSBE_SHARDED)``, or pass by pass through
+  ``ptsbe_slot_norms`` / ``ptsbe_finalize_norms`` (one process, or a
+  torch.distributed transport) -- so every shard applies the same weight and
+  deferred renormalisation (ref ``statevector.py:136-145``, ``execute.py:93-97``);
 * sampling: each shard's exact fixed-point CDF total (``ptsbe_norm_totals``,
   integers, so the split is exact) gives the multinomial split of the
   trajectory's shots over shards; every shard draws its share with its own
@@ -23,10 +32,10 @@ index):
   offered by the unsharded engine only.)
 
 Transports: ``VirtualShards`` keeps all shards in one process (one device;
-used by the GPU tests), ``DistributedShards`` runs one shard per rank and
-exchanges halves with ``torch.distributed`` point-to-point ops (NCCL over
-NVLink on a B200 box; gloo in the CPU tests).  Renormalising (general)
-channels need a cross-shard norm and are rejected here.
+GPU tests and single-GPU validation up to 34 qubits), ``DistributedShards``
+runs one shard per rank -- ``EngineShardBackend(transport="nccl")`` exchanges
+through the engine's own NCCL communicator (the B200 path), ``"torch"``
+through ``torch.distributed`` point-to-point ops (gloo in the CPU tests).
 """
 
 from __future__ import annotations
@@ -49,6 +58,7 @@ class ShardPlan:
     final_map: dict                # logical qubit -> ("L", bit) | ("G", bit)
     program: Program               # program over n - k local qubits
     initial_map: dict = field(default_factory=dict)
+    pass_general: list = field(default_factory=list)   # per pass: has renormalising sites
 
     @property
     def n_local(self) -> int:
@@ -57,6 +67,10 @@ class ShardPlan:
     @property
     def n_swaps(self) -> int:
         return sum(len(s) for s in self.swaps)
+
+    @property
+    def any_general(self) -> bool:
+        return any(self.pass_general)
 
 
 def _next_use(stream, start, q):
@@ -74,8 +88,6 @@ def plan_sharded(circuit, k: int, dtype: str = "c64", tile_bits: int | None = No
     if not 1 <= k < n - 2:
         raise ValidationError(f"cannot shard {n} qubits over 2^{k} shards")
     prog = lower(circuit)
-    if any(so.general for so in prog.stream):
-        raise ValidationError("sharded execution supports unitary-mixture channels only")
     stream = prog.stream
     nl = n - k
     # initial layout: the k qubits used latest are global; local bits by usage (busiest lowest)
@@ -120,7 +132,8 @@ def plan_sharded(circuit, k: int, dtype: str = "c64", tile_bits: int | None = No
         ranges.append((p0, len(passes)))
     sprog = Program(nl, new_stream, prog.mats, prog.chans, prog.chan_index, prog.site_chan,
                     passes=passes, g_ref=prog.g_ref, perm=None)
-    return ShardPlan(n, k, ranges, swaps, dict(where), sprog, initial)
+    pass_general = [any(new_stream[i].general for i in pp.ops) for pp in passes]
+    return ShardPlan(n, k, ranges, swaps, dict(where), sprog, initial, pass_general)
 
 
 def physical_to_logical(shard: np.ndarray, local_idx: np.ndarray, plan: ShardPlan) -> np.ndarray:
@@ -160,26 +173,29 @@ class VirtualShards:
         for e in self.engines:
             e.close()
 
-    def _swap(self, B, g, l):
-        import torch
-        dev = torch.device("cuda", self.engines[0].device)
-        cdt = torch.complex64 if self.dtype == "c64" else torch.complex128
-        half = 1 << (self.plan.n_local - 1)
-        for b in range(B):
-            bufs = [torch.empty(half, dtype=cdt, device=dev) for _ in range(self.D)]
-            for s, e in enumerate(self.engines):
-                e.exchange_half(b, l, 1 - ((s >> g) & 1), bufs[s].data_ptr(), unpack=False)
-            for s, e in enumerate(self.engines):
-                partner = s ^ (1 << g)
-                e.exchange_half(b, l, 1 - ((s >> g) & 1), bufs[partner].data_ptr(), unpack=True)
-
     def run(self, sel: np.ndarray):
+        """Prepare B trajectories over the shards; returns (weights, status) of the whole states."""
+        from .engine import shard_swap_local
         B = sel.shape[0]
-        for i, (p0, p1) in enumerate(self.plan.segments):
-            for s, e in enumerate(self.engines):   # only shard 0 holds |0...0> initially
-                e.run_range(sel, p0, p1, zero_vector=(p0 == 0 and s != 0))
-            for g, l in self.plan.swaps[i]:
-                self._swap(B, g, l)
+        plan = self.plan
+        for i, (p0, p1) in enumerate(plan.segments):
+            if plan.any_general:     # pass by pass: global norms of renormalising sites
+                for p in range(p0, p1):
+                    for s, e in enumerate(self.engines):
+                        e.run_range(sel, p, p + 1, zero_vector=(p == 0 and s != 0),
+                                    defer_norms=plan.pass_general[p])
+                    if plan.pass_general[p]:
+                        total = self.engines[0].slot_norms(B)
+                        for e in self.engines[1:]:
+                            total = total + e.slot_norms(B)      # fixed shard order
+                        for e in self.engines:
+                            e.finalize_norms(B, total)
+            else:
+                for s, e in enumerate(self.engines):   # only shard 0 holds |0...0> initially
+                    e.run_range(sel, p0, p1, zero_vector=(p0 == 0 and s != 0))
+            if plan.swaps[i]:
+                shard_swap_local(self.engines, B, plan.swaps[i])
+        return self.engines[0].get_weights(B)
 
     def sample(self, shots, seeds):
         """Philox shots per trajectory -> list of (logical indices sorted, counts)."""
@@ -216,7 +232,13 @@ class VirtualShards:
 
 
 class DistributedShards:
-    """One shard per rank (one process per GPU); swaps over torch.distributed P2P (NCCL)."""
+    """One shard per rank (one process per GPU).
+
+    ``backend`` is this rank's shard.  A backend with ``native = True`` (the engine's
+    NCCL group, ``EngineShardBackend(transport="nccl")``) does swaps and cross-shard
+    norms itself on the GPU; otherwise swaps go over ``torch.distributed`` P2P and the
+    norms of renormalising sites through ``all_reduce`` pass by pass.
+    """
 
     def __init__(self, plan: ShardPlan, backend, dtype: str = "c64", group=None):
         import torch.distributed as dist
@@ -227,30 +249,56 @@ class DistributedShards:
         self.world = dist.get_world_size(group)
         if self.world != 1 << plan.k:
             raise ValidationError(f"{self.world} ranks for 2^{plan.k} shards")
-        self.backend = backend      # object with run_range / exchange_half / norm_totals / sample / device tensors
+        self.backend = backend
 
     def run(self, sel: np.ndarray):
-        import torch.distributed as dist
+        """Prepare B trajectories; returns this rank's (weights, status) -- the same on every shard."""
         B = sel.shape[0]
         s = self.rank
-        for i, (p0, p1) in enumerate(self.plan.segments):
-            self.backend.run_range(sel, p0, p1, p0 == 0 and s != 0)
-            for g, l in self.plan.swaps[i]:
-                partner = s ^ (1 << g)
-                v = 1 - ((s >> g) & 1)
-                for b in range(B):
-                    send = self.backend.half_buffer()
-                    recv = self.backend.half_buffer()
-                    self.backend.exchange_half(b, l, v, send, unpack=False)
-                    self.backend.before_send()
-                    reqs = dist.batch_isend_irecv([dist.P2POp(dist.isend, send, partner, self.group),
-                                                   dist.P2POp(dist.irecv, recv, partner, self.group)])
-                    for r in reqs:
-                        r.wait()
-                    # NCCL's wait() only orders torch's current stream; the unpack runs on the
-                    # engine's own stream, so it must not start before the receive landed
-                    self.backend.after_recv()
-                    self.backend.exchange_half(b, l, v, recv, unpack=True)
+        plan = self.plan
+        native = getattr(self.backend, "native", False)
+        for i, (p0, p1) in enumerate(plan.segments):
+            if native or not plan.any_general:
+                self.backend.run_range(sel, p0, p1, p0 == 0 and s != 0)
+            else:
+                for p in range(p0, p1):
+                    self.backend.run_range(sel, p, p + 1, p == 0 and s != 0, defer_norms=plan.pass_general[p])
+                    if plan.pass_general[p]:
+                        self.backend.finalize_norms(B, self._all_reduce(self.backend.slot_norms(B)))
+            if not plan.swaps[i]:
+                continue
+            if native:
+                self.backend.swap(B, plan.swaps[i])      # one all-to-all for every pair due here
+            else:
+                for g, l in plan.swaps[i]:
+                    self._swap_torch(B, g, l)
+        return self.backend.get_weights(B)
+
+    def _all_reduce(self, a: np.ndarray) -> np.ndarray:
+        import torch
+        import torch.distributed as dist
+        t = torch.from_numpy(np.ascontiguousarray(a)).to(self.backend.comm_device())
+        dist.all_reduce(t, group=self.group)
+        return t.cpu().numpy()
+
+    def _swap_torch(self, B, g, l):
+        import torch.distributed as dist
+        s = self.rank
+        partner = s ^ (1 << g)
+        v = 1 - ((s >> g) & 1)
+        send = self.backend.half_buffer()
+        recv = self.backend.half_buffer()
+        for b in range(B):
+            self.backend.exchange_half(b, l, v, send, unpack=False)
+            self.backend.before_send()
+            reqs = dist.batch_isend_irecv([dist.P2POp(dist.isend, send, partner, self.group),
+                                           dist.P2POp(dist.irecv, recv, partner, self.group)])
+            for r in reqs:
+                r.wait()
+            # NCCL's wait() only orders torch's current stream; the unpack runs on the
+            # engine's own stream, so it must not start before the receive landed
+            self.backend.after_recv()
+            self.backend.exchange_half(b, l, v, recv, unpack=True)
 
     def sample(self, shots, seeds):
         """Returns per-trajectory (logical indices, counts) on rank 0, None elsewhere."""
@@ -286,22 +334,49 @@ def sharded_selection(plan: ShardPlan, specs) -> np.ndarray:
 
 
 class EngineShardBackend:
-    """This rank's shard on its GPU, for DistributedShards (NCCL exchanges)."""
+    """This rank's shard on its GPU, for DistributedShards.
 
-    def __init__(self, plan: ShardPlan, dtype: str = "c64", batch_cap: int = 1, device: int = 0):
-        from .engine import Engine
+    ``transport="nccl"`` (default): the engine joins an NCCL group of the shard ranks
+    (``ptsbe_shard_init``; rank 0 makes the id, ``group`` broadcasts it) and does the
+    swaps and cross-shard norms on the GPU.  ``"torch"``: swaps over torch.distributed
+    P2P with host-driven norms (any backend, e.g. gloo)."""
+
+    def __init__(self, plan: ShardPlan, dtype: str = "c64", batch_cap: int = 1, device: int = 0,
+                 transport: str = "nccl", group=None):
+        from .engine import Engine, nccl_unique_id
         self.plan = plan
         self.dtype = dtype
         self.engine = Engine(plan.n_local, dtype, batch_cap=batch_cap, device=device)
         self.engine.load_program(plan.program)
+        self.native = transport == "nccl"
+        if self.native:
+            import torch.distributed as dist
+            rank, world = dist.get_rank(group), dist.get_world_size(group)
+            obj = [nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0, group=group)
+            self.engine.shard_init(obj[0], rank, world)
+        elif transport != "torch":
+            raise ValidationError(f"unknown shard transport '{transport}'")
 
     def half_buffer(self):
         import torch
         cdt = torch.complex64 if self.dtype == "c64" else torch.complex128
         return torch.empty(1 << (self.plan.n_local - 1), dtype=cdt, device=torch.device("cuda", self.engine.device))
 
-    def run_range(self, sel, p0, p1, zero_vector=False):
-        self.engine.run_range(sel, p0, p1, zero_vector=zero_vector)
+    def run_range(self, sel, p0, p1, zero_vector=False, defer_norms=False):
+        self.engine.run_range(sel, p0, p1, zero_vector=zero_vector, defer_norms=defer_norms, sharded=self.native)
+
+    def swap(self, B, pairs):
+        self.engine.shard_swap(B, pairs)
+
+    def slot_norms(self, B):
+        return self.engine.slot_norms(B)
+
+    def finalize_norms(self, B, sums):
+        self.engine.finalize_norms(B, sums)
+
+    def get_weights(self, B):
+        return self.engine.get_weights(B)
 
     def comm_device(self):
         import torch

@@ -10,7 +10,9 @@ the identical input; SURVEY section 8(d) describes each config.
   4  steane_blocks(4)        28 q: four [[7,1,3]] blocks, encode + transversal non-Clifford
                              layers + inter-block transversal cx + decode; depolarizing (1q) +
                              bit_flip (cx) on every target
-  5  steane_blocks(5)        35 q, same construction
+  5  steane_blocks(5)        35 q, same construction (two+ GPUs of sharded state at c64);
+     steane_blocks(4, ancillas=6) is its 34-qubit form (CONFIG5_34: fits one B200 sharded
+     virtually, 2 x 64 GiB at c64)
 """
 
 from __future__ import annotations
@@ -71,10 +73,13 @@ def _steane_encode(base: int):
     return out
 
 
-def steane_blocks(blocks: int = 4, rounds: int = 7, seed: int = 11, p1: float = 1e-3, p2: float = 1e-3):
+def steane_blocks(blocks: int = 4, rounds: int = 7, seed: int = 11, p1: float = 1e-3, p2: float = 1e-3,
+                  ancillas: int = 0):
     """``blocks`` [[7,1,3]] blocks (7*blocks qubits): encode, `rounds` x (transversal 1q layer +
-    inter-block transversal cx), decode.  >= 300 ops at 4 blocks."""
-    n = 7 * blocks
+    inter-block transversal cx), decode.  >= 300 ops at 4 blocks.  ``ancillas`` extra qubits
+    (after the blocks) each extract one Z-type stabilizer of a block (cx from its 4 qubits)
+    before the decode -- 4 blocks + 6 ancillas is the 34-qubit size of config 5."""
+    n = 7 * blocks + ancillas
     rng = np.random.default_rng(seed)
     lines = []
     for b in range(blocks):
@@ -82,7 +87,7 @@ def steane_blocks(blocks: int = 4, rounds: int = 7, seed: int = 11, p1: float = 
     kinds = ("ry", "t", "h", "rz")
     for r in range(rounds):
         kind = kinds[r % len(kinds)]
-        for q in range(n):
+        for q in range(7 * blocks):
             if kind in ("ry", "rz"):
                 lines.append(f"gate {kind} {q} @ {float(rng.uniform(0, 2 * math.pi))!r}")
             else:
@@ -95,6 +100,9 @@ def steane_blocks(blocks: int = 4, rounds: int = 7, seed: int = 11, p1: float = 
                 continue
             used.update((b, partner))
             lines += [f"gate cx {7 * b + i} {7 * partner + i}" for i in range(7)]
+    for a in range(ancillas):
+        b, (p, ts) = a % blocks, _STEANE_CHECKS[(a // blocks) % 3]
+        lines += [f"gate cx {7 * b + q} {7 * blocks + a}" for q in (p,) + ts]
     for b in range(blocks):
         enc = _steane_encode(7 * b)
         lines += list(reversed(enc))     # h and cx are self-inverse
@@ -109,7 +117,9 @@ CONFIGS = {
     3: ("random_brickwork", lambda: random_brickwork(20)),
     4: ("steane_blocks", lambda: steane_blocks(4)),
     5: ("steane_blocks", lambda: steane_blocks(5)),
+    534: ("steane_blocks+ancillas", lambda: steane_blocks(4, ancillas=6)),
 }
+CONFIG5_34 = 534
 
 
 def build(config: int, parse_circuit, parse_noise_model, attach_noise):
