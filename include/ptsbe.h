@@ -70,6 +70,9 @@ typedef enum { PTSBE_C64 = 0, PTSBE_C128 = 1 } ptsbe_dtype;
 #define PTSBE_SHARDED     0x40u /* ptsbe_run_range of a shard in an NCCL shard group
                                    (ptsbe_shard_init): norms of renormalising sites are
                                    all-reduced over the group on the engine stream */
+#define PTSBE_HOST_MIRROR 0x80u /* with PTSBE_DEVICE_PTRS: the host copies registered by
+                                   ptsbe_set_host_mirror stand in for reading the device outcome
+                                   table / shot counts back (no device->host sync per call) */
 #define PTSBE_KEEP_SEL    0x10u /* continued ptsbe_run_range: keep the device outcome table as it
                                    is (sel may be NULL) -- e.g. outcomes chosen on device */
 
@@ -217,6 +220,11 @@ int ptsbe_shard_swap_local(ptsbe_engine* const* hs, int D, int B, int nswap, con
  * over all shards finalise weights / status / stored norms on every shard. */
 int ptsbe_slot_norms(ptsbe_engine* h, int B, double* out, int* out_slots);
 int ptsbe_finalize_norms(ptsbe_engine* h, int B, const double* sums);
+/* Host copies of the device-resident inputs of the next PTSBE_HOST_MIRROR calls (the
+ * caller keeps them alive): sel[B*n_sites] for ptsbe_run_batch's scheduling, shots[B]
+ * for ptsbe_sample's shot layout.  With PTSBE_DEVICE_PTRS, ptsbe_sample's CSR output
+ * (out_idx / out_cnt / out_nuniq) is compacted on device; the stream is not drained. */
+int ptsbe_set_host_mirror(ptsbe_engine* h, const uint8_t* sel, const int64_t* shots, int B);
 /* Realized weights and status of the first B rows (after a run / finalize). */
 int ptsbe_get_weights(ptsbe_engine* h, int B, double* out_weight, int32_t* out_status);
 /* Amplitudes of state b at `count` PHYSICAL basis indices (normalised; verification of

@@ -43,6 +43,7 @@ from .presample import (
     joint_probability,
     presample_band,
     presample_probabilistic,
+    presample_probabilistic_iter,
     reallocate_proportional,
     site_outcome_probs,
     unique_kraus,
@@ -59,7 +60,7 @@ def __getattr__(name):
         "Dataset": "execute", "ShotRecord": "execute", "format_records": "execute", "execute_all": "execute", "execute_naive": "execute",
         "execute_trajectory": "execute", "manifest_core": "execute", "mix_seed": "execute",
         "prepare_state": "execute", "stream_rng": "execute", "throughput_report": "execute",
-        "unique_fraction": "execute", "run_specs": "execute", "dataset_from_output": "execute",
+        "unique_fraction": "execute", "run_specs": "execute", "presample_and_execute": "execute", "dataset_from_output": "execute",
         "execute_all_distributed": "distributed",
         "ComplexState": "statevector", "ShotBatch": "statevector", "apply_gate": "statevector",
         "apply_kraus_normalized": "statevector", "apply_matrix": "statevector", "init_zero": "statevector",

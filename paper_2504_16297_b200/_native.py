@@ -34,6 +34,7 @@ PTSBE_CONTINUE = 0x8
 PTSBE_KEEP_SEL = 0x10
 PTSBE_DEFER_NORMS = 0x20
 PTSBE_SHARDED = 0x40
+PTSBE_HOST_MIRROR = 0x80
 
 RNG_PCG64 = 0
 RNG_PHILOX = 1
@@ -83,6 +84,7 @@ SIGNATURES = {
     "ptsbe_shard_swap_local": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     "ptsbe_slot_norms": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
     "ptsbe_finalize_norms": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
+    "ptsbe_set_host_mirror": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
     "ptsbe_get_weights": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
     "ptsbe_gather_amplitudes": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int64, C.c_void_p]),
     "ptsbe_exchange_half": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int]),

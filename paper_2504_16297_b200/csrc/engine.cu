@@ -145,6 +145,11 @@ struct ptsbe_engine {
   double* d_slotsum = nullptr;    // per (slot, row) shard-local norm^2 of renormalising sites
   size_t slotsum_cap = 0;
   uint32_t run_flags = 0;         // flags of the current run_common call (launch_passes reads them)
+  // PTSBE_HOST_MIRROR: host copies of the next device-pointer call's outcome table / shot
+  // counts (scheduling only; the kernels read the device copies)
+  const uint8_t* mirror_sel = nullptr;
+  const int64_t* mirror_shots = nullptr;
+  int mirror_B = 0;
   int pending_pass = -1;          // PTSBE_DEFER_NORMS: pass whose slot norms await the global sums
   int pending_ent = 0, pending_E = 0;
   std::string err;
@@ -484,7 +489,10 @@ int run_common(ptsbe_engine* h, const uint8_t* sel, int B, double* out_weight, i
     if (int r = copy_in(h, h->d_sel, sel, (size_t)B * h->n_sites, flags)) return r;
     // the shared-trunk schedule needs each trajectory's first non-default site on the host
     h->host_sel.resize((size_t)B * h->n_sites);
-    if (flags & PTSBE_DEVICE_PTRS) {
+    if ((flags & PTSBE_DEVICE_PTRS) && (flags & PTSBE_HOST_MIRROR)) {
+      if (!h->mirror_sel || h->mirror_B < B) return fail(h, PTSBE_ERR_VALIDATION, "no host mirror of the outcome table");
+      std::memcpy(h->host_sel.data(), h->mirror_sel, h->host_sel.size());
+    } else if (flags & PTSBE_DEVICE_PTRS) {
       CK(h, cudaMemcpyAsync(h->host_sel.data(), h->d_sel, h->host_sel.size(), cudaMemcpyDeviceToHost, h->stream));
       CK(h, cudaStreamSynchronize(h->stream));
     } else {
@@ -537,7 +545,10 @@ int sample_impl(ptsbe_engine* h, int B, const int64_t* shots, int rng_mode, cons
                 const uint64_t* keys, uint64_t* out_idx, uint32_t* out_cnt, int64_t* out_nuniq,
                 uint32_t flags) {
   std::vector<int64_t> m(B), off(B);
-  if (flags & PTSBE_DEVICE_PTRS) {
+  if ((flags & PTSBE_DEVICE_PTRS) && (flags & PTSBE_HOST_MIRROR)) {
+    if (!h->mirror_shots || h->mirror_B < B) return fail(h, PTSBE_ERR_VALIDATION, "no host mirror of the shot counts");
+    std::memcpy(m.data(), h->mirror_shots, (size_t)B * 8);
+  } else if (flags & PTSBE_DEVICE_PTRS) {
     CK(h, cudaMemcpyAsync(m.data(), shots, (size_t)B * 8, cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
   } else {
@@ -658,6 +669,22 @@ int sample_impl(ptsbe_engine* h, int B, const int64_t* shots, int rng_mode, cons
   sample_rle<<<B, 1024, 0, h->stream>>>(h->d_idx, h->d_off, h->d_m, h->d_status, h->d_runidx, h->d_runcnt,
                                         h->d_nuniq);
   CKL(h);
+  if (flags & PTSBE_DEVICE_PTRS) {
+    // device outputs: CSR offsets scanned and runs compacted on device -- no host round trip
+    long long maxm = 0;
+    for (int b = 0; b < B; ++b) maxm = std::max<long long>(maxm, m[b]);
+    exclusive_scan_i64<<<1, 1024, 0, h->stream>>>(h->d_nuniq, B, h->d_uoff);
+    CKL(h);
+    if (maxm > 0) {
+      dim3 gc((unsigned)std::min<long long>((maxm + 255) / 256, 4096), (unsigned)B);
+      compact_runs<<<gc, 256, 0, h->stream>>>(h->d_runidx, h->d_runcnt, h->d_off, h->d_nuniq, h->d_uoff, out_idx,
+                                              out_cnt);
+      CKL(h);
+    }
+    CK(h, cudaMemcpyAsync(out_nuniq, h->d_nuniq, (size_t)B * 8, cudaMemcpyDeviceToDevice, h->stream));
+    if (!(flags & PTSBE_NO_SYNC)) CK(h, cudaStreamSynchronize(h->stream));
+    return 0;
+  }
   std::vector<int64_t> nu(B), uoff(B);
   CK(h, cudaMemcpyAsync(nu.data(), h->d_nuniq, (size_t)B * 8, cudaMemcpyDeviceToHost, h->stream));
   CK(h, cudaStreamSynchronize(h->stream));
@@ -1636,6 +1663,14 @@ int ptsbe_finalize_norms(ptsbe_engine* h, int B, const double* sums) {
   CKL(h);
   h->pending_pass = -1;
   CK(h, cudaStreamSynchronize(h->stream));
+  return 0;
+}
+
+int ptsbe_set_host_mirror(ptsbe_engine* h, const uint8_t* sel, const int64_t* shots, int B) {
+  if (!h || B < 0) return PTSBE_ERR_VALIDATION;
+  h->mirror_sel = sel;
+  h->mirror_shots = shots;
+  h->mirror_B = B;
   return 0;
 }
 

@@ -475,6 +475,30 @@ __global__ void pack_half(const V* st, V* buf, int n, int bit, int value, int un
   }
 }
 
+// Exclusive prefix sum of n <= 1024*64 int64 counts (one CTA): CSR offsets on device.
+__global__ void __launch_bounds__(1024) exclusive_scan_i64(const int64_t* in, int n, int64_t* out) {
+  __shared__ int64_t part[1024];
+  constexpr int PER = 64;
+  const int t = threadIdx.x;
+  int64_t s = 0;
+  for (int e = 0; e < PER; ++e) {
+    const int i = t * PER + e;
+    if (i < n) s += in[i];
+  }
+  part[t] = s;
+  __syncthreads();
+  if (t == 0) {
+    int64_t acc = 0;
+    for (int i = 0; i < 1024; ++i) { const int64_t v = part[i]; part[i] = acc; acc += v; }
+  }
+  __syncthreads();
+  int64_t acc = part[t];
+  for (int e = 0; e < PER; ++e) {
+    const int i = t * PER + e;
+    if (i < n) { out[i] = acc; acc += in[i]; }
+  }
+}
+
 // Gather each trajectory's runs into one contiguous CSR stream.
 __global__ void compact_runs(const uint64_t* run_idx, const uint32_t* run_cnt, const int64_t* off,
                              const int64_t* nuniq, const int64_t* uoff, uint64_t* out_idx, uint32_t* out_cnt) {

@@ -178,18 +178,35 @@ class Engine:
                                                     _ptr(probs), 0), "ptsbe_run_conventional")
         return (out, w, s, probs) if with_probs else (out, w, s)
 
-    def run_device(self, sel_ptr: int, B: int, w_ptr: int, s_ptr: int, sync: bool = False):
+    def set_host_mirror(self, sel: np.ndarray | None, shots: np.ndarray | None) -> None:
+        """Host copies of the device-resident inputs of the next ``mirror=True`` device calls
+        (scheduling only: no device->host read-back per call).  Kept alive by the engine."""
+        self._mirror = (None if sel is None else np.ascontiguousarray(sel, dtype=np.uint8),
+                        None if shots is None else np.ascontiguousarray(shots, dtype=np.int64))
+        a, b = self._mirror
+        B = (a.shape[0] if a is not None else b.size) if (a is not None or b is not None) else 0
+        self._check(self.lib.ptsbe_set_host_mirror(self.h, _ptr(a), _ptr(b), B), "ptsbe_set_host_mirror")
+
+    def run_device(self, sel_ptr: int, B: int, w_ptr: int, s_ptr: int, sync: bool = False, mirror: bool = False):
         """Device-pointer variant (inputs already resident in HBM)."""
-        flags = N.PTSBE_DEVICE_PTRS | (0 if sync else N.PTSBE_NO_SYNC)
+        flags = N.PTSBE_DEVICE_PTRS | (0 if sync else N.PTSBE_NO_SYNC) | (N.PTSBE_HOST_MIRROR if mirror else 0)
         self._check(self.lib.ptsbe_run_batch(self.h, C.c_void_p(sel_ptr), B, C.c_void_p(w_ptr),
                                              C.c_void_p(s_ptr), flags), "ptsbe_run_batch")
 
-    def sample(self, shots, rng_mode: int = N.RNG_PCG64, rng_state=None, keys=None) -> Shots:
+    def sample(self, shots, rng_mode: int = N.RNG_PCG64, rng_state=None, keys=None, out=None) -> Shots:
+        """``out``: optional preallocated (indices uint64, counts uint32) host arrays with room for
+        sum(shots) entries -- e.g. pinned memory, so the CSR read-back runs at full DMA speed."""
         shots = np.ascontiguousarray(shots, dtype=np.int64)
         B = shots.size
         total = int(shots.sum()) if B else 0
-        idx = np.empty(max(total, 1), dtype=np.uint64)
-        cnt = np.empty(max(total, 1), dtype=np.uint32)
+        if out is not None:
+            idx, cnt = out
+            if idx.dtype != np.uint64 or cnt.dtype != np.uint32 or idx.size < total or cnt.size < total \
+                    or not (idx.flags.c_contiguous and cnt.flags.c_contiguous):
+                raise ValidationError("sample output buffers: contiguous uint64 / uint32 with room for every shot")
+        else:
+            idx = np.empty(max(total, 1), dtype=np.uint64)
+            cnt = np.empty(max(total, 1), dtype=np.uint32)
         nu = np.zeros(B, dtype=np.int64)
         rs = None if rng_state is None else np.ascontiguousarray(rng_state, dtype=np.uint64)
         ks = None if keys is None else np.ascontiguousarray(keys, dtype=np.uint64)
@@ -202,9 +219,9 @@ class Engine:
         return Shots(idx[:U], cnt[:U], off)
 
     def sample_device(self, B: int, shots_ptr: int, rng_mode: int, rng_ptr: int, idx_ptr: int, cnt_ptr: int,
-                      nuniq_ptr: int, sync: bool = False) -> None:
+                      nuniq_ptr: int, sync: bool = False, mirror: bool = False) -> None:
         """Device-pointer variant of sample(): inputs and CSR outputs stay in HBM."""
-        flags = N.PTSBE_DEVICE_PTRS | (0 if sync else N.PTSBE_NO_SYNC)
+        flags = N.PTSBE_DEVICE_PTRS | (0 if sync else N.PTSBE_NO_SYNC) | (N.PTSBE_HOST_MIRROR if mirror else 0)
         st = self.lib.ptsbe_sample(self.h, B, C.c_void_p(shots_ptr), rng_mode, C.c_void_p(rng_ptr), None,
                                    C.c_void_p(idx_ptr), C.c_void_p(cnt_ptr), C.c_void_p(nuniq_ptr), flags)
         self._check(st, "ptsbe_sample")
