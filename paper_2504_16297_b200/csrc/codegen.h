@@ -212,6 +212,143 @@ inline Swizzle choose_swizzle(bool c64, int L, const std::vector<DevPhase>& phas
   return best;
 }
 
+// TMA tile staging for a pass (gen_prelude.cuh run_pass TMA): 128-B rows need the pass's
+// contiguous low run to cover a row (c64: 16 amplitudes, c128: 8) and the row table holds
+// <= 64 gather groups (256 rows).  Default: complex128 passes (config 4: 456 K vs 445 K
+// shots/s with cp.async, pass roofline 0.757 vs 0.739); complex64 passes keep cp.async
+// (1.371 M vs 1.385 M: the 5-bit 128-thread passes lose a few % to the store drain).
+// PTSBE_TMA=1 / 0 forces either way.
+inline bool tma_ok(bool c64, int c, int L) {
+  const char* e = std::getenv("PTSBE_TMA");
+  const bool want = std::getenv("PTSBE_NO_TMA") ? false : e ? std::atoi(e) != 0 : !c64;
+  return want && c >= (c64 ? 4 : 3) && L - (c64 ? 4 : 3) <= 8;
+}
+
+// TMA tile staging lands each 128-B tile row u at shared-memory row slot(u) with the
+// hardware's 128-B swizzle (16-B chunk ^= slot & 7).  With slot = any GF(2)-linear
+// bijection whose low three bits are B(u), the chunk of row u is XORed with B(u): exactly
+// the free family above (chunk ^= a linear function of the row bits) whenever that
+// function has rank 3.  make_tma_layout takes the model-chosen free swizzle, repairs its
+// rank if needed (coordinate descent under the rank constraint), and returns the
+// amplitude-index map (row bits move too) plus slot^-1 for the gathers.
+struct TmaLayout {
+  Swizzle sw;              // amplitude index -> shared-memory slot (rows and chunks)
+  uint32_t inv[32] = {0};  // slot row -> tile row u (linear: XOR of inv[j] over set bits j)
+  int R = 0;               // row bits
+};
+
+inline int gf2_rank3(const uint32_t* col, int R) {   // rank of 3-bit columns
+  uint32_t basis[3] = {0, 0, 0};
+  int r = 0;
+  for (int k = 0; k < R; ++k) {
+    uint32_t v = col[k] & 7u;
+    for (int b = 2; b >= 0 && v; --b)
+      if ((v >> b) & 1u) {
+        if (basis[b]) v ^= basis[b];
+        else { basis[b] = v; ++r; v = 0; }
+      }
+  }
+  return r;
+}
+
+inline bool make_tma_layout(bool c64, int L, const std::vector<DevPhase>& phases, int GB, const Swizzle& free_sw,
+                            TmaLayout* out) {
+  const int cb = c64 ? 1 : 0, lo = c64 ? 4 : 3;
+  const int R = L - lo;
+  if (R < 3 || R > 20) return false;
+  uint32_t col[32] = {0};
+  for (int k = 0; k < R; ++k) col[k] = (free_sw.m[lo + k] >> cb) & 7u;
+  auto build = [&](const uint32_t* c) {
+    Swizzle z;
+    z.c64 = c64;
+    for (int k = 0; k < R; ++k) z.m[lo + k] = c[k] << cb;
+    return z;
+  };
+  auto cost = [&](const uint32_t* c) {
+    if (gf2_rank3(c, R) < 3) return 1 << 30;
+    const Swizzle z = build(c);
+    int t = 0;
+    for (const DevPhase& D : phases) t += phase_wavefronts(z, D, GB);
+    return t;
+  };
+  int bc = cost(col);
+  if (bc >= (1 << 30)) {   // rank < 3: start from the row-low-bits map and descend
+    uint32_t c2[32] = {0};
+    for (int k = 0; k < R; ++k) c2[k] = k < 3 ? (1u << k) : col[k];
+    std::memcpy(col, c2, sizeof c2);
+    bc = cost(col);
+    for (int sweep = 0; sweep < 4; ++sweep) {
+      bool improved = false;
+      for (int k = 0; k < R; ++k)
+        for (uint32_t v = 0; v < 8; ++v) {
+          uint32_t cand[32];
+          std::memcpy(cand, col, sizeof cand);
+          cand[k] = v;
+          const int c = cost(cand);
+          if (c < bc) { bc = c; std::memcpy(col, cand, sizeof cand); improved = true; }
+        }
+      if (!improved) break;
+    }
+  }
+  // pivots: three row bits with independent columns -> slot bits 0-2 carry B(u)
+  int piv[3] = {-1, -1, -1};
+  {
+    uint32_t basis[3] = {0, 0, 0};
+    for (int k = 0, got = 0; k < R && got < 3; ++k) {
+      uint32_t v = col[k];
+      for (int b = 2; b >= 0 && v; --b)
+        if ((v >> b) & 1u) {
+          if (basis[b]) v ^= basis[b];
+          else { basis[b] = v; piv[got++] = k; v = 0; }
+        }
+    }
+    if (piv[2] < 0) return false;
+  }
+  uint32_t slot_of[32] = {0};   // slot(e_k)
+  for (int k = 0, nxt = 3; k < R; ++k) {
+    const bool is_piv = k == piv[0] || k == piv[1] || k == piv[2];
+    slot_of[k] = col[k] | (is_piv ? 0u : (1u << nxt));
+    if (!is_piv) ++nxt;
+  }
+  // invert the R x R slot matrix over GF(2) (columns slot_of[k])
+  uint32_t a[32], inv[32];
+  for (int j = 0; j < R; ++j) { a[j] = 0; inv[j] = 0; }
+  for (int k = 0; k < R; ++k)   // row j of the matrix: bit k set iff slot_of[k] has bit j
+    for (int j = 0; j < R; ++j)
+      if ((slot_of[k] >> j) & 1u) a[j] |= 1u << k;
+  uint32_t e[32];
+  for (int j = 0; j < R; ++j) e[j] = 1u << j;     // augmented identity rows
+  for (int c = 0; c < R; ++c) {
+    int pr = -1;
+    for (int j = c; j < R; ++j)
+      if ((a[j] >> c) & 1u) { pr = j; break; }
+    if (pr < 0) return false;
+    std::swap(a[c], a[pr]);
+    std::swap(e[c], e[pr]);
+    for (int j = 0; j < R; ++j)
+      if (j != c && ((a[j] >> c) & 1u)) { a[j] ^= a[c]; e[j] ^= e[c]; }
+  }
+  // a is identity now; row k of the inverse (u bit k) = e[k]: u_k = parity(e[k] & s)
+  for (int j = 0; j < R; ++j)      // inv[j] = slot^-1(e_j): bit k set iff e[k] has bit j
+    for (int k = 0; k < R; ++k)
+      if ((e[k] >> j) & 1u) inv[j] |= 1u << k;
+  out->R = R;
+  out->sw = Swizzle();
+  out->sw.c64 = c64;
+  for (int k = 0; k < R; ++k) out->sw.m[lo + k] = ((slot_of[k] ^ (1u << k)) << lo) | (col[k] << cb);
+  std::memcpy(out->inv, inv, sizeof inv);
+  return true;
+}
+
+// Device functor for the slot -> tile-row map of a TMA layout.
+inline std::string slot_inv_struct(const std::string& name, const TmaLayout& t) {
+  std::ostringstream o;
+  o << "struct " << name << " { __device__ __forceinline__ uint32_t operator()(uint32_t s) const { return 0u";
+  for (int j = 0; j < t.R; ++j) o << " ^ ((0u - ((s >> " << j << ") & 1u)) & " << t.inv[j] << "u)";
+  o << "; } };\n";
+  return o.str();
+}
+
 // Device functor for a swizzle (compile-time masks).
 inline std::string swizzle_struct(const std::string& name, const Swizzle& z, int L) {
   std::ostringstream o;
@@ -338,6 +475,7 @@ struct GenProgram {
   const ptsbe_channel* chans;
   const int32_t* site_chan;
   std::vector<GenPass> passes;
+  bool tma = true;          // the engine has a tensor map over its states (TMA tile staging allowed)
 };
 
 inline std::string kernel_name(int pass) { return "ptsbe_pass_" + std::to_string(pass); }
@@ -458,8 +596,16 @@ inline std::string generate(const GenProgram& P) {
     const uint64_t nmask = P.n >= 64 ? ~0ull : ((1ull << P.n) - 1);
     const uint64_t comp = ~gp.qmask & nmask;
     const uint64_t hmask = gp.qmask & ~((1ull << gp.c) - 1);
-    const Swizzle sw = std::getenv("PTSBE_FIXED_SWIZZLE") ? Swizzle::fixed(P.c64)   // A/B knob
-                                                        : choose_swizzle(P.c64, gp.L, gp.phases, GB);
+    const Swizzle free_sw = std::getenv("PTSBE_FIXED_SWIZZLE") ? Swizzle::fixed(P.c64)   // A/B knob
+                                                               : choose_swizzle(P.c64, gp.L, gp.phases, GB);
+    TmaLayout tl;
+    const bool tma = P.tma && tma_ok(P.c64, gp.c, gp.L) && make_tma_layout(P.c64, gp.L, gp.phases, GB, free_sw, &tl);
+    const Swizzle sw = tma ? tl.sw : free_sw;
+    if (std::getenv("PTSBE_SWIZZLE_REPORT")) {   // analysis: model wavefronts, free vs TMA layout
+      auto cost = [&](const Swizzle& z) { int t = 0; for (const DevPhase& D : gp.phases) t += phase_wavefronts(z, D, GB); return t; };
+      std::fprintf(stderr, "pass %zu gb %d phases %zu wavefronts: free %d tma %d\n", pi, GB, gp.phases.size(),
+                   cost(free_sw), tma ? cost(tl.sw) : -1);
+    }
     const std::string swname = "Swz" + std::to_string(pi);
     Emitter ke(P.c64);
     std::ostringstream slow_fns;   // out-of-line slow variants of this pass's phases
@@ -467,10 +613,13 @@ inline std::string generate(const GenProgram& P) {
     std::ostringstream& k = ke.o;
     Cx F{1.0, 0.0};
     k << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << min_blocks << ") "
-      << kernel_name((int)pi) << "(const ptg::PassParams p) {\n"
+      << kernel_name((int)pi) << "(const ptg::PassParams p, const __grid_constant__ ptg::TMapDesc tm) {\n"
       << "  typedef " << ke.V << " V;\n"
       << "  ptg::run_pass<" << ke.R << ", " << gp.L << ", " << gp.c << ", " << (P.n - gp.L) << ", " << threads
-      << ", " << (pi + 1 == P.passes.size() ? "true" : "false") << ">(p, " << swname << "(),\n"
+      << ", " << (pi + 1 == P.passes.size() ? "true" : "false") << ", " << (tma ? "true" : "false") << ", " << (tma && !std::getenv("PTSBE_NO_TMA_STORE") ? "true" : "false")
+      << ", " << (std::getenv("PTSBE_TMA_LANES") ? std::atoi(std::getenv("PTSBE_TMA_LANES")) : 32)
+      << ">(p, &tm, "
+      << swname << "(), " << swname << "Inv(),\n"
       << "    " << scatter_fn(comp, "uint64_t") << ",\n"
       << "    " << scatter_fn(hmask, "uint32_t") << ",\n"
       << "    " << err_mask_fn(gp) << ",\n"
@@ -698,7 +847,8 @@ inline std::string generate(const GenProgram& P) {
     k << "  });\n}\n";
     const double mag = cxabs(F);
     G = cxmul(G, Cx{F.re / mag, F.im / mag});
-    kernels.push_back(swizzle_struct(swname, sw, gp.L) + slow_fns.str() + k.str());
+    kernels.push_back(swizzle_struct(swname, sw, gp.L) + slot_inv_struct(swname + "Inv", tl) + slow_fns.str() +
+                      k.str());
   }
   o << kGenPrelude << "\n"
     << "#define GZERO_RE " << hexd(G.re) << "\n#define GZERO_IM " << hexd(G.im) << "\n";
@@ -787,7 +937,8 @@ inline bool compile(const std::string& src, int n_passes, int dev, Module& out, 
 }
 
 inline size_t smem_bytes(int L, int /*c*/, size_t amp_bytes) {
-  return 2 * ((size_t)1 << L) * amp_bytes + 32 * 8 + 16 + 8 * kMaxHitWords;   // tiles | red | emask | hits
+  // [1024-B alignment slack for TMA's 128-B swizzle] tiles | mbarriers | red | emask | hits | TMA row table
+  return 1024 + 2 * ((size_t)1 << L) * amp_bytes + 16 + 32 * 8 + 16 + 8 * kMaxHitWords + 16 * 64;
 }
 
 }  // namespace gen

@@ -122,6 +122,10 @@ struct ptsbe_engine {
   uint64_t tsum_qmask = 0;
   int tsum_L = 0, tsum_c = 0, tsum_threads = 0;
   std::string gen_src;
+  // TMA tile staging: one 2-D tensor map over every state slot, as rows of 128 B
+  // (16 x 8-B words); the generated pass kernels gather / scatter a tile's rows with it
+  alignas(64) CUtensorMap tmap;
+  bool tmap_ok = false;
   // conventional (Algorithm 1) selection: per pass, the general-channel site that
   // opens it (outcome chosen on device from the state at the pass boundary)
   struct Decision { int site = -1, p0 = -1, p1 = -1, arity = 0, mat_base = 0, n_out = 0; };
@@ -361,7 +365,7 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero, int p_begin = 0, int p
       const long long total = (long long)E * p.tiles;
       const long long want = (long long)std::max(per_sm, 1) * h->num_sms;
       const unsigned nblk = (unsigned)std::max<long long>(1, std::min(total, want));
-      void* args[] = {&p};
+      void* args[] = {&p, &h->tmap};
       if (gen::api().launch(f, nblk, 1, 1, threads, 1, 1, (unsigned)gsm, (CUstream)h->stream, args, nullptr) !=
           CUDA_SUCCESS)
         return fail(h, PTSBE_ERR_CUDA, "cuLaunchKernel of generated pass %zu failed", pi);
@@ -749,6 +753,29 @@ int ptsbe_create(int device, int n_qubits, int dtype, int batch_cap, ptsbe_engin
     const size_t bytes = (size_t)(batch_cap + (h->tree_enabled ? 2 : 0)) * ((size_t)1 << n_qubits) * h->amp_bytes;
     e = cudaMalloc(&h->states, bytes);
     if (e != cudaSuccess) r = fail(h, PTSBE_ERR_CUDA, "cannot allocate %zu bytes of state: %s", bytes, cudaGetErrorString(e));
+  }
+  if (!r) {   // tensor map for TMA tile staging (generated kernels); optional
+    typedef CUresult (*encode_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    encode_t enc = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    const size_t bytes = (size_t)(batch_cap + (h->tree_enabled ? 2 : 0)) * ((size_t)1 << n_qubits) * h->amp_bytes;
+    const size_t rows = bytes / 128;
+    if (((size_t)1 << n_qubits) * h->amp_bytes >= 512 && rows < (1ull << 31) &&
+        cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess && enc) {
+      const cuuint64_t gdim[2] = {16, (cuuint64_t)rows};
+      const cuuint64_t gstr[1] = {128};
+      const cuuint32_t box[2] = {16, 1};   // tile::gather4 / scatter4: four 1-row boxes per instruction
+      const cuuint32_t es[2] = {1, 1};
+      h->tmap_ok = enc(&h->tmap, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, h->states, gdim, gstr, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                       std::getenv("PTSBE_TMA_L2_256") ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                       : std::getenv("PTSBE_TMA_L2_NONE") ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                                          : CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
   }
   // per-row tables: batch rows + the trunk row (index batch_cap)
   if (!r) r = dalloc(h, &h->d_weight, batch_cap + 1);
@@ -1223,6 +1250,7 @@ static gen::GenProgram gen_program(ptsbe_engine* h, const std::vector<PassHost>&
   G.kinds = kinds.data();
   G.chans = chans;
   G.site_chan = site_chan;
+  G.tma = h->host_only || h->tmap_ok;
   for (const PassHost& P : ph) {
     gen::GenPass gp;
     gp.L = P.L;

@@ -25,6 +25,8 @@ typedef long long int64_t;
 
 namespace ptg {
 
+#define PTG_MAX_HIT_WORDS 480   // = codegen.h kMaxHitWords (shared-memory room for the hit words)
+
 struct DevOp { int32_t kind, arity, b0, b1, ref, slot, k0, k1; };
 struct DevPhase { uint32_t pbits; int32_t op_begin, n_ops, pad; };
 struct DevChan { int32_t n_outcomes, mat_base, general, arity; uint64_t identity_mask; };
@@ -222,6 +224,44 @@ __device__ __forceinline__ void cp_async16(void* smem_ptr, const void* gptr) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gptr) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+
+// ---- TMA tile staging (sm_100a): the state viewed as rows of 128 B (16 x 8-B words), one
+// 2-D tensor map over every state slot; a tile's rows are gathered four at a time
+// (tile::gather4: four arbitrary row coordinates -> 512 contiguous B of shared memory,
+// 128-B swizzled) and written back with tile::scatter4.  Completion of the gathers is
+// an mbarrier transaction count; the scatters are bulk groups.
+struct __align__(64) TMapDesc { unsigned long long opaque[16]; };
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) { return (uint32_t)__cvta_generic_to_shared(ptr); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_gather4(void* dst, const TMapDesc* tm, int r0, int r1, int r2, int r3,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(smem_u32(dst)), "l"(tm), "r"(0), "r"(r0), "r"(r1),
+      "r"(r2), "r"(r3), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_scatter4(const TMapDesc* tm, int r0, int r1, int r2, int r3, const void* src) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.tile::scatter4.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];\n"
+      ::"l"(tm), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(src)) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ void st_stream(float4* p, float4 v) { __stcs(p, v); }
@@ -342,10 +382,10 @@ __device__ __forceinline__ void zerog(V (&a)[N], uint64_t base, uint32_t gb, con
 // per trajectory (and fills the hit words).  body(cur, b, sel_row, tile, base,
 // scale, red, emask, hits) runs
 // the pass's phases on one tile.
-template <typename R, int L, int C, int TLOG, int NT, bool SUMS, class Sw, class TileBase, class RowOff, class ErrMask,
-          class Body>
-__device__ __forceinline__ void run_pass(const PassParams& p, Sw swz_, TileBase tile_base, RowOff row_off,
-                                         ErrMask err_mask, Body body) {
+template <typename R, int L, int C, int TLOG, int NT, bool SUMS, bool TMA, bool TMA_ST, int TMA_LANES, class Sw,
+          class SlotInv, class TileBase, class RowOff, class ErrMask, class Body>
+__device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm, Sw swz_, SlotInv slot_inv,
+                                         TileBase tile_base, RowOff row_off, ErrMask err_mask, Body body) {
   typedef typename Cplx<R>::V V;
   typedef typename Cplx<R>::W W;
   constexpr int VPW = sizeof(W) / sizeof(V);
@@ -356,12 +396,20 @@ __device__ __forceinline__ void run_pass(const PassParams& p, Sw swz_, TileBase 
   constexpr bool FAST = THREADS >= (1 << CPR_LOG) && (NVEC % THREADS) == 0;
   constexpr int ITER = FAST ? (int)(NVEC / THREADS) : 1;
   constexpr int RSTEP = FAST ? (THREADS >> CPR_LOG) : 1;   // row stride between a thread's vectors
-  extern __shared__ __align__(16) unsigned char smem[];
+  // TMA rows: 128 B = 2^LOGU amplitudes; a tile is 2^(L - LOGU) rows, gathered in groups of 4
+  constexpr int LOGU = sizeof(V) == 8 ? 4 : 3;
+  constexpr int NGRP = TMA ? (1 << (L - LOGU)) / 4 : 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // TMA's 128-B swizzle needs 1024-B aligned tiles (the engine adds the slack)
+  unsigned char* smem = TMA ? smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) : smem_raw;
   V* buf0 = reinterpret_cast<V*>(smem);
   V* buf1 = buf0 + TL;
-  double* red = reinterpret_cast<double*>(buf1 + TL);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(buf1 + TL);   // TMA: one transaction barrier per tile buffer
+  double* red = reinterpret_cast<double*>(mbar + 2);
   uint64_t* emask_s = reinterpret_cast<uint64_t*>(red + 32);
   uint64_t* hits_s = emask_s + 2;   // per-phase hit words (codegen.h err_mask_fn)
+  // TMA: tile-relative row coordinates of each gather group (shared-memory slots 4g..4g+3)
+  uint4* rowtab = reinterpret_cast<uint4*>(hits_s + PTG_MAX_HIT_WORDS);
   int lb = -1;
   const uint32_t tid = threadIdx.x;
   const uint32_t j0 = tid & ((1u << CPR_LOG) - 1u);
@@ -400,16 +448,79 @@ __device__ __forceinline__ void run_pass(const PassParams& p, Sw swz_, TileBase 
     }
   };
 
+  // TMA path: every warp issues an equal share of the tile's gather4s (NGRP / warps, one per
+  // issuing lane, each arming the buffer's transaction barrier with its own 512 B), from a
+  // per-CTA table of tile-relative row coordinates (the same for every tile of the pass)
+  constexpr int NWARP = NT / 32;
+  constexpr int PERW = TMA ? (NGRP + NWARP - 1) / NWARP : 1;   // gather4s per warp
+  constexpr int NISSUE = TMA ? (NGRP < NWARP * PERW ? NGRP : NWARP * PERW) : 1;
+  const uint32_t lane = tid & 31u;
+  const int gi = (int)(tid >> 5) * PERW + (int)lane;            // this thread's gather group
+  const bool issuer = TMA && lane < (uint32_t)PERW && gi < NGRP;
+  auto tma_load = [&](long long tt, int k) {
+    V* dst = k ? buf1 : buf0;
+    const int e = (int)(tt >> TLOG);
+    if (e != le) {
+      le = e;
+      const int4 en = p.ent[e];
+      lsrc = (p.gen_zero || p.status[en.x] != 0) ? nullptr
+                                                  : reinterpret_cast<const V*>(p.states) + ((size_t)en.y << p.n);
+    }
+    if (!issuer) return;
+    if (TMA_ST) bulk_wait_read0();
+    if (!lsrc) {
+      mbar_arrive(&mbar[k]);
+      return;
+    }
+    mbar_arrive_tx(&mbar[k], 512u);   // 4 rows x 128 B
+    const uint64_t row0 = ((uint64_t)(lsrc - reinterpret_cast<const V*>(p.states)) +
+                           tile_base((uint64_t)(tt & ((1ll << TLOG) - 1)))) >> LOGU;
+    const uint4 r = rowtab[gi];
+    tma_gather4(dst + ((size_t)gi << (LOGU + 2)), tm, (int)(row0 + r.x), (int)(row0 + r.y), (int)(row0 + r.z),
+                (int)(row0 + r.w), &mbar[k]);
+  };
+  auto tma_store = [&](const V* src, long long slot_base_amp, uint64_t base) {
+    if (!issuer) return;
+    const uint64_t row0 = ((uint64_t)slot_base_amp + base) >> LOGU;
+    const uint4 r = rowtab[gi];
+    tma_scatter4(tm, (int)(row0 + r.x), (int)(row0 + r.y), (int)(row0 + r.z), (int)(row0 + r.w),
+                 src + ((size_t)gi << (LOGU + 2)));
+    bulk_commit();
+  };
+
   long long t = blockIdx.x;
-  if (t < total) load_tile(t, buf0);
-  cp_async_commit();
+  if (TMA) {
+    for (int g = (int)tid; g < NGRP; g += NT) {
+      uint32_t q4[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {   // tile row in shared-memory slot 4g+q: slot^-1, then its row offset
+        const uint32_t u = slot_inv((uint32_t)(4 * g + q));
+        q4[q] = (uint32_t)((((uint64_t)(u & ((1u << (C - LOGU)) - 1u)) << LOGU) | row_off(u >> (C - LOGU))) >> LOGU);
+      }
+      rowtab[g] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
+    }
+    if (tid == 0) {
+      mbar_init(&mbar[0], NISSUE);
+      mbar_init(&mbar[1], NISSUE);
+    }
+    __syncthreads();
+    if (t < total) tma_load(t, 0);
+  } else {
+    if (t < total) load_tile(t, buf0);
+    cp_async_commit();
+  }
   for (int it = 0; t < total; t += gridDim.x, ++it) {
     V* cur = (it & 1) ? buf1 : buf0;
     V* nxt = (it & 1) ? buf0 : buf1;
-    if (t + gridDim.x < total) load_tile(t + gridDim.x, nxt);
-    cp_async_commit();
-    cp_async_wait1();
-    __syncthreads();
+    if (TMA) {
+      if (t + gridDim.x < total) tma_load(t + gridDim.x, (it + 1) & 1);
+      mbar_wait(&mbar[it & 1], (uint32_t)(it >> 1) & 1u);
+    } else {
+      if (t + gridDim.x < total) load_tile(t + gridDim.x, nxt);
+      cp_async_commit();
+      cp_async_wait1();
+      __syncthreads();
+    }
     if ((int)(t >> TLOG) != ce) {
       ce = (int)(t >> TLOG);
       cen = p.ent[ce];
@@ -430,7 +541,28 @@ __device__ __forceinline__ void run_pass(const PassParams& p, Sw swz_, TileBase 
     const double scale = cscale_v;
     body(cur, b, p.sel + (size_t)b * p.S, tile, base, scale, red, emask, hits_s);
     V* st = reinterpret_cast<V*>(p.states) + ((size_t)en.z << p.n) + base;
-    if (SUMS && FAST && p.tsum) {
+    if (TMA && TMA_ST) {
+      // the phases' shared-memory writes must be visible to the async proxy before the scatter
+      fence_proxy_async();
+      __syncthreads();
+      tma_store(cur, (long long)en.z << p.n, base);
+      if (SUMS && FAST && p.tsum) {   // fused sampler block sums straight from the tile (see below)
+        constexpr int PER_THREAD = ITER * VPW;
+        constexpr int LANES = 512 / PER_THREAD;
+        uint64_t q = 0;
+#pragma unroll
+        for (int k = 0; k < ITER; ++k) {
+          const W w = *reinterpret_cast<const W*>(cur + (s0 ^ swz_((uint32_t)(k * RSTEP) << C)));
+          const V* pv = reinterpret_cast<const V*>(&w);
+#pragma unroll
+          for (int e = 0; e < VPW; ++e) q += qfix(pv[e]);
+        }
+#pragma unroll
+        for (int o = LANES / 2; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+        if ((tid & (LANES - 1)) == 0 && en.x < p.B - 1)
+          p.tsum[(size_t)en.x * p.tsum_stride + ((size_t)tile << (L - 9)) + tid / LANES] = q;
+      }
+    } else if (SUMS && FAST && p.tsum) {
       // Last pass of a unitary program: the sampler's block sums of q = qfix(a)
       // (2^-62 fixed point) are produced here, so sampling needs no separate read
       // of the states.  CDF order inside a tile is THREAD-major (thread, k, vector
@@ -468,7 +600,11 @@ __device__ __forceinline__ void run_pass(const PassParams& p, Sw swz_, TileBase 
     }
     __syncthreads();
   }
-  cp_async_wait0();
+  if (TMA && TMA_ST) {
+    if (issuer) bulk_wait0();   // the last scatters must be done with shared memory before the CTA exits
+  } else {
+    cp_async_wait0();
+  }
 }
 
 }  // namespace ptg
