@@ -4,6 +4,7 @@
 // sampler pipeline.  No torch, no Python; the Python package binds this with
 // ctypes (paper_2504_16297_b200/_native.py), which releases the GIL per call.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX3: no-ops unless a profiler injects itself
 
 #include <algorithm>
 #include <cstdarg>
@@ -25,6 +26,14 @@
 #include "nccl_api.h"
 
 using namespace ptsbe;
+
+namespace {
+// RAII NVTX range (nsys / ncu --nvtx show the engine's phases: passes, sampling, swaps)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 struct PassHost {
   uint64_t qmask;
@@ -307,6 +316,7 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero, int p_begin = 0, int p
     CKL(h);
   }
   int fork_off = 0;
+  NvtxRange nvtx_passes("ptsbe_passes");
   for (size_t pi = (size_t)p_begin; pi < (size_t)p_end; ++pi) {
     const PassHost& ph = h->passes[pi];
     const int E = ent_begin[pi + 1] - ent_begin[pi];
@@ -548,6 +558,7 @@ template <typename R>
 int sample_impl(ptsbe_engine* h, int B, const int64_t* shots, int rng_mode, const uint64_t* rng_state,
                 const uint64_t* keys, uint64_t* out_idx, uint32_t* out_cnt, int64_t* out_nuniq,
                 uint32_t flags) {
+  NvtxRange nvtx_sample("ptsbe_sample");
   std::vector<int64_t> m(B), off(B);
   if ((flags & PTSBE_DEVICE_PTRS) && (flags & PTSBE_HOST_MIRROR)) {
     if (!h->mirror_shots || h->mirror_B < B) return fail(h, PTSBE_ERR_VALIDATION, "no host mirror of the shot counts");
@@ -1315,6 +1326,7 @@ int ptsbe_run_conventional(ptsbe_engine* h, const uint8_t* sel, const double* u,
     return fail(h, PTSBE_ERR_VALIDATION,
                 "program not planned for state-dependent selection (a general site does not open its pass)");
   if (B == 0) return 0;
+  NvtxRange nvtx_conv("ptsbe_run_conventional");
   const int P = (int)h->passes.size();
   const int S = h->n_sites;
   std::vector<int> cuts;   // passes opened by a decision site
@@ -1536,6 +1548,7 @@ static int shard_swap_impl(ptsbe_engine* h, int B, const PartMap& m, const int32
     CK(h, cudaMalloc(&h->xbuf, need));
     h->xbuf_bytes = need;
   }
+  NvtxRange nvtx_swap("ptsbe_shard_swap");
   V* sendb[2] = {(V*)h->xbuf, (V*)h->xbuf + (size_t)P * CH};
   V* recvb[2] = {(V*)h->xbuf + 2ull * P * CH, (V*)h->xbuf + 3ull * P * CH};
   nccl::Api& A = nccl::api();

@@ -139,6 +139,9 @@ __global__ void __launch_bounds__(256) exact_blockmaps(SampleParams p, BlockMap*
 
 // One warp per trajectory: chain the blocks in order -> C[b][blk] = numpy's cum at the
 // block's last element (float64 bits in the u64 buffer), total[b] = cum_last.
+// Blocks go 32 at a time: when all 32 maps are valid for the binade of the running sum
+// and the group's end stays inside it, a warp scan of the maps gives every block end at
+// once (one step per 32 blocks); otherwise the group is chained block by block.
 template <typename R>
 __global__ void __launch_bounds__(32) exact_chain(SampleParams p, const BlockMap* maps, uint64_t* C) {
   using V = typename Cplx<R>::V;
@@ -150,36 +153,66 @@ __global__ void __launch_bounds__(32) exact_chain(SampleParams p, const BlockMap
   const V* st = reinterpret_cast<const V*>(p.states) + ((size_t)b << p.n);
   const BlockMap* mp = maps + (size_t)b * p.nblk;
   uint64_t* Cb = C + (size_t)b * p.nblk;
-  __shared__ BlockMap sm[32];
-  double s = 0.0;
-  for (long long blk = 0; blk < p.nblk; ++blk) {
-    if ((blk & 31) == 0) {   // stage the next 32 maps (independent loads, off the serial chain)
-      __syncwarp();
-      if (blk + lane < p.nblk) sm[lane] = mp[blk + lane];
-      __syncwarp();
+  double s = 0.0;   // running sum (identical in every lane)
+  for (long long g0 = 0; g0 < p.nblk; g0 += 32) {
+    const long long blk = g0 + lane;
+    const bool have = blk < p.nblk;
+    BlockMap m{};
+    if (have) m = mp[blk];
+    // fast path: one warp scan for the whole group
+    const int e0 = __shfl_sync(0xffffffffu, m.e, 0);
+    const bool mine_ok = !have || (m.valid && m.e == e0);
+    bool fast = __all_sync(0xffffffffu, mine_ok) && s > 0.0 && ilogb(s) == e0;
+    if (fast) {
+      ParMap pm;
+      if (have) { pm.inc0 = m.inc[0]; pm.inc1 = m.inc[1]; pm.out0 = m.out[0]; pm.out1 = m.out[1]; }
+      else { pm.inc0 = pm.inc1 = 0; pm.out0 = 0; pm.out1 = 1; }
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {   // inclusive scan: maps of lanes <= this one, in order
+        ParMap o;
+        o.inc0 = shfl_up_u64(pm.inc0, d);
+        o.inc1 = shfl_up_u64(pm.inc1, d);
+        o.out0 = __shfl_up_sync(0xffffffffu, pm.out0, d);
+        o.out1 = __shfl_up_sync(0xffffffffu, pm.out1, d);
+        if (lane >= d) pm = parmap_then(o, pm);
+      }
+      const uint64_t K = (uint64_t)ldexp(s, 52 - e0);
+      const uint64_t Kj = K + ((K & 1) ? pm.inc1 : pm.inc0);
+      const uint64_t Kend = shfl_u64(Kj, 31);
+      fast = Kend < (1ull << 53);   // the group ends inside the binade
+      if (fast) {
+        if (have) Cb[blk] = (uint64_t)__double_as_longlong(ldexp((double)Kj, e0 - 52));
+        s = ldexp((double)Kend, e0 - 52);
+      }
     }
-    int ok = 0;
-    if (lane == 0) {
-      const BlockMap m = sm[blk & 31];
-      if (m.valid && s > 0.0 && ilogb(s) == m.e) {
-        const uint64_t K = (uint64_t)ldexp(s, 52 - m.e);
-        const uint64_t Kend = K + m.inc[K & 1];
+    if (fast) continue;
+    // slow path: block by block, map when it provably applies, else sequential sums
+    const int nb = (int)min((long long)32, p.nblk - g0);
+    for (int j = 0; j < nb; ++j) {
+      const int me = __shfl_sync(0xffffffffu, m.e, j);
+      const int mv = __shfl_sync(0xffffffffu, (int)m.valid, j);
+      const uint64_t i0 = shfl_u64(m.inc[0], j), i1 = shfl_u64(m.inc[1], j);
+      int ok = 0;
+      if (mv && s > 0.0 && ilogb(s) == me) {
+        const uint64_t K = (uint64_t)ldexp(s, 52 - me);
+        const uint64_t Kend = K + ((K & 1) ? i1 : i0);
         if (Kend < (1ull << 53)) {
-          s = ldexp((double)Kend, m.e - 52);
+          s = ldexp((double)Kend, me - 52);
           ok = 1;
         }
       }
+      if (!ok) {   // the block crosses a binade (or the sum is still tiny)
+        const V* src = st + (size_t)(g0 + j) * bsz;
+        for (uint32_t t = lane; t < bsz; t += 32) pv[t] = np_abs2(src[t]);
+        __syncwarp();
+        double acc = s;
+        if (lane == 0)
+          for (uint32_t t = 0; t < bsz; ++t) acc = __dadd_rn(acc, pv[t]);
+        s = __shfl_sync(0xffffffffu, acc, 0);
+        __syncwarp();
+      }
+      if (lane == 0) Cb[g0 + j] = (uint64_t)__double_as_longlong(s);
     }
-    ok = __shfl_sync(0xffffffffu, ok, 0);
-    if (!ok) {   // sequential: the block crosses a binade (or the sum is still tiny)
-      const V* src = st + (size_t)blk * bsz;
-      for (uint32_t j = lane; j < bsz; j += 32) pv[j] = np_abs2(src[j]);
-      __syncwarp();
-      if (lane == 0)
-        for (uint32_t j = 0; j < bsz; ++j) s = __dadd_rn(s, pv[j]);
-      __syncwarp();
-    }
-    if (lane == 0) Cb[blk] = (uint64_t)__double_as_longlong(s);
   }
   if (lane == 0) p.total[b] = (uint64_t)__double_as_longlong(s);
 }
