@@ -212,6 +212,16 @@ inline Swizzle choose_swizzle(bool c64, int L, const std::vector<DevPhase>& phas
   return best;
 }
 
+// Tile buffers per CTA: two (the next tile streams in while this one computes) for 32-KB
+// tiles; ONE for 64-KB tiles (c128 L = 12, c64 L = 13), where a second buffer would leave a
+// single CTA per SM -- three single-buffered CTAs hide the load latency for each other
+// instead (PTSBE_STAGES = 1 / 2 overrides).
+inline int stages_for(int L, size_t amp_bytes) {
+  if (const char* e = std::getenv("PTSBE_STAGES")) return std::atoi(e) == 1 ? 1 : 2;
+  return ((size_t)1 << L) * amp_bytes > (48u << 10) ? 1 : 2;
+}
+inline size_t smem_bytes_for(int L, size_t amp_bytes);   // below (smem_bytes)
+
 // TMA tile staging for a pass (gen_prelude.cuh run_pass TMA): 128-B rows need the pass's
 // contiguous low run to cover a row (c64: 16 amplitudes, c128: 8) and the row table holds
 // <= 64 gather groups (256 rows).  Default: complex128 passes (config 4: 456 K vs 445 K
@@ -221,7 +231,7 @@ inline Swizzle choose_swizzle(bool c64, int L, const std::vector<DevPhase>& phas
 inline bool tma_ok(bool c64, int c, int L) {
   const char* e = std::getenv("PTSBE_TMA");
   const bool want = std::getenv("PTSBE_NO_TMA") ? false : e ? std::atoi(e) != 0 : !c64;
-  return want && c >= (c64 ? 4 : 3) && L - (c64 ? 4 : 3) <= 8;
+  return want && c >= (c64 ? 4 : 3) && L - (c64 ? 4 : 3) <= 9;   // <= 128 gather groups (row table)
 }
 
 // TMA tile staging lands each 128-B tile row u at shared-memory row slot(u) with the
@@ -592,14 +602,23 @@ inline std::string generate(const GenProgram& P) {
     int n_gates = 0;
     for (const DevOp& op : gp.ops) n_gates += op.kind == 0;
     static const int mb128 = std::getenv("PTSBE_GB5_MB") ? std::atoi(std::getenv("PTSBE_GB5_MB")) : 3;
-    const int min_blocks = threads <= 128 ? mb128 : (threads <= 256 ? (n_gates >= 40 ? 3 : 2) : 1);
+    // complex128 256-thread passes: 2 CTAs/SM at <= 128 registers (16 amplitudes = 64 registers
+    // per thread; a 3-CTA budget of 85 spills 50-200 B per thread: config 4 558 K vs 566 K)
+    int min_blocks = threads <= 128 ? mb128 : (threads <= 256 ? (!P.c64 ? 2 : (n_gates >= 40 ? 3 : 2)) : 1);
+    {   // never budget registers for more CTAs than the tile buffers let share an SM
+      const int by_smem = std::max(1, (int)((227u << 10) / smem_bytes_for(gp.L, P.c64 ? 8 : 16)));
+      min_blocks = std::min(min_blocks, by_smem);
+      if (const char* e = std::getenv("PTSBE_MIN_BLOCKS")) min_blocks = std::max(1, std::atoi(e));   // A/B knob
+    }
     const uint64_t nmask = P.n >= 64 ? ~0ull : ((1ull << P.n) - 1);
     const uint64_t comp = ~gp.qmask & nmask;
     const uint64_t hmask = gp.qmask & ~((1ull << gp.c) - 1);
     const Swizzle free_sw = std::getenv("PTSBE_FIXED_SWIZZLE") ? Swizzle::fixed(P.c64)   // A/B knob
                                                                : choose_swizzle(P.c64, gp.L, gp.phases, GB);
     TmaLayout tl;
-    const bool tma = P.tma && tma_ok(P.c64, gp.c, gp.L) && make_tma_layout(P.c64, gp.L, gp.phases, GB, free_sw, &tl);
+    const bool tma = P.tma && tma_ok(P.c64, gp.c, gp.L) &&
+                     (1 << (gp.L - (P.c64 ? 4 : 3))) / 4 <= threads &&   // one gather group per issuing lane
+                     make_tma_layout(P.c64, gp.L, gp.phases, GB, free_sw, &tl);
     const Swizzle sw = tma ? tl.sw : free_sw;
     if (std::getenv("PTSBE_SWIZZLE_REPORT")) {   // analysis: model wavefronts, free vs TMA layout
       auto cost = [&](const Swizzle& z) { int t = 0; for (const DevPhase& D : gp.phases) t += phase_wavefronts(z, D, GB); return t; };
@@ -618,7 +637,7 @@ inline std::string generate(const GenProgram& P) {
       << "  ptg::run_pass<" << ke.R << ", " << gp.L << ", " << gp.c << ", " << (P.n - gp.L) << ", " << threads
       << ", " << (pi + 1 == P.passes.size() ? "true" : "false") << ", " << (tma ? "true" : "false") << ", " << (tma && !std::getenv("PTSBE_NO_TMA_STORE") ? "true" : "false")
       << ", " << (std::getenv("PTSBE_TMA_LANES") ? std::atoi(std::getenv("PTSBE_TMA_LANES")) : 32)
-      << ">(p, &tm, "
+      << ", " << stages_for(gp.L, P.c64 ? 8 : 16) << ">(p, &tm, "
       << swname << "(), " << swname << "Inv(),\n"
       << "    " << scatter_fn(comp, "uint64_t") << ",\n"
       << "    " << scatter_fn(hmask, "uint32_t") << ",\n"
@@ -936,10 +955,12 @@ inline bool compile(const std::string& src, int n_passes, int dev, Module& out, 
   return true;
 }
 
-inline size_t smem_bytes(int L, int /*c*/, size_t amp_bytes) {
+inline size_t smem_bytes_for(int L, size_t amp_bytes) {
   // [1024-B alignment slack for TMA's 128-B swizzle] tiles | mbarriers | red | emask | hits | TMA row table
-  return 1024 + 2 * ((size_t)1 << L) * amp_bytes + 16 + 32 * 8 + 16 + 8 * kMaxHitWords + 16 * 64;
+  return 1024 + (size_t)stages_for(L, amp_bytes) * ((size_t)1 << L) * amp_bytes + 16 + 32 * 8 + 16 +
+         8 * kMaxHitWords + 16 * 128;
 }
+inline size_t smem_bytes(int L, int /*c*/, size_t amp_bytes) { return smem_bytes_for(L, amp_bytes); }
 
 }  // namespace gen
 }  // namespace ptsbe

@@ -382,8 +382,8 @@ __device__ __forceinline__ void zerog(V (&a)[N], uint64_t base, uint32_t gb, con
 // per trajectory (and fills the hit words).  body(cur, b, sel_row, tile, base,
 // scale, red, emask, hits) runs
 // the pass's phases on one tile.
-template <typename R, int L, int C, int TLOG, int NT, bool SUMS, bool TMA, bool TMA_ST, int TMA_LANES, class Sw,
-          class SlotInv, class TileBase, class RowOff, class ErrMask, class Body>
+template <typename R, int L, int C, int TLOG, int NT, bool SUMS, bool TMA, bool TMA_ST, int TMA_LANES, int STAGES,
+          class Sw, class SlotInv, class TileBase, class RowOff, class ErrMask, class Body>
 __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm, Sw swz_, SlotInv slot_inv,
                                          TileBase tile_base, RowOff row_off, ErrMask err_mask, Body body) {
   typedef typename Cplx<R>::V V;
@@ -403,7 +403,7 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
   // TMA's 128-B swizzle needs 1024-B aligned tiles (the engine adds the slack)
   unsigned char* smem = TMA ? smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) : smem_raw;
   V* buf0 = reinterpret_cast<V*>(smem);
-  V* buf1 = buf0 + TL;
+  V* buf1 = STAGES == 2 ? buf0 + TL : buf0;   // one buffer: tiles load after the previous one is stored
   uint64_t* mbar = reinterpret_cast<uint64_t*>(buf1 + TL);   // TMA: one transaction barrier per tile buffer
   double* red = reinterpret_cast<double*>(mbar + 2);
   uint64_t* emask_s = reinterpret_cast<uint64_t*>(red + 32);
@@ -454,6 +454,7 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
   constexpr int NWARP = NT / 32;
   constexpr int PERW = TMA ? (NGRP + NWARP - 1) / NWARP : 1;   // gather4s per warp
   constexpr int NISSUE = TMA ? (NGRP < NWARP * PERW ? NGRP : NWARP * PERW) : 1;
+  static_assert(PERW <= 32, "TMA: more gather groups per warp than lanes");
   const uint32_t lane = tid & 31u;
   const int gi = (int)(tid >> 5) * PERW + (int)lane;            // this thread's gather group
   const bool issuer = TMA && lane < (uint32_t)PERW && gi < NGRP;
@@ -489,7 +490,19 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
   };
 
   long long t = blockIdx.x;
-  if (TMA) {
+  if (TMA && STAGES == 1) {   // single buffer: loads issued at the top of each iteration
+    for (int g = (int)tid; g < NGRP; g += NT) {
+      uint32_t q4[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t u = slot_inv((uint32_t)(4 * g + q));
+        q4[q] = (uint32_t)((((uint64_t)(u & ((1u << (C - LOGU)) - 1u)) << LOGU) | row_off(u >> (C - LOGU))) >> LOGU);
+      }
+      rowtab[g] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
+    }
+    if (tid == 0) mbar_init(&mbar[0], NISSUE);
+    __syncthreads();
+  } else if (TMA) {
     for (int g = (int)tid; g < NGRP; g += NT) {
       uint32_t q4[4];
 #pragma unroll
@@ -505,14 +518,24 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
     }
     __syncthreads();
     if (t < total) tma_load(t, 0);
-  } else {
+  } else if (STAGES == 2) {
     if (t < total) load_tile(t, buf0);
     cp_async_commit();
   }
   for (int it = 0; t < total; t += gridDim.x, ++it) {
     V* cur = (it & 1) ? buf1 : buf0;
     V* nxt = (it & 1) ? buf0 : buf1;
-    if (TMA) {
+    if (STAGES == 1) {
+      if (TMA) {
+        tma_load(t, 0);
+        mbar_wait(&mbar[0], (uint32_t)it & 1u);
+      } else {
+        load_tile(t, buf0);
+        cp_async_commit();
+        cp_async_wait0();
+        __syncthreads();
+      }
+    } else if (TMA) {
       if (t + gridDim.x < total) tma_load(t + gridDim.x, (it + 1) & 1);
       mbar_wait(&mbar[it & 1], (uint32_t)(it >> 1) & 1u);
     } else {

@@ -36,7 +36,9 @@ from .errors import ValidationError
 KIND_GATE = 0
 KIND_SITE = 1
 
-DEFAULT_TILE_BITS = {"c64": 12, "c128": 11}
+# 32-KB tiles for complex64; 64-KB single-buffered tiles for complex128 (config 4: 12 passes
+# instead of 17 at 11 bits -- 566 K vs 473 K shots/s on one B200)
+DEFAULT_TILE_BITS = {"c64": 12, "c128": 12}
 DEFAULT_LOW_BITS = {"c64": 4, "c128": 3}     # 16 x 8 B / 8 x 16 B = 128-B rows
 
 

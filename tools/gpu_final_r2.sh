@@ -13,7 +13,7 @@ timeout 900 python bench.py --impl reference --steps 4 --warmup 1 > gpurun_out/b
 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533 \
   bench.py --gpus 1 --steps 2 --warmup 3 --no-cpu > gpurun_out/bench_torchrun_$tag.log 2>&1; echo "torchrun rc=$?" >> gpurun_out/bench_torchrun_$tag.log
 bash tools/gpu_prof_r2.sh $tag
-heavy=${HEAVY:-14}
+heavy=${HEAVY:-7}
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ptsbe_pass_${heavy}\$" -s 3 -c 1 -o /tmp/full_$tag -f \
   python bench.py --steps 1 --warmup 3 --no-cpu --dtype c128 --secondary none > gpurun_out/ncu_full_$tag.log 2>&1
 ncu -i /tmp/full_$tag.ncu-rep --page raw --csv > gpurun_out/ncu_full_raw_$tag.csv 2>/dev/null

@@ -4,7 +4,13 @@ mkdir -p gpurun_out
 tag=${1:-r}
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_$tag.log 2>&1
 for d in c128 c64; do
-  if [ $d = c128 ]; then np=17; else np=12; fi
+  np=$(python -c "
+import sys; sys.path.insert(0, '.')
+import paper_2504_16297_b200 as P
+from paper_2504_16297_b200 import workloads
+from paper_2504_16297_b200.program import compile_circuit
+c = workloads.build(4, P.parse_circuit, P.parse_noise_model, P.attach_noise)
+print(compile_circuit(c, '$d').n_passes)")
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1000 --csv \
     --log-file gpurun_out/launches_${d}_$tag.csv python bench.py --steps 2 --warmup 3 --no-cpu --dtype $d --secondary none \
     > gpurun_out/ncu_launch_${d}_$tag.log 2>&1
