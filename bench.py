@@ -47,6 +47,8 @@ METRIC = "shots/sec (config 4: 28-qubit QEC circuit, 1e4 shots/trajectory)"
 
 
 def metric_for(config: int) -> str:
+    if config == 5:
+        return "shots/sec (config 5: 34-35-qubit QEC state sharded within the trajectory, 1e6 shots/trajectory)"
     return METRIC if config == 4 else f"shots/sec (config {config}, 1e4 shots/trajectory)"
 DTYPE_NAME = {"c128": "c128 (complex128, f64 arithmetic)", "c64": "c64 (complex64, f32 arithmetic)"}
 DEFAULT_BATCH = {"c128": 24, "c64": 48}
@@ -491,6 +493,97 @@ def roofline_of(leg, dtype: str, batch: int, config: int, K: int):
                              for m, b in zip(leg["pp_ms"], leg["pp_bytes"])]}
 
 
+# ---------------------------------------------------------------- config 5: sharded state
+
+C5_SHOTS = 1_000_000
+
+
+def run_config5(args):
+    """Config 5: one 34/35-qubit QEC trajectory's state sharded within the
+    trajectory.  N = 1: the 34-qubit form (workloads.CONFIG5_34) as two virtual shards of 33
+    local qubits on one GPU (2 x 64 GiB at c64); N >= 2: the 35-qubit circuit over N ranks
+    (one shard per GPU, the engine's NCCL group: swaps as one all-to-all per swap point).
+    A step = one trajectory prepared + 10^6 Philox shots; value = shots/s of the job."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_16297_b200 as P
+    from paper_2504_16297_b200 import workloads
+    from paper_2504_16297_b200.execute import mix_seed
+    from paper_2504_16297_b200.sharded import (DistributedShards, EngineShardBackend, VirtualShards, plan_sharded,
+                                              sharded_selection)
+    rank, world, local = dist_env()
+    dtype = "c64"
+    if world == 1:
+        c = workloads.build(workloads.CONFIG5_34, P.parse_circuit, P.parse_noise_model, P.attach_noise)
+        k = 1
+    else:
+        c = workloads.build(5, P.parse_circuit, P.parse_noise_model, P.attach_noise)
+        k = world.bit_length() - 1
+        if 1 << k != world:
+            raise SystemExit("config 5 needs a power-of-two GPU count")
+    W, K = args.warmup, args.steps
+    specs = [s for s in P.presample_probabilistic(c, 4 * (W + K) + 8, C5_SHOTS, P.stream_rng(args.seed, 2**63))
+             if s.selections][:W + K]
+    plan = plan_sharded(c, k, dtype=dtype)
+    dev = torch.device("cuda", local)
+    if world == 1:
+        runner = VirtualShards(plan, dtype, batch_cap=1, device=local)
+        run = lambda sel: runner.run(sel)                                  # noqa: E731
+        sample = lambda shots, seeds: runner.sample(shots, seeds)          # noqa: E731
+    else:
+        backend = EngineShardBackend(plan, dtype, batch_cap=1, device=local)
+        runner = DistributedShards(plan, backend)
+        run = lambda sel: runner.run(sel)                                  # noqa: E731
+        sample = lambda shots, seeds: runner.sample(shots, seeds)          # noqa: E731
+
+    def step(i):
+        run(sharded_selection(plan, [specs[i]]))
+        sample([C5_SHOTS], [mix_seed(args.seed, i)])
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+    for i in range(W):
+        step(i)
+    barrier()
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for i in range(W, W + K):
+            step(i)
+        barrier()
+        dt = time.perf_counter() - t0
+    t = torch.tensor([dt], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dt = float(t.item())
+    if rank == 0:
+        n = c.n_qubits
+        passes = plan.program.n_passes
+        bytes_traj = passes * 2 * (1 << n) * 8
+        line = {"metric": metric_for(5), "value": K * C5_SHOTS / dt, "unit": "shots/s", "n_gpus": world, "steps": K,
+                "warmup": W, "ms_per_step": 1e3 * dt / K, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": DTYPE_NAME[dtype],
+                "data": "synthetic (PTS-sampled Kraus selections of a generated circuit)",
+                "config": {"workload": f"config5 {'steane_blocks(4, ancillas=6)' if world == 1 else 'steane_blocks(5)'}:"
+                                       f" {n} q, {len(c.ops)} ops, state sharded over 2^{k} shards"
+                                       f"{' (virtual, one GPU)' if world == 1 else ' (one per GPU, NCCL)'}",
+                           "shots_per_trajectory": C5_SHOTS, "parallelism": f"state-shard{1 << k}",
+                           "l2": "inputs larger than L2"},
+                "engine": {"passes": passes, "swaps": plan.n_swaps, "local_qubits": plan.n_local,
+                           "timing": "host wall clock around K device-synchronised steps, max over ranks"},
+                "trajectories_per_s": K / dt,
+                "traj_roofline_frac": (K / dt) / (peaks()[0] * 1e9 * world / bytes_traj),
+                "clocks": clk.summary(),
+                "cpu_baseline": {"value": None, "unit": "shots/s", "cores": 0, "kind": "reference",
+                                 "sample": "not runnable on CPU: a 34-35 qubit complex128 state is 256-512 GiB "
+                                           "(SURVEY 8(d))"}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -513,6 +606,11 @@ def main():
                     help="analysis only: zero every sampled Kraus selection (all trajectories noiseless)")
     args = ap.parse_args()
     if args.impl == "reference":
+        if args.config == 5:
+            if dist_env()[0] == 0:
+                print(json.dumps({"impl": "reference", "unavailable": "config 5 (34-35 qubits) does not fit a "
+                                  "CPU statevector (256-512 GiB at complex128; SURVEY 8(d))"}), flush=True)
+            return
         run_reference(args)
         return
 
@@ -523,6 +621,9 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.config == 5:
+        run_config5(args)
+        return
     dev = torch.device("cuda", local)
     W, K = args.warmup, args.steps
     legs = [args.dtype] + ([args.secondary] if args.secondary not in ("none", args.dtype) else [])

@@ -80,9 +80,52 @@ def _next_use(stream, start, q):
     return len(stream) + 1
 
 
+def _segment_pass_counter(segments_ops, stream, nl, L, c):
+    """Total passes of all segments under a local-bit relabelling sigma (native planner, no
+    per-segment layout search): the objective of plan_sharded's layout search."""
+    import ctypes as C
+
+    from . import _native as N
+    lib = N.load_library()
+    segs = []
+    for ops, mapping in segments_ops:
+        if not ops:
+            continue
+        t0 = np.array([mapping[stream[i].targets[0]][1] for i in ops], dtype=np.int64)
+        t1 = np.array([mapping[stream[i].targets[1]][1] if len(stream[i].targets) > 1 else -1 for i in ops],
+                      dtype=np.int64)
+        gen = np.array([(1 if stream[i].general else 0) | (2 if stream[i].kind == 0 else 0) for i in ops],
+                       dtype=np.uint8)
+        segs.append((t0, t1, gen))
+    out_pass = np.zeros(max((len(t0) for t0, _, _ in segs), default=1) + 1, dtype=np.int32)
+    out_masks = np.zeros(out_pass.size + 1, dtype=np.uint64)
+    ptr = lambda a: C.c_void_p(a.ctypes.data)  # noqa: E731
+
+    def count(sigma: np.ndarray) -> int:
+        tot = 0
+        for t0, t1, gen in segs:
+            masks = (np.uint64(1) << sigma[t0].astype(np.uint64))
+            has1 = t1 >= 0
+            masks[has1] |= np.uint64(1) << sigma[t1[has1]].astype(np.uint64)
+            perm = np.arange(nl, dtype=np.int32)
+            P = lib.ptsbe_plan(nl, t0.size, ptr(masks), ptr(gen), L, c, 0, 0, ptr(perm), ptr(out_pass),
+                               ptr(out_masks), out_masks.size)
+            if P < 0:
+                return 1 << 30
+            tot += P
+        return tot
+    return count
+
+
 def plan_sharded(circuit, k: int, dtype: str = "c64", tile_bits: int | None = None,
-                 low_bits: int | None = None) -> ShardPlan:
-    """Segments of local-only ops with global<->local swaps between them."""
+                 low_bits: int | None = None, search_iters: int | None = None, seed: int = 0) -> ShardPlan:
+    """Segments of local-only ops with global<->local swaps between them.
+
+    The segmentation (which ops run between which swaps) depends only on which qubits are
+    global; the local BIT each local qubit occupies is free.  A local search over that
+    labelling (random transpositions, sideways moves accepted -- the unsharded planner's
+    layout search, with the summed pass count of every segment as its objective) cuts
+    config 5's passes from 29 to about half."""
     from .program import DEFAULT_LOW_BITS, DEFAULT_TILE_BITS
     n = circuit.n_qubits
     if not 1 <= k < n - 2:
@@ -118,6 +161,26 @@ def plan_sharded(circuit, k: int, dtype: str = "c64", tile_bits: int | None = No
     # one program over the local qubits: segments' passes back to back
     L = tile_bits if tile_bits is not None else DEFAULT_TILE_BITS[dtype]
     c = low_bits if low_bits is not None else DEFAULT_LOW_BITS[dtype]
+    iters = (2000 if nl > L else 0) if search_iters is None else search_iters
+    sigma = np.arange(nl, dtype=np.int64)           # local label -> physical local bit
+    if iters > 0:
+        count = _segment_pass_counter(segments_ops, stream, nl, min(L, nl), min(c, L, nl))
+        best = count(sigma)
+        rng = np.random.Generator(np.random.PCG64(seed))
+        for _ in range(iters):
+            a, b = rng.integers(0, nl, size=2)
+            if a == b:
+                continue
+            cand = sigma.copy()
+            cand[a], cand[b] = cand[b], cand[a]
+            p = count(cand)
+            if p <= best:
+                best, sigma = p, cand
+    relabel = lambda m: {q: (kind, int(sigma[bit]) if kind == "L" else bit) for q, (kind, bit) in m.items()}  # noqa: E731
+    segments_ops = [(ops, relabel(mapping)) for ops, mapping in segments_ops]
+    where = relabel(where)
+    initial = relabel(initial)
+    swaps = [[(g, int(sigma[l])) for g, l in sw] for sw in swaps]
     new_stream, passes, ranges = [], [], []
     for ops, mapping in segments_ops:
         seg_stream = [replace(stream[i], targets=tuple(mapping[q][1] for q in stream[i].targets)) for i in ops]
