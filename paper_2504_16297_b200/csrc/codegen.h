@@ -637,7 +637,8 @@ inline std::string generate(const GenProgram& P) {
       << "  ptg::run_pass<" << ke.R << ", " << gp.L << ", " << gp.c << ", " << (P.n - gp.L) << ", " << threads
       << ", " << (pi + 1 == P.passes.size() ? "true" : "false") << ", " << (tma ? "true" : "false") << ", " << (tma && !std::getenv("PTSBE_NO_TMA_STORE") ? "true" : "false")
       << ", " << (std::getenv("PTSBE_TMA_LANES") ? std::atoi(std::getenv("PTSBE_TMA_LANES")) : 32)
-      << ", " << stages_for(gp.L, P.c64 ? 8 : 16) << ">(p, &tm, "
+      << ", " << stages_for(gp.L, P.c64 ? 8 : 16) << ", " << (std::getenv("PTSBE_TMA_PREFETCH") ? "true" : "false")
+      << ">(p, &tm, "
       << swname << "(), " << swname << "Inv(),\n"
       << "    " << scatter_fn(comp, "uint64_t") << ",\n"
       << "    " << scatter_fn(hmask, "uint32_t") << ",\n"

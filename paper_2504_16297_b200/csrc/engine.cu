@@ -165,6 +165,7 @@ struct ptsbe_engine {
   int mirror_B = 0;
   int pending_pass = -1;          // PTSBE_DEFER_NORMS: pass whose slot norms await the global sums
   int pending_ent = 0, pending_E = 0;
+  void* scratch_state = nullptr;  // one state's worth of scratch for relayouts (allocated on first use)
   std::string err;
 };
 
@@ -440,26 +441,69 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero, int p_begin = 0, int p
   return 0;
 }
 
+// Persistent one-state scratch (a per-call cudaMallocAsync of a multi-GiB buffer remaps it
+// every time: it dominated verification-mode sampling of permuted layouts).
+void* state_scratch(ptsbe_engine* h) {
+  if (!h->scratch_state && cudaMalloc(&h->scratch_state, ((size_t)1 << h->n) * h->amp_bytes) != cudaSuccess) {
+    h->scratch_state = nullptr;
+    cudaGetLastError();
+  }
+  return h->scratch_state;
+}
+
+// out = in with its index bits permuted by P (out bit q <- in bit P.src[q]): the tiled
+// kernel (row-contiguous reads and writes) when the state has >= 2^8 amplitudes.
+template <typename V>
+int permute_into(ptsbe_engine* h, const V* in, V* out, const BitPerm& P) {
+  const int n = h->n;
+  const int R = sizeof(V) == 8 ? 4 : 3;   // 128-B rows
+  if (n < 8) {
+    const unsigned g = (unsigned)std::min<size_t>(((size_t)1 << n) / 256 + 1, 8192);
+    permute_state<V><<<g, 256, 0, h->stream>>>(in, out, n, P);
+    CKL(h);
+    return 0;
+  }
+  TilePerm T{};
+  T.k = std::min(n, 10);
+  uint64_t qin = (1ull << R) - 1;
+  for (int q = 0; q < R; ++q) qin |= 1ull << P.src[q];
+  for (int b = 0; b < n && __builtin_popcountll(qin) < T.k; ++b) qin |= 1ull << b;
+  T.k = __builtin_popcountll(qin);
+  uint64_t qout = 0;
+  for (int q = 0; q < n; ++q)
+    if ((qin >> P.src[q]) & 1) qout |= 1ull << q;
+  T.qin = qin;
+  T.qout = qout;
+  // output-tile bit b is output bit qb (b-th set bit of qout); it comes from input bit P.src[qb],
+  // which is input-tile bit (rank of P.src[qb] among qin's set bits)
+  for (int b = 0, qb = -1; b < T.k; ++b) {
+    do { ++qb; } while (!((qout >> qb) & 1));
+    const int ib = P.src[qb];
+    T.fmap[b] = (int8_t)__builtin_popcountll(qin & ((1ull << ib) - 1));
+  }
+  const unsigned g = (unsigned)std::min<uint64_t>(1ull << (n - T.k), 8u * (unsigned)h->num_sms);
+  const size_t smem = ((size_t)1 << T.k) * (sizeof(V) + 8 + 8 + 2);   // tile | offin | offout | emap
+  permute_tiled<V><<<g, 256, smem, h->stream>>>(in, out, n, P, T);
+  CKL(h);
+  return 0;
+}
+
 // Re-store state b in logical (to_logical) or physical order.
 int relayout(ptsbe_engine* h, int b, bool to_logical) {
   if (!h->permuted || (h->logical[b] != 0) == to_logical) return 0;
   h->tsum_ok = false;
   const size_t bytes = ((size_t)1 << h->n) * h->amp_bytes;
   char* st = (char*)h->states + (size_t)b * bytes;
-  void* scratch = nullptr;
-  CK(h, cudaMallocAsync(&scratch, bytes, h->stream));
+  void* scratch = state_scratch(h);
+  if (!scratch) return fail(h, PTSBE_ERR_CUDA, "cannot allocate %zu bytes of relayout scratch", bytes);
   BitPerm P = h->layout;            // physical -> logical
   if (!to_logical) {                 // logical -> physical
     for (int q = 0; q < h->n; ++q) P.src[h->layout.src[q]] = (int8_t)q;
   }
-  const unsigned g = (unsigned)std::min<size_t>(((size_t)1 << h->n) / 256 + 1, 8192);
-  if (h->dtype == PTSBE_C64)
-    permute_state<float2><<<g, 256, 0, h->stream>>>((const float2*)st, (float2*)scratch, h->n, P);
-  else
-    permute_state<double2><<<g, 256, 0, h->stream>>>((const double2*)st, (double2*)scratch, h->n, P);
-  CKL(h);
+  if (int r = h->dtype == PTSBE_C64 ? permute_into<float2>(h, (const float2*)st, (float2*)scratch, P)
+                                    : permute_into<double2>(h, (const double2*)st, (double2*)scratch, P))
+    return r;
   CK(h, cudaMemcpyAsync(st, scratch, bytes, cudaMemcpyDeviceToDevice, h->stream));
-  CK(h, cudaFreeAsync(scratch, h->stream));
   h->logical[b] = to_logical ? 1 : 0;
   return 0;
 }
@@ -850,7 +894,7 @@ int ptsbe_destroy(ptsbe_engine* h) {
                   h->d_phases, h->d_matkind,
                   h->d_chans, h->d_site_chan, h->d_slot_site, h->d_partials, h->d_bs, h->d_total, h->d_off,
                   h->d_m, h->d_nuniq, h->d_uoff, h->d_rng, h->d_keys, h->d_tmp, h->d_idx, h->d_runidx,
-                  h->d_runcnt, h->d_chunks, h->d_ent, h->d_forks, h->d_mats64, h->d_u, h->d_rdm, h->d_maps, h->xbuf, h->d_slotsum};
+                  h->d_runcnt, h->d_chunks, h->d_ent, h->d_forks, h->d_mats64, h->d_u, h->d_rdm, h->d_maps, h->xbuf, h->d_slotsum, h->scratch_state};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
@@ -1782,17 +1826,15 @@ int ptsbe_get_state(ptsbe_engine* h, int b, void* buf, uint32_t flags) {
   const char* src = (char*)h->states + (size_t)b * bytes;
   void* scratch = nullptr;
   if (h->permuted && !h->logical[b]) {   // logical order for the caller
-    CK(h, cudaMallocAsync(&scratch, bytes, h->stream));
-    const unsigned g = (unsigned)std::min<size_t>(((size_t)1 << h->n) / 256 + 1, 8192);
-    if (h->dtype == PTSBE_C64)
-      permute_state<float2><<<g, 256, 0, h->stream>>>((const float2*)src, (float2*)scratch, h->n, h->layout);
-    else
-      permute_state<double2><<<g, 256, 0, h->stream>>>((const double2*)src, (double2*)scratch, h->n, h->layout);
-    CKL(h);
+    scratch = state_scratch(h);
+    if (!scratch) return fail(h, PTSBE_ERR_CUDA, "cannot allocate %zu bytes of relayout scratch", bytes);
+    if (int r = h->dtype == PTSBE_C64
+                    ? permute_into<float2>(h, (const float2*)src, (float2*)scratch, h->layout)
+                    : permute_into<double2>(h, (const double2*)src, (double2*)scratch, h->layout))
+      return r;
     src = (const char*)scratch;
   }
   int e = copy_out(h, buf, src, bytes, flags);
-  if (scratch) cudaFreeAsync(scratch, h->stream);
   if (e) return e;
   CK(h, cudaStreamSynchronize(h->stream));
   return 0;
@@ -1806,19 +1848,15 @@ int ptsbe_set_state(ptsbe_engine* h, int b, const void* buf, uint32_t flags) {
   char* dst = (char*)h->states + (size_t)b * bytes;
   h->logical[b] = 0;
   if (h->permuted) {   // caller gives logical order; store physical
-    void* scratch = nullptr;
-    CK(h, cudaMallocAsync(&scratch, bytes, h->stream));
+    void* scratch = state_scratch(h);
+    if (!scratch) return fail(h, PTSBE_ERR_CUDA, "cannot allocate %zu bytes of relayout scratch", bytes);
     if (int e = copy_in(h, scratch, buf, bytes, flags)) return e;
     BitPerm fwd;     // physical bit perm[q] <- logical bit q
     fwd.n = h->n;
     for (int q = 0; q < h->n; ++q) fwd.src[h->layout.src[q]] = (int8_t)q;
-    const unsigned g = (unsigned)std::min<size_t>(((size_t)1 << h->n) / 256 + 1, 8192);
-    if (h->dtype == PTSBE_C64)
-      permute_state<float2><<<g, 256, 0, h->stream>>>((const float2*)scratch, (float2*)dst, h->n, fwd);
-    else
-      permute_state<double2><<<g, 256, 0, h->stream>>>((const double2*)scratch, (double2*)dst, h->n, fwd);
-    CKL(h);
-    cudaFreeAsync(scratch, h->stream);
+    if (int r = h->dtype == PTSBE_C64 ? permute_into<float2>(h, (const float2*)scratch, (float2*)dst, fwd)
+                                      : permute_into<double2>(h, (const double2*)scratch, (double2*)dst, fwd))
+      return r;
   } else if (int e = copy_in(h, dst, buf, bytes, flags)) {
     return e;
   }

@@ -258,6 +258,10 @@ __device__ __forceinline__ void tma_scatter4(const TMapDesc* tm, int r0, int r1,
       "cp.async.bulk.tensor.2d.global.shared::cta.tile::scatter4.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];\n"
       ::"l"(tm), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(src)) : "memory");
 }
+__device__ __forceinline__ void tma_prefetch4(const TMapDesc* tm, int r0, int r1, int r2, int r3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile::gather4 [%0, {%1, %2, %3, %4, %5}];\n"
+               ::"l"(tm), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3) : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
@@ -383,7 +387,7 @@ __device__ __forceinline__ void zerog(V (&a)[N], uint64_t base, uint32_t gb, con
 // scale, red, emask, hits) runs
 // the pass's phases on one tile.
 template <typename R, int L, int C, int TLOG, int NT, bool SUMS, bool TMA, bool TMA_ST, int TMA_LANES, int STAGES,
-          class Sw, class SlotInv, class TileBase, class RowOff, class ErrMask, class Body>
+          bool TMA_PF, class Sw, class SlotInv, class TileBase, class RowOff, class ErrMask, class Body>
 __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm, Sw swz_, SlotInv slot_inv,
                                          TileBase tile_base, RowOff row_off, ErrMask err_mask, Body body) {
   typedef typename Cplx<R>::V V;
@@ -480,6 +484,16 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
     tma_gather4(dst + ((size_t)gi << (LOGU + 2)), tm, (int)(row0 + r.x), (int)(row0 + r.y), (int)(row0 + r.z),
                 (int)(row0 + r.w), &mbar[k]);
   };
+  // single buffer: the tile after this one is prefetched into L2 while this one computes, so
+  // its gather (issued once this tile is stored) is served from L2 instead of HBM latency
+  auto tma_prefetch = [&](long long tt) {
+    if (!issuer) return;
+    const int4 en = p.ent[(int)(tt >> TLOG)];
+    if (p.gen_zero || p.status[en.x] != 0) return;
+    const uint64_t row0 = (((uint64_t)en.y << p.n) + tile_base((uint64_t)(tt & ((1ll << TLOG) - 1)))) >> LOGU;
+    const uint4 r = rowtab[gi];
+    tma_prefetch4(tm, (int)(row0 + r.x), (int)(row0 + r.y), (int)(row0 + r.z), (int)(row0 + r.w));
+  };
   auto tma_store = [&](const V* src, long long slot_base_amp, uint64_t base) {
     if (!issuer) return;
     const uint64_t row0 = ((uint64_t)slot_base_amp + base) >> LOGU;
@@ -529,6 +543,7 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
       if (TMA) {
         tma_load(t, 0);
         mbar_wait(&mbar[0], (uint32_t)it & 1u);
+        if (TMA_PF && t + gridDim.x < total) tma_prefetch(t + gridDim.x);
       } else {
         load_tile(t, buf0);
         cp_async_commit();

@@ -462,6 +462,62 @@ __global__ void __launch_bounds__(256) permute_state(const V* in, V* out, int n,
   }
 }
 
+// The same bit permutation, tiled so that reads AND writes move whole 128-B rows: a CTA
+// handles tiles of 2^K amplitudes spanning the input bits Qin (input bits 0..R-1 plus the
+// input bits that feed output bits 0..R-1, padded with low bits), loads them row-contiguous
+// into shared memory and writes them out row-contiguous in output order.  Element f of the
+// output tile takes element e = sum_b bit_b(f) << fmap[b] of the input tile.
+struct TilePerm {
+  uint64_t qin, qout;   // tile bits on the input / output side
+  int8_t fmap[16];      // output-tile bit b <- input-tile bit fmap[b]
+  int k;                // tile bits
+};
+
+__device__ __forceinline__ uint64_t pdep_loop(uint64_t src, uint64_t mask) {
+  uint64_t out = 0;
+  while (mask) {
+    const uint64_t low = mask & (~mask + 1);
+    if (src & 1) out |= low;
+    src >>= 1;
+    mask ^= low;
+  }
+  return out;
+}
+
+template <typename V>
+__global__ void __launch_bounds__(256) permute_tiled(const V* in, V* out, int n, BitPerm P, TilePerm T) {
+  extern __shared__ __align__(16) unsigned char psm[];
+  const uint32_t K = 1u << T.k;
+  V* tile = reinterpret_cast<V*>(psm);
+  uint64_t* offin = reinterpret_cast<uint64_t*>(tile + K);    // pdep(e, qin)
+  uint64_t* offout = offin + K;                                 // pdep(f, qout)
+  uint16_t* emap = reinterpret_cast<uint16_t*>(offout + K);    // input-tile element of output element f
+  __shared__ uint64_t base_s[2];
+  for (uint32_t e = threadIdx.x; e < K; e += blockDim.x) {       // per-CTA tables, once
+    offin[e] = pdep_loop(e, T.qin);
+    offout[e] = pdep_loop(e, T.qout);
+    uint32_t m = 0;
+    for (int b = 0; b < T.k; ++b) m |= ((e >> b) & 1u) << T.fmap[b];
+    emap[e] = (uint16_t)m;
+  }
+  const uint64_t nmask = (n >= 64) ? ~0ull : ((1ull << n) - 1);
+  const uint64_t outside = ~T.qin & nmask;
+  const uint64_t ntiles = 1ull << (n - T.k);
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    if (threadIdx.x == 0) {
+      const uint64_t ib = pdep_loop(t, outside);
+      base_s[0] = ib;
+      base_s[1] = permute_bits(ib, P);
+    }
+    __syncthreads();
+    const uint64_t ibase = base_s[0], jbase = base_s[1];
+    for (uint32_t e = threadIdx.x; e < K; e += blockDim.x) tile[e] = in[ibase | offin[e]];
+    __syncthreads();
+    for (uint32_t f = threadIdx.x; f < K; f += blockDim.x) out[jbase | offout[f]] = tile[emap[f]];
+    __syncthreads();
+  }
+}
+
 // State sharding: the half of a shard whose local bit `bit` equals `value`,
 // packed contiguously (index order) for a global<->local qubit swap.
 template <typename V>
