@@ -54,13 +54,18 @@ DTYPE_NAME = {"c128": "c128 (complex128, f64 arithmetic)", "c64": "c64 (complex6
 # trajectories per step: more trajectories share the noiseless trunk's passes (c128: 24 -> 553 K,
 # 32 -> 581 K, 36 -> 596 K, 40 -> 595 K shots/s; 36 x 4 GiB states + trunk fit the 180 GB)
 DEFAULT_BATCH = {"c128": 36, "c64": 48}
+# trajectories of the whole job (BASELINE.json configs): config 4 = 10^4 trajectories x 10^4 shots
+JOB_TRAJECTORIES = {1: 100, 3: 1_000, 4: 10_000}
 
 
 def workload_config(config: int, world: int) -> dict:
     """The workload description, identical in both arms."""
     return {"workload": "config4 steane_blocks(4): 28 q, 390 ops, 560 sites, probabilistic PTS"
             if config == 4 else f"config{config}",
+            "job_trajectories": JOB_TRAJECTORIES.get(config),
             "shots_per_trajectory": SHOTS, "parallelism": f"traj-dp{world}",
+            "step": "one batch of the job's trajectories prepared + sampled; timed steps = evenly spaced "
+                    "batches of the job's execution order",
             "l2": "inputs larger than L2 (2-4 GiB states)"}
 
 
@@ -361,13 +366,27 @@ def run_engine_leg(args, dtype: str, batch: int, c, specs_for, dev, world, rank,
     from paper_2504_16297_b200 import _native as N
     from paper_2504_16297_b200.engine import Engine, pcg64_state_words
     from paper_2504_16297_b200.execute import mix_seed
-    from paper_2504_16297_b200.program import compile_circuit, selection_matrix
+    from paper_2504_16297_b200.program import compile_circuit, prefix_order, selection_matrix
 
     B, W, K = batch, args.warmup, args.steps
     per_rank = (W + K) * B
-    ids, specs = specs_for(per_rank)
+    share_ids, share_specs = specs_for()      # this rank's share of the whole job's trajectories
     prog = compile_circuit(c, dtype, tile_bits=args.tile_bits, low_bits=args.low_bits,
                            search_iters=args.search_iters)
+    # The job runs its share in batches of B in the order execute_all uses (trajectories with
+    # common outcome prefixes side by side: the engine's tree schedule computes a shared prefix
+    # once).  A step = one of those batches; the timed steps are K batches evenly spaced over the
+    # whole order (an unbiased sample of the job's batches), the warm-up steps W others.
+    order = list(range(len(share_specs))) if args.no_prefix_order else prefix_order(prog, share_specs)
+    nb = len(order) // B
+    timed = sorted({min(nb - 1, int((i + 0.5) * nb / K)) for i in range(K)})
+    if nb < W + K or len(timed) < K:
+        raise SystemExit(f"job too small for {W} + {K} steps of {B} trajectories ({len(order)} per rank)")
+    rest = [j for j in range(nb) if j not in set(timed)]
+    warm = [rest[int(i * len(rest) / W)] for i in range(W)]
+    pick = [order[j * B + i] for j in warm + timed for i in range(B)]
+    ids, specs = [share_ids[i] for i in pick], [share_specs[i] for i in pick]
+    steps_info = {"job_trajectories_per_rank": len(order), "batches_per_rank": nb, "timed_batches": timed}
     eng = Engine(c.n_qubits, dtype, batch_cap=B, device=local)
     t_load = time.perf_counter()
     eng.load_program(prog)          # plans phases, generates + NVRTC-compiles the pass kernels
@@ -435,7 +454,8 @@ def run_engine_leg(args, dtype: str, batch: int, c, specs_for, dev, world, rank,
     step_ms = e0.elapsed_time(e1)
     ms = max_over_ranks(step_ms)
     total_traj = K * B * world
-    out = {"prog": prog, "eng_info": eng.info(), "t_load": t_load, "ms": ms, "value": total_traj * SHOTS / (ms / 1e3),
+    out = {"prog": prog, "eng_info": eng.info(), "t_load": t_load, "steps_info": steps_info, "ms": ms,
+           "value": total_traj * SHOTS / (ms / 1e3),
            "traj_s": total_traj / (ms / 1e3), "launches": launches, "clocks": clk.summary(),
            "pass_ms": pass_ms, "pass_n": pass_n, "pass_bytes": pass_bytes, "pp_ms": pp_ms, "pp_bytes": pp_bytes,
            "step_ms_local": step_ms, "total_traj": total_traj}
@@ -604,6 +624,8 @@ def main():
     ap.add_argument("--tile-bits", type=int, default=None, help="fused-pass tile qubits (default: planner's)")
     ap.add_argument("--low-bits", type=int, default=None, help="contiguous low qubits per tile row (default: planner's)")
     ap.add_argument("--search-iters", type=int, default=None, help="layout-search steps of the planner")
+    ap.add_argument("--no-prefix-order", action="store_true",
+                    help="run trajectories in PTS order instead of grouping common outcome prefixes")
     ap.add_argument("--no-errors", action="store_true",
                     help="analysis only: zero every sampled Kraus selection (all trajectories noiseless)")
     args = ap.parse_args()
@@ -630,12 +652,13 @@ def main():
     W, K = args.warmup, args.steps
     legs = [args.dtype] + ([args.secondary] if args.secondary not in ("none", args.dtype) else [])
     batches = {d: (args.batch if (args.batch and d == args.dtype) else DEFAULT_BATCH[d]) for d in legs}
-    need = max(batches.values()) * (W + K) * world
+    need = max(JOB_TRAJECTORIES.get(args.config, 0), 2 * max(batches.values()) * (W + K) * world)
     c, specs_all = make_workload(args.config, need, args.seed)
 
-    def specs_for(per_rank):
-        # deterministic deal by trajectory id: rank r owns ids [r*per_rank, (r+1)*per_rank)
-        ids = list(range(rank * per_rank, (rank + 1) * per_rank))
+    def specs_for():
+        # deterministic deal by trajectory id: rank r owns a contiguous block of the job's ids
+        per = len(specs_all) // world
+        ids = list(range(rank * per, (rank + 1) * per))
         return ids, [specs_all[i] for i in ids]
 
     res = {}
@@ -660,7 +683,9 @@ def main():
         "config": workload_config(args.config, world),
         "engine": {"batch_per_gpu": B, "passes": prog.n_passes, "g_ref": prog.g_ref, "rng": args.rng,
                    "codegen": bool(head["eng_info"]["codegen"]), "program_load_s": round(head["t_load"], 2),
-                   "trajectories_timed": head["total_traj"]},
+                   "trajectories_timed": head["total_traj"],
+                   "execution_order": "PTS order" if args.no_prefix_order else "prefix-sorted (execute_all's)",
+                   **head["steps_info"]},
         "trajectories_per_s": head["traj_s"],
         "traj_roofline_frac": head["traj_s"] / (hbm * 1e9 * world / traj_bytes),
         "roofline": roofline_of(head, args.dtype, B, args.config, K),

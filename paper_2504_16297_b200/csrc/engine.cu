@@ -242,16 +242,20 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero, int p_begin = 0, int p
     h->final_general = false;
     return 0;
   }
-  // Launch entries per pass.  Shared-trunk schedule (fresh |0> batches): every
-  // trajectory equals the noiseless "trunk" until f_t, the first pass in which
-  // it takes a non-default outcome.  The trunk (row cap, slots cap / cap+1
-  // alternating) runs while anybody still needs it; trajectory t forks at pass
-  // f_t by reading the trunk's previous state and writing its own slot, then
-  // evolves alone.  Same kernels, same ops, same inputs: bit-identical to
-  // evolving every trajectory from |0> separately.
+  // Launch entries per pass: the shared-prefix TREE schedule (fresh |0> batches).  Two
+  // trajectories have identical states through pass k iff they take identical outcomes at
+  // every site of passes <= k.  The batch is kept as groups of such trajectories; each
+  // group's state lives in one member's slot (its owner) and is computed ONCE per pass.
+  // When a group's members take different outcomes in pass k it splits: every new
+  // subgroup reads the group's state from pass k-1 and writes its own owner's slot (the
+  // first launch of the pass); the subgroup that keeps the old owner updates that slot in
+  // place in a second launch, after everybody has read it.  Weight / norm / status rows are
+  // inherited at the split (fork rows).  Groups still shared after the last pass (equal
+  // outcome tables) are copied to their members.  Same kernels, same ops, same inputs:
+  // bit-identical to evolving every trajectory from |0> separately
+  // (test_shared_trunk_schedule_is_bit_identical); the noiseless trunk of round 1 is the
+  // root of this tree.
   const int P = (int)h->passes.size();
-  const int trunk = h->cap;
-  std::vector<int> fpass(B, 0);
   const bool tree = from_zero && p_begin == 0 && p_end == P && P >= 2 && h->tree_enabled && !h->host_sel.empty();
   h->tsum_ok = false;
   // (a 512-amplitude sampler block must be the amplitudes of a warp or a half warp of
@@ -267,69 +271,106 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero, int p_begin = 0, int p
     const int cpr_log = lp.c - (vpw == 2 ? 1 : 0);
     store_fast = cpr_log >= 0 && thr >= (1ll << cpr_log) && ((1ll << lp.L) / vpw) % thr == 0;
   }
-  const bool fuse_sums = h->gen_active && !h->any_general && from_zero && p_begin == 0 && p_end == P && P >= 1 &&
-                         h->sbits == 9 && store_fast && (per_thread * 32 == 512 || per_thread * 16 == 512) &&
-                         !std::getenv("PTSBE_NO_FUSED_SUMS");
-  if (tree) {
+  bool fuse_sums = h->gen_active && !h->any_general && from_zero && p_begin == 0 && p_end == P && P >= 1 &&
+                   h->sbits == 9 && store_fast && (per_thread * 32 == 512 || per_thread * 16 == 512) &&
+                   !std::getenv("PTSBE_NO_FUSED_SUMS");
+  struct LaunchRec { int pass, ent_begin, E, fork_begin, nfork; };
+  std::vector<int4> ents;
+  std::vector<int32_t> forkpairs;               // (child row, parent row) pairs
+  std::vector<LaunchRec> launches;
+  std::vector<std::pair<int, int>> end_copies;  // (member, owner) of groups shared to the end
+  if (!tree) {
+    for (int k = p_begin; k < p_end; ++k) {
+      launches.push_back(LaunchRec{k, (int)ents.size(), B, 0, 0});
+      for (int b = 0; b < B; ++b) ents.push_back(make_int4(b, b, b, 0));
+    }
+  } else {
+    // per (trajectory, pass): its non-default (site, outcome) pairs, ascending site
+    std::vector<std::vector<std::pair<int, int>>> errs((size_t)B * P);
     for (int b = 0; b < B; ++b) {
-      int f = P - 1;
       const uint8_t* row = h->host_sel.data() + (size_t)b * h->n_sites;
       for (int s = 0; s < h->n_sites; ++s)
-        if (row[s] && h->site_pass[s] < f) f = h->site_pass[s];
-      fpass[b] = f;
+        if (row[s] && h->site_pass[s] < P) errs[(size_t)b * P + h->site_pass[s]].push_back({s, (int)row[s]});
     }
-  }
-  std::vector<int4> ents;
-  std::vector<int> ent_begin(P + 1, 0);
-  std::vector<std::vector<int32_t>> forks(P);
-  for (int k = 0; k < P; ++k) {
-    ent_begin[k] = (int)ents.size();
-    bool trunk_needed = false;
-    for (int b = 0; b < B; ++b) {
-      if (!tree) { ents.push_back(make_int4(b, b, b, 0)); continue; }
-      if (fpass[b] < k) ents.push_back(make_int4(b, b, b, 0));
-      else if (fpass[b] == k) {
-        ents.push_back(make_int4(b, k == 0 ? b : trunk + ((k - 1) & 1), b, 0));
-        if (k > 0) forks[k].push_back(b);
-      } else trunk_needed = true;
+    struct Group { int owner; std::vector<int> mem; };
+    std::vector<Group> groups(1);
+    groups[0].owner = 0;
+    for (int b = 0; b < B; ++b) groups[0].mem.push_back(b);
+    for (int k = 0; k < P; ++k) {
+      std::vector<int4> inA, inB;
+      std::vector<int32_t> fk;
+      std::vector<Group> next;
+      for (const Group& g : groups) {
+        std::vector<Group> subs;
+        std::vector<const std::vector<std::pair<int, int>>*> keys;
+        for (int b : g.mem) {
+          const auto* key = &errs[(size_t)b * P + k];
+          size_t j = 0;
+          while (j < keys.size() && *keys[j] != *key) ++j;
+          if (j == keys.size()) { keys.push_back(key); subs.push_back(Group{b, {}}); }
+          subs[j].mem.push_back(b);
+        }
+        if (subs.size() == 1) {                     // no split: in place
+          inA.push_back(make_int4(g.owner, g.owner, g.owner, 0));
+          next.push_back(Group{g.owner, subs[0].mem});
+          continue;
+        }
+        for (Group& sg : subs) {
+          if (std::find(sg.mem.begin(), sg.mem.end(), g.owner) != sg.mem.end()) {
+            sg.owner = g.owner;                     // keeps the slot: updated after the others read it
+            (k == 0 ? inA : inB).push_back(make_int4(g.owner, g.owner, g.owner, 0));
+          } else {
+            sg.owner = sg.mem[0];
+            inA.push_back(make_int4(sg.owner, g.owner, sg.owner, 0));
+            if (k > 0) { fk.push_back(sg.owner); fk.push_back(g.owner); }
+          }
+          next.push_back(sg);
+        }
+      }
+      launches.push_back(LaunchRec{k, (int)ents.size(), (int)inA.size(), (int)forkpairs.size() / 2,
+                                   (int)fk.size() / 2});
+      ents.insert(ents.end(), inA.begin(), inA.end());
+      forkpairs.insert(forkpairs.end(), fk.begin(), fk.end());
+      if (!inB.empty()) {
+        launches.push_back(LaunchRec{k, (int)ents.size(), (int)inB.size(), 0, 0});
+        ents.insert(ents.end(), inB.begin(), inB.end());
+      }
+      groups.swap(next);
     }
-    if (trunk_needed) ents.push_back(make_int4(trunk, k == 0 ? trunk : trunk + ((k - 1) & 1), trunk + (k & 1), 0));
+    for (const Group& g : groups)
+      for (int m : g.mem)
+        if (m != g.owner) end_copies.push_back({m, g.owner});
   }
-  ent_begin[P] = (int)ents.size();
   h->last_entries = (long long)ents.size();
   if (ents.size() > h->ent_cap) {
     if (dalloc(h, &h->d_ent, ents.size())) return PTSBE_ERR_CUDA;
     h->ent_cap = ents.size();
   }
-  CK(h, cudaMemcpyAsync(h->d_ent, ents.data(), ents.size() * sizeof(int4), cudaMemcpyHostToDevice, h->stream));
-  if (tree) {
-    std::vector<int32_t> allf;
-    for (int k = 0; k < P; ++k) allf.insert(allf.end(), forks[k].begin(), forks[k].end());
-    if (allf.size() > h->fork_cap) {
-      if (dalloc(h, &h->d_forks, allf.size())) return PTSBE_ERR_CUDA;
-      h->fork_cap = allf.size();
+  if (!ents.empty())
+    CK(h, cudaMemcpyAsync(h->d_ent, ents.data(), ents.size() * sizeof(int4), cudaMemcpyHostToDevice, h->stream));
+  if (!forkpairs.empty()) {
+    if (forkpairs.size() > h->fork_cap) {
+      if (dalloc(h, &h->d_forks, forkpairs.size())) return PTSBE_ERR_CUDA;
+      h->fork_cap = forkpairs.size();
     }
-    if (!allf.empty())
-      CK(h, cudaMemcpyAsync(h->d_forks, allf.data(), allf.size() * 4, cudaMemcpyHostToDevice, h->stream));
-    // trunk row starts like every trajectory
-    batch_reset<<<1, 32, 0, h->stream>>>(h->d_weight + trunk, h->d_nst + trunk, h->d_status + trunk,
-                                         h->d_fail + trunk, 1);
-    CKL(h);
+    CK(h, cudaMemcpyAsync(h->d_forks, forkpairs.data(), forkpairs.size() * 4, cudaMemcpyHostToDevice, h->stream));
   }
-  int fork_off = 0;
   NvtxRange nvtx_passes("ptsbe_passes");
-  for (size_t pi = (size_t)p_begin; pi < (size_t)p_end; ++pi) {
+  int last_pass = -1;
+  for (const LaunchRec& L : launches) {
+    const size_t pi = (size_t)L.pass;
+    if ((int)pi != last_pass && last_pass >= 0) prev_general = h->passes[last_pass].n_slots > 0;
+    last_pass = (int)pi;
     const PassHost& ph = h->passes[pi];
-    const int E = ent_begin[pi + 1] - ent_begin[pi];
-    if (!forks[pi].empty()) {   // forks inherit the trunk's weight / norm / status
-      const int nf = (int)forks[pi].size();
-      fork_rows<<<(nf + 127) / 128, 128, 0, h->stream>>>(h->d_forks + fork_off, nf, trunk, h->d_weight, h->d_nst,
-                                                           h->d_status, h->d_fail);
+    const int E = L.E;
+    if (E == 0) continue;
+    if (L.nfork > 0) {   // split-off groups inherit their parent's weight / norm / status
+      fork_pairs<<<(L.nfork + 127) / 128, 128, 0, h->stream>>>(h->d_forks + 2 * L.fork_begin, L.nfork,
+                                                                h->d_weight, h->d_nst, h->d_status, h->d_fail);
       CKL(h);
-      fork_off += nf;
     }
     PassParams p;
-    p.ent = h->d_ent + ent_begin[pi];
+    p.ent = h->d_ent + L.ent_begin;
     p.E = E;
     const bool last_fused = fuse_sums && (int)pi == P - 1;
     p.tsum = last_fused ? h->d_bs : nullptr;
@@ -409,7 +450,7 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero, int p_begin = 0, int p
         CKL(h);
         if (h->run_flags & PTSBE_DEFER_NORMS) {   // the caller adds the shards' sums (ptsbe_finalize_norms)
           h->pending_pass = (int)pi;
-          h->pending_ent = ent_begin[pi];
+          h->pending_ent = L.ent_begin;
           h->pending_E = E;
         } else {
           if (!h->comm) return fail(h, PTSBE_ERR_VALIDATION, "PTSBE_SHARDED needs ptsbe_shard_init");
@@ -428,9 +469,28 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero, int p_begin = 0, int p
         CKL(h);
       }
     }
-    prev_general = ph.n_slots > 0;
   }
+  if (last_pass >= 0) prev_general = h->passes[last_pass].n_slots > 0;
   h->final_general = prev_general;
+  if (!end_copies.empty()) {   // trajectories with identical outcome tables: copy the shared state
+    const size_t bytes = ((size_t)1 << h->n) * h->amp_bytes;
+    std::vector<int32_t> pairs;
+    for (auto& mc : end_copies) {
+      CK(h, cudaMemcpyAsync((char*)h->states + (size_t)mc.first * bytes, (char*)h->states + (size_t)mc.second * bytes,
+                            bytes, cudaMemcpyDeviceToDevice, h->stream));
+      pairs.push_back(mc.first);
+      pairs.push_back(mc.second);
+    }
+    int32_t* d_pairs = nullptr;
+    CK(h, cudaMallocAsync((void**)&d_pairs, pairs.size() * 4, h->stream));
+    CK(h, cudaMemcpyAsync(d_pairs, pairs.data(), pairs.size() * 4, cudaMemcpyHostToDevice, h->stream));
+    fork_pairs<<<((int)end_copies.size() + 127) / 128, 128, 0, h->stream>>>(d_pairs, (int)end_copies.size(),
+                                                                            h->d_weight, h->d_nst, h->d_status,
+                                                                            h->d_fail);
+    CKL(h);
+    CK(h, cudaFreeAsync(d_pairs, h->stream));
+    fuse_sums = false;   // the copies have no fused sampler sums: sample with the standalone block sums
+  }
   if (fuse_sums) {
     h->tsum_ok = true;
     h->tsum_qmask = h->passes[P - 1].qmask;
@@ -801,11 +861,10 @@ int ptsbe_create(int device, int n_qubits, int dtype, int batch_cap, ptsbe_engin
     r = fail(h, PTSBE_ERR_CUDA, "device %d unavailable: %s", device, cudaGetErrorString(e));
   }
   if (!r) {
-    // batch slots + the shared trunk's two alternating slots (skipped for huge
-    // states, where two extra copies would not fit next to the batch)
+    // batch slots only: the shared-prefix tree keeps every group's state in a member's slot
     const char* tree_env = std::getenv("PTSBE_TREE");
-    h->tree_enabled = tree_env ? std::atoi(tree_env) != 0 : n_qubits <= 30;
-    const size_t bytes = (size_t)(batch_cap + (h->tree_enabled ? 2 : 0)) * ((size_t)1 << n_qubits) * h->amp_bytes;
+    h->tree_enabled = tree_env ? std::atoi(tree_env) != 0 : true;
+    const size_t bytes = (size_t)batch_cap * ((size_t)1 << n_qubits) * h->amp_bytes;
     e = cudaMalloc(&h->states, bytes);
     if (e != cudaSuccess) r = fail(h, PTSBE_ERR_CUDA, "cannot allocate %zu bytes of state: %s", bytes, cudaGetErrorString(e));
   }
@@ -815,7 +874,7 @@ int ptsbe_create(int device, int n_qubits, int dtype, int batch_cap, ptsbe_engin
                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
     encode_t enc = nullptr;
     cudaDriverEntryPointQueryResult q;
-    const size_t bytes = (size_t)(batch_cap + (h->tree_enabled ? 2 : 0)) * ((size_t)1 << n_qubits) * h->amp_bytes;
+    const size_t bytes = (size_t)batch_cap * ((size_t)1 << n_qubits) * h->amp_bytes;
     const size_t rows = bytes / 128;
     if (((size_t)1 << n_qubits) * h->amp_bytes >= 512 && rows < (1ull << 31) &&
         cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q) == cudaSuccess &&

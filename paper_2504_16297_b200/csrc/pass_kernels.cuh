@@ -579,6 +579,17 @@ __global__ void fork_rows(const int32_t* rows, int n, int trunk, double* weight,
   }
 }
 
+// Split-off trajectory groups inherit their parent's running weight / norm / status:
+// pairs[2i] (child row) <- pairs[2i+1] (parent row).
+__global__ void fork_pairs(const int32_t* pairs, int n, double* weight, double* nst, int32_t* status,
+                           int32_t* fail_site) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const int r = pairs[2 * i], src = pairs[2 * i + 1];
+    weight[r] = weight[src]; nst[r] = nst[src]; status[r] = status[src]; fail_site[r] = fail_site[src];
+  }
+}
+
 // Multiply state b by 1/sqrt(nst[b]) (normalise before download).
 template <typename R>
 __global__ void scale_states(void* states, int n, int B, const double* nst, int invert_sqrt) {

@@ -285,3 +285,23 @@ def selection_matrix(program: Program, specs) -> np.ndarray:
         for sid, k in spec.selections:
             sel[b, sid] = k
     return sel
+
+
+def site_passes(program: Program) -> np.ndarray:
+    """Pass index of every site of a planned program (-1: not in any pass)."""
+    sp = np.full(program.n_sites, -1, dtype=np.int64)
+    for p, plan in enumerate(program.passes):
+        for i in plan.ops:
+            so = program.stream[i]
+            if so.kind == KIND_SITE:
+                sp[so.ref] = p
+    return sp
+
+
+def prefix_order(program: Program, specs) -> list:
+    """Execution order that puts trajectories with common outcome prefixes (in pass order) next
+    to each other: batches of neighbours share more of the engine's tree schedule (a group of
+    trajectories with identical outcomes through pass k is computed once through pass k)."""
+    sp = site_passes(program)
+    keys = [tuple(sorted((int(sp[sid]), sid, k) for sid, k in spec.selections)) for spec in specs]
+    return sorted(range(len(specs)), key=lambda i: (keys[i], i))

@@ -380,3 +380,64 @@ def test_execute_all_distributed_single_rank_equals_execute_all(tmp_path):
     assert (tmp_path / "a" / "records.jsonl").read_bytes() == (tmp_path / "b" / "records.jsonl").read_bytes()
     assert P.manifest_core(a.manifest) == P.manifest_core(b.manifest)
     b.validate()
+
+
+@pytest.mark.parametrize("dtype", ["c64", "c128"])
+def test_tree_schedule_shared_prefixes_splits_and_duplicates(dtype, monkeypatch):
+    """The shared-prefix tree schedule with groups that share several errors, split in the middle
+    of the program (owner kept in place after the others read it), renormalising sites and
+    duplicated outcome tables (copied at the end) equals independent evolution bit for bit."""
+    from paper_2504_16297_b200.program import prefix_order, site_passes
+    c = workloads.build(3, P.parse_circuit, P.parse_noise_model, P.attach_noise)
+    prog = compile_circuit(c, dtype)
+    sp = site_passes(prog)
+    by_pass = [[s for s in range(prog.n_sites) if sp[s] == p] for p in range(prog.n_passes)]
+    a, b2, b3 = by_pass[0][0], by_pass[1][2], by_pass[prog.n_passes - 1][1]
+    sel = [(), ((a, 1),), ((a, 1), (b2, 2)), ((a, 1), (b2, 2), (b3, 1)), ((a, 1), (b2, 3)), ((b2, 2),),
+           ((a, 1), (b2, 2)), ()]
+    specs = [P.TrajectorySpec(tuple(sorted(x)), 10) for x in sel]
+    order = prefix_order(prog, specs)
+    assert sorted(order) == list(range(len(specs)))
+    out = {}
+    for tree in ("1", "0"):
+        monkeypatch.setenv("PTSBE_TREE", tree)
+        with Engine(c.n_qubits, dtype, batch_cap=len(specs)) as eng:
+            eng.load_program(prog)
+            w, st = eng.run(selection_matrix(prog, specs))
+            words = np.concatenate([pcg64_state_words(mix_seed(3, t)) for t in range(len(specs))])
+            shots = eng.sample([200] * len(specs), N.RNG_PCG64, rng_state=words)   # order-independent exact CDF
+            out[tree] = (w, st, [eng.get_state(b) for b in range(len(specs))], shots)
+    assert np.array_equal(out["1"][0], out["0"][0]) and np.array_equal(out["1"][1], out["0"][1])
+    for x, y in zip(out["1"][2], out["0"][2]):
+        assert np.array_equal(x, y)
+    assert np.array_equal(out["1"][3].indices, out["0"][3].indices)
+    assert np.array_equal(out["1"][3].counts, out["0"][3].counts)
+    # and against the oracle
+    for b, spec in enumerate(specs):
+        ref, _ = O.prepare(c, spec.selections)
+        assert rel(out["1"][2][b].astype(np.complex128), ref) <= TOL[dtype]
+
+
+def test_tree_schedule_renormalising_groups(monkeypatch):
+    """Groups sharing amplitude-damping outcomes (renormalising, weights inherited at splits)."""
+    text = "qubits 6\n" + "".join(f"gate h {q}\ngate ry {q} @ 0.{q + 3}\n" for q in range(6)) + \
+        "".join(f"gate cx {q} {q + 1}\n" for q in range(5)) + "".join(f"gate rx {q} @ 1.1\n" for q in range(6))
+    c = P.attach_noise(P.parse_circuit(text), P.parse_noise_model("rule gate=* qubit=* channel=amplitude_damping(0.2)\n"))
+    prog = compile_circuit(c, "c128", tile_bits=4, low_bits=2)
+    assert prog.n_passes >= 3
+    S = prog.n_sites
+    specs = [P.TrajectorySpec(x, 5) for x in [(), ((0, 1),), ((0, 1), (S - 1, 1)), ((0, 1), (S - 2, 1)),
+                                              ((3, 1),), ((0, 1), (S - 1, 1))]]
+    out = {}
+    for tree in ("1", "0"):
+        monkeypatch.setenv("PTSBE_TREE", tree)
+        with Engine(c.n_qubits, "c128", batch_cap=len(specs)) as eng:
+            eng.load_program(prog)
+            w, st = eng.run(selection_matrix(prog, specs))
+            out[tree] = (w, st, [eng.get_state(b) for b in range(len(specs))])
+    assert np.array_equal(out["1"][0], out["0"][0]) and np.array_equal(out["1"][1], out["0"][1])
+    for b, (x, y) in enumerate(zip(out["1"][2], out["0"][2])):
+        assert np.array_equal(x, y)
+        if out["1"][1][b] == 0:
+            ref, rw = O.prepare(c, specs[b].selections)
+            assert rel(x, ref) <= 1e-12 and out["1"][0][b] == pytest.approx(rw, rel=1e-12)
