@@ -51,9 +51,9 @@ def metric_for(config: int) -> str:
         return "shots/sec (config 5: 34-35-qubit QEC state sharded within the trajectory, 1e6 shots/trajectory)"
     return METRIC if config == 4 else f"shots/sec (config {config}, 1e4 shots/trajectory)"
 DTYPE_NAME = {"c128": "c128 (complex128, f64 arithmetic)", "c64": "c64 (complex64, f32 arithmetic)"}
-# trajectories per step: more trajectories share the noiseless trunk's passes (c128: 24 -> 553 K,
-# 32 -> 581 K, 36 -> 596 K, 40 -> 595 K shots/s; 36 x 4 GiB states + trunk fit the 180 GB)
-DEFAULT_BATCH = {"c128": 36, "c64": 48}
+# trajectories per step (config 4, prefix-sorted job, 12 timed batches): c128 24 / 28 / 36 ->
+# 722 / 747 / 728 K shots/s; c64 48 / 64 / 80 -> 1.76 / 1.77 / 1.75 M
+DEFAULT_BATCH = {"c128": 28, "c64": 48}
 # trajectories of the whole job (BASELINE.json configs): config 4 = 10^4 trajectories x 10^4 shots
 JOB_TRAJECTORIES = {1: 100, 3: 1_000, 4: 10_000}
 
