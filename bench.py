@@ -496,17 +496,17 @@ def roofline_of(leg, dtype: str, batch: int, config: int, K: int):
     bytes_per_launch = leg["pass_bytes"] / max(leg["pass_n"], 1)
     avg_launch_ms = leg["pass_ms"] / max(leg["pass_n"], 1)
     achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
-    traffic, traffic_src = None, None
+    traffic, traffic_src, ratio = None, None, None
     tf = REPO / "profiles" / f"pass_traffic_config{config}_{dtype}.json"
-    if tf.exists():   # ncu DRAM bytes per pass launch of the same workload (committed capture)
+    if tf.exists():   # ncu DRAM bytes / algorithmic bytes of the pass launches (committed capture)
         t = json.loads(tf.read_text())
-        if (t.get("config"), t.get("batch_per_gpu"), t.get("dtype"), t.get("launches")) == \
-                (config, batch, dtype, leg["prog"].n_passes):
-            traffic, traffic_src = t["per_launch_dram_bytes"], t["source"]
-            if not traffic == traffic:   # nan counters: report none
-                traffic, traffic_src = None, None
+        if (t.get("config"), t.get("batch_per_gpu"), t.get("dtype")) == (config, batch, dtype) and \
+                t.get("dram_over_algorithmic"):
+            ratio = float(t["dram_over_algorithmic"])
+            traffic, traffic_src = ratio * bytes_per_launch, t["source"]
     return {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
             "traffic": traffic, "traffic_unit": "bytes/launch (dram read+write, ncu)", "traffic_source": traffic_src,
+            "traffic_over_algorithmic": ratio,
             "kernel": "ptsbe_pass_<p> (circuit-specialised fused pass kernels, NVRTC sm_100a)",
             "peak_kind": peak_kind, "bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch_ms,
             "pass_share_of_step": leg["pass_ms"] / max(1e-9, leg["step_ms_local"]),

@@ -120,6 +120,10 @@ struct ptsbe_engine {
   std::vector<int> ev_pass;               // pass index of each profiled launch (event pair)
   std::vector<double> ev_bytes;           // its algorithmic bytes
   std::vector<double> per_pass_ms, per_pass_bytes;
+  // PTSBE_LAUNCH_LOG=path: every pass launch's (pass, launch entries, algorithmic bytes),
+  // appended to the file when the handle is destroyed -- matched line by line against an
+  // ncu capture of the same process to turn DRAM counters into a traffic / algorithmic ratio
+  std::vector<double> launch_log;
   // host-only handle (ptsbe_create_host): load_program plans and generates the
   // pass kernels' source without touching a device (offline SASS inspection)
   bool host_only = false;
@@ -434,6 +438,11 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero, int p_begin = 0, int p
       pass_kernel_small<R><<<grid, 32, 0, h->stream>>>(p);
     }
     CKL(h);
+    if (std::getenv("PTSBE_LAUNCH_LOG")) {
+      h->launch_log.push_back((double)pi);
+      h->launch_log.push_back((double)E);
+      h->launch_log.push_back(2.0 * E * (double)((size_t)1 << h->n) * (double)h->amp_bytes);
+    }
     if (h->profiling) {
       CK(h, cudaEventRecord(h->ev[h->ev_used + 1], h->stream));
       h->ev_used += 2;
@@ -947,6 +956,14 @@ int64_t ptsbe_codegen_source(ptsbe_engine* h, char* buf, size_t len) {
 
 int ptsbe_destroy(ptsbe_engine* h) {
   if (!h) return 0;
+  if (const char* path = std::getenv("PTSBE_LAUNCH_LOG")) {
+    if (!h->launch_log.empty())
+      if (FILE* f = std::fopen(path, "a")) {
+        for (size_t i = 0; i + 2 < h->launch_log.size(); i += 3)
+          std::fprintf(f, "%d %d %.0f\n", (int)h->launch_log[i], (int)h->launch_log[i + 1], h->launch_log[i + 2]);
+        std::fclose(f);
+      }
+  }
   if (h->host_only) { delete h; return 0; }
   cudaSetDevice(h->dev);
   void* ptrs[] = {h->states, h->d_sel, h->d_weight, h->d_nst, h->d_status, h->d_fail, h->d_ops, h->d_mats,

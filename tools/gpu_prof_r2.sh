@@ -14,7 +14,11 @@ print(compile_circuit(c, '$d').n_passes)")
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1000 --csv \
     --log-file gpurun_out/launches_${d}_$tag.csv python bench.py --steps 2 --warmup 3 --no-cpu --dtype $d --secondary none \
     > gpurun_out/ncu_launch_${d}_$tag.log 2>&1
-  timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
-    -k regex:ptsbe_pass -s $((3 * np)) -c $np --csv --log-file gpurun_out/pass_dram_${d}_$tag.csv \
-    python bench.py --steps 1 --warmup 3 --no-cpu --dtype $d --secondary none > gpurun_out/ncu_dram_${d}_$tag.log 2>&1
+  # every pass launch of a short bench run, with the engine's own log of each launch's
+  # algorithmic bytes (same process, same order) -> DRAM traffic / algorithmic bytes
+  rm -f gpurun_out/launchlog_${d}_$tag.txt
+  PTSBE_LAUNCH_LOG=gpurun_out/launchlog_${d}_$tag.txt timeout 1200 ncu --metrics \
+    dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+    -k regex:ptsbe_pass --csv --log-file gpurun_out/pass_dram_${d}_$tag.csv \
+    python bench.py --steps 1 --warmup 1 --no-cpu --dtype $d --secondary none > gpurun_out/ncu_dram_${d}_$tag.log 2>&1
 done

@@ -15,7 +15,7 @@ import sys
 from pathlib import Path
 
 tag, out = sys.argv[1], sys.argv[2]
-batch = {"c128": int(sys.argv[3]) if len(sys.argv) > 3 else 24, "c64": int(sys.argv[4]) if len(sys.argv) > 4 else 48}
+batch = {"c128": int(sys.argv[3]) if len(sys.argv) > 3 else 28, "c64": int(sys.argv[4]) if len(sys.argv) > 4 else 48}
 G = Path("gpurun_out")
 UNIT = {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0, "second": 1e3}
 BYTES = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
@@ -70,19 +70,31 @@ for d in ("c128", "c64"):
         launches = list(per.values())
         by = [e["read"] + e["write"] for e in launches]
         shutil.copy(pf, f"{out}_pass_dram_config4_{d}.csv")
-        n_q = 28
-        amp = 16 if d == "c128" else 8
+        # the engine's own launch log of the same process: (pass, entries, algorithmic bytes)
+        ll = G / f"launchlog_{d}_{tag}.txt"
+        alg = [tuple(float(x) for x in line.split()) for line in open(ll)] if ll.exists() else []
+        m = min(len(alg), len(by))
+        if m:
+            shutil.copy(ll, f"{out}_launchlog_config4_{d}.txt")
+        ratio = sum(by[:m]) / sum(a[2] for a in alg[:m]) if m else None
+        per_pass = {}
+        for (p_, e_, a_), b_ in zip(alg[:m], by[:m]):
+            x = per_pass.setdefault(int(p_), [0.0, 0.0])
+            x[0] += b_
+            x[1] += a_
         traffic = {
+            "dram_over_algorithmic": ratio,
+            "per_pass_dram_over_algorithmic": {k: v[0] / v[1] for k, v in sorted(per_pass.items())},
+            "launches_matched": m,
             "per_launch_dram_bytes": sum(by) / len(by),
             "launches": len(by),
-            "per_pass_dram_bytes": by,
-            "per_pass_ncu_ms": [e["ms"] for e in launches],
-            "kernels": [e["name"] for e in launches],
             "config": 4, "batch_per_gpu": batch[d], "dtype": d,
-            "note": f"algorithmic bytes per launch = 2 * E * 2^{n_q} * {amp} B (E = launch entries incl. the trunk)",
+            "note": "algorithmic bytes per launch = 2 * E * 2^n * s (E = launch entries of the tree schedule); "
+                    "bench.py reports traffic = dram_over_algorithmic x its own algorithmic bytes per launch",
             "source": f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum -k "
-                      f"regex:ptsbe_pass of one bench step after 3 warm-up steps (gpurun tag {tag}; raw CSV "
-                      f"{Path(out).name}_pass_dram_config4_{d}.csv)",
+                      f"regex:ptsbe_pass over every pass launch of a short bench run, matched in order with the "
+                      f"engine's PTSBE_LAUNCH_LOG of the same process (gpurun tag {tag}; raw files "
+                      f"{Path(out).name}_pass_dram_config4_{d}.csv, {Path(out).name}_launchlog_config4_{d}.txt)",
         }
         Path(f"profiles/pass_traffic_config4_{d}.json").write_text(json.dumps(traffic, indent=1) + "\n")
-        print(d, "passes", len(by), "mean GB/launch", round(traffic["per_launch_dram_bytes"] / 1e9, 2))
+        print(d, "launches", len(by), "matched", m, "dram / algorithmic", ratio)
