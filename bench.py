@@ -674,7 +674,8 @@ def main():
     B = batches[args.dtype]
     amp = 8 if args.dtype == "c64" else 16
     prog = head["prog"]
-    traj_bytes = prog.n_passes * 2 * (1 << c.n_qubits) * amp + (1 << c.n_qubits) * amp + 16 * SHOTS
+    # per trajectory: pass 0 writes the state, every later pass reads + writes it, sampling reads it
+    traj_bytes = (2 * prog.n_passes - 1) * (1 << c.n_qubits) * amp + (1 << c.n_qubits) * amp + 16 * SHOTS
     line = {
         "metric": metric_for(args.config), "value": head["value"], "unit": "shots/s",
         "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": head["ms"] / K, "higher_is_better": True,

@@ -441,12 +441,14 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero, int p_begin = 0, int p
     if (std::getenv("PTSBE_LAUNCH_LOG")) {
       h->launch_log.push_back((double)pi);
       h->launch_log.push_back((double)E);
-      h->launch_log.push_back(2.0 * E * (double)((size_t)1 << h->n) * (double)h->amp_bytes);
+      h->launch_log.push_back((p.gen_zero ? 1.0 : 2.0) * E * (double)((size_t)1 << h->n) * (double)h->amp_bytes);
     }
     if (h->profiling) {
       CK(h, cudaEventRecord(h->ev[h->ev_used + 1], h->stream));
       h->ev_used += 2;
-      const double by = 2.0 * E * (double)((size_t)1 << h->n) * (double)h->amp_bytes;
+      // one read + one write of every state of the launch; a pass that starts from |0...0>
+      // (gen_zero) only writes
+      const double by = (p.gen_zero ? 1.0 : 2.0) * E * (double)((size_t)1 << h->n) * (double)h->amp_bytes;
       h->pass_bytes_total += by;
       h->ev_pass.push_back((int)pi);
       h->ev_bytes.push_back(by);
