@@ -268,11 +268,15 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero, int p_begin = 0, int p
                                             gen::threads_for(h->passes[P - 1].L, h->passes[P - 1].gb, false) : 0;
   // and the pass's store loop must be the vectorised one (gen_prelude.cuh run_pass FAST)
   bool store_fast = false;
+  int tsum_ce = 0;   // effective contiguous bits of the last pass's (sub-)rows (gen_prelude.cuh CE)
   if (P >= 1) {
     const PassHost& lp = h->passes[P - 1];
     const long long thr = gen::threads_for(lp.L, lp.gb, false);
     const int vpw = h->dtype == PTSBE_C64 ? 2 : 1;
-    const int cpr_log = lp.c - (vpw == 2 ? 1 : 0);
+    int tlog2 = 5;
+    while ((1ll << (tlog2 + 1)) <= thr && tlog2 < 10) ++tlog2;
+    const int cpr_log = std::min(lp.c - (vpw == 2 ? 1 : 0), tlog2);
+    tsum_ce = cpr_log + (vpw == 2 ? 1 : 0);
     store_fast = cpr_log >= 0 && thr >= (1ll << cpr_log) && ((1ll << lp.L) / vpw) % thr == 0;
   }
   bool fuse_sums = h->gen_active && !h->any_general && from_zero && p_begin == 0 && p_end == P && P >= 1 &&
@@ -506,7 +510,7 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero, int p_begin = 0, int p
     h->tsum_ok = true;
     h->tsum_qmask = h->passes[P - 1].qmask;
     h->tsum_L = h->passes[P - 1].L;
-    h->tsum_c = h->passes[P - 1].c;
+    h->tsum_c = tsum_ce;
     h->tsum_threads = gen::threads_for(h->passes[P - 1].L, h->passes[P - 1].gb, false);
   }
   return 0;

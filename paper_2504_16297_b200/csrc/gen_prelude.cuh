@@ -395,7 +395,13 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
   constexpr int VPW = sizeof(W) / sizeof(V);
   constexpr uint32_t TL = 1u << L;
   constexpr int THREADS = NT;
-  constexpr int CPR_LOG = C - (VPW == 2 ? 1 : 0);          // 16-B vectors per row, log2
+  // rows of 2^C contiguous amplitudes longer than the CTA's threads are walked as 2^(C - CE)
+  // sub-rows of 2^CE (CE: one 16-B vector per thread per sub-row), so the per-thread vector
+  // layout (and the fused sampler sums) works for every pass; roff(r) scatters a sub-row index
+  constexpr int CPR_FULL = C - (VPW == 2 ? 1 : 0);
+  constexpr int TLOG2 = NT >= 1024 ? 10 : NT >= 512 ? 9 : NT >= 256 ? 8 : NT >= 128 ? 7 : NT >= 64 ? 6 : 5;
+  constexpr int CPR_LOG = CPR_FULL < TLOG2 ? CPR_FULL : TLOG2;   // 16-B vectors per (sub-)row, log2
+  constexpr int CE = CPR_LOG + (VPW == 2 ? 1 : 0);
   constexpr uint32_t NVEC = TL / VPW;
   constexpr bool FAST = THREADS >= (1 << CPR_LOG) && (NVEC % THREADS) == 0;
   constexpr int ITER = FAST ? (int)(NVEC / THREADS) : 1;
@@ -416,10 +422,13 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
   uint4* rowtab = reinterpret_cast<uint4*>(hits_s + PTG_MAX_HIT_WORDS);
   int lb = -1;
   const uint32_t tid = threadIdx.x;
+  auto roff = [&](uint32_t r) -> uint64_t {
+    return ((uint64_t)(r & ((1u << (C - CE)) - 1u)) << CE) | row_off(r >> (C - CE));
+  };
   const uint32_t j0 = tid & ((1u << CPR_LOG) - 1u);
   const uint32_t r0 = tid >> CPR_LOG;
-  const uint32_t s0 = swz_((r0 << C) | (j0 * VPW));
-  const uint64_t g0 = row_off(r0) + (uint64_t)j0 * VPW;
+  const uint32_t s0 = swz_((r0 << CE) | (j0 * VPW));
+  const uint64_t g0 = roff(r0) + (uint64_t)j0 * VPW;
   const long long total = (long long)p.E << TLOG;
 
   // Launch entries change every 2^TLOG tiles: the entry record, its row's status
@@ -443,11 +452,11 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
     if (FAST) {
 #pragma unroll
       for (int k = 0; k < ITER; ++k)
-        cp_async16(dst + (s0 ^ swz_((uint32_t)(k * RSTEP) << C)), src + g0 + row_off((uint32_t)(k * RSTEP)));
+        cp_async16(dst + (s0 ^ swz_((uint32_t)(k * RSTEP) << CE)), src + g0 + roff((uint32_t)(k * RSTEP)));
     } else {
       for (uint32_t u = tid; u < NVEC; u += blockDim.x) {
         const uint32_t r = u >> CPR_LOG, j = u & ((1u << CPR_LOG) - 1u);
-        cp_async16(dst + swz_((r << C) | (j * VPW)), src + row_off(r) + (uint64_t)j * VPW);
+        cp_async16(dst + swz_((r << CE) | (j * VPW)), src + roff(r) + (uint64_t)j * VPW);
       }
     }
   };
@@ -590,7 +599,7 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
         uint64_t q = 0;
 #pragma unroll
         for (int k = 0; k < ITER; ++k) {
-          const W w = *reinterpret_cast<const W*>(cur + (s0 ^ swz_((uint32_t)(k * RSTEP) << C)));
+          const W w = *reinterpret_cast<const W*>(cur + (s0 ^ swz_((uint32_t)(k * RSTEP) << CE)));
           const V* pv = reinterpret_cast<const V*>(&w);
 #pragma unroll
           for (int e = 0; e < VPW; ++e) q += qfix(pv[e]);
@@ -613,8 +622,8 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
       uint64_t q = 0;
 #pragma unroll
       for (int k = 0; k < ITER; ++k) {
-        const W w = *reinterpret_cast<const W*>(cur + (s0 ^ swz_((uint32_t)(k * RSTEP) << C)));
-        st_stream(reinterpret_cast<W*>(st + g0 + row_off((uint32_t)(k * RSTEP))), w);
+        const W w = *reinterpret_cast<const W*>(cur + (s0 ^ swz_((uint32_t)(k * RSTEP) << CE)));
+        st_stream(reinterpret_cast<W*>(st + g0 + roff((uint32_t)(k * RSTEP))), w);
         const V* pv = reinterpret_cast<const V*>(&w);
 #pragma unroll
         for (int e = 0; e < VPW; ++e) q += qfix(pv[e]);
@@ -626,14 +635,14 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
     } else if (FAST) {
 #pragma unroll
       for (int k = 0; k < ITER; ++k) {
-        const W w = *reinterpret_cast<const W*>(cur + (s0 ^ swz_((uint32_t)(k * RSTEP) << C)));
-        st_stream(reinterpret_cast<W*>(st + g0 + row_off((uint32_t)(k * RSTEP))), w);
+        const W w = *reinterpret_cast<const W*>(cur + (s0 ^ swz_((uint32_t)(k * RSTEP) << CE)));
+        st_stream(reinterpret_cast<W*>(st + g0 + roff((uint32_t)(k * RSTEP))), w);
       }
     } else {
       for (uint32_t u = tid; u < NVEC; u += blockDim.x) {
         const uint32_t r = u >> CPR_LOG, j = u & ((1u << CPR_LOG) - 1u);
-        const W w = *reinterpret_cast<const W*>(cur + swz_((r << C) | (j * VPW)));
-        st_stream(reinterpret_cast<W*>(st + row_off(r) + (uint64_t)j * VPW), w);
+        const W w = *reinterpret_cast<const W*>(cur + swz_((r << CE) | (j * VPW)));
+        st_stream(reinterpret_cast<W*>(st + roff(r) + (uint64_t)j * VPW), w);
       }
     }
     __syncthreads();
