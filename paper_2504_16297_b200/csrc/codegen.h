@@ -25,6 +25,8 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <atomic>
@@ -220,7 +222,25 @@ inline int stages_for(int L, size_t amp_bytes) {
   if (const char* e = std::getenv("PTSBE_STAGES")) return std::atoi(e) == 1 ? 1 : 2;
   return ((size_t)1 << L) * amp_bytes > (48u << 10) ? 1 : 2;
 }
-inline size_t smem_bytes_for(int L, size_t amp_bytes);   // below (smem_bytes)
+inline size_t smem_bytes_for(int L, size_t amp_bytes, int teams = 1);   // below (smem_bytes)
+
+// Compute teams per CTA (gen_prelude.cuh run_pass TEAMS): a single-buffered TMA pass runs
+// as ONE CTA per SM of two teams sharing three tile buffers -- each team finds its next
+// tile already loading while it computes -- instead of two single-buffered CTAs that each
+// wait out their own loads.  The teams are coupled (a team's next tile is loaded by the
+// other team once it frees a buffer), which costs the light, memory-bound passes what it
+// gains on the compute-heavy ones.  Measured on config 4 (complex128, 12-qubit tiles,
+// per-pass GB/s, 2 teams vs 2 CTAs): passes with 41-86 gates +3..16 %, passes with 11-30
+// gates -5..-8 % -> two teams from 40 gates (PTSBE_TEAMS_MIN_GATES); PTSBE_TEAMS = 1 / 2
+// forces one / two teams everywhere (A/B knob).
+inline int teams_for(int L, size_t amp_bytes, bool tma, int n_gates) {
+  if (!tma || stages_for(L, amp_bytes) != 1) return 1;
+  static const int force = std::getenv("PTSBE_TEAMS") ? std::atoi(std::getenv("PTSBE_TEAMS")) : 0;
+  static const int min_gates = std::getenv("PTSBE_TEAMS_MIN_GATES") ? std::atoi(std::getenv("PTSBE_TEAMS_MIN_GATES")) : 40;
+  if (force) return force >= 2 ? 2 : 1;
+  return n_gates >= min_gates ? 2 : 1;
+}
+constexpr const char* kTeamsTag = "// @@ptsbe-teams@@ ";
 
 // TMA tile staging for a pass (gen_prelude.cuh run_pass TMA): 128-B rows need the pass's
 // contiguous low run to cover a row (c64: 16 amplitudes, c128: 8) and the row table holds
@@ -620,33 +640,39 @@ inline std::string generate(const GenProgram& P) {
                      (1 << (gp.L - (P.c64 ? 4 : 3))) / 4 <= threads &&   // one gather group per issuing lane
                      make_tma_layout(P.c64, gp.L, gp.phases, GB, free_sw, &tl);
     const Swizzle sw = tma ? tl.sw : free_sw;
+    uint32_t lowm = 0;   // every bit a swizzle mask can flip (gen_prelude.cuh slot_ptr)
+    for (int b = 0; b < 32; ++b) lowm |= sw.m[b];
     if (std::getenv("PTSBE_SWIZZLE_REPORT")) {   // analysis: model wavefronts, free vs TMA layout
       auto cost = [&](const Swizzle& z) { int t = 0; for (const DevPhase& D : gp.phases) t += phase_wavefronts(z, D, GB); return t; };
       std::fprintf(stderr, "pass %zu gb %d phases %zu wavefronts: free %d tma %d\n", pi, GB, gp.phases.size(),
                    cost(free_sw), tma ? cost(tl.sw) : -1);
     }
     const std::string swname = "Swz" + std::to_string(pi);
+    const int teams = teams_for(gp.L, P.c64 ? 8 : 16, tma, n_gates);
+    if (teams > 1) min_blocks = 1;
+    const std::string tix = "ptg::gtid<" + std::to_string(threads) + ">()";   // team-local thread index
     Emitter ke(P.c64);
     std::ostringstream slow_fns;   // out-of-line slow variants of this pass's phases
     const std::vector<int> woff = hit_word_offsets(gp);
     std::ostringstream& k = ke.o;
     Cx F{1.0, 0.0};
-    k << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << min_blocks << ") "
+    k << kTeamsTag << teams << "\n"
+      << "extern \"C\" __global__ void __launch_bounds__(" << threads * teams << ", " << min_blocks << ") "
       << kernel_name((int)pi) << "(const ptg::PassParams p, const __grid_constant__ ptg::TMapDesc tm) {\n"
       << "  typedef " << ke.V << " V;\n"
       << "  ptg::run_pass<" << ke.R << ", " << gp.L << ", " << gp.c << ", " << (P.n - gp.L) << ", " << threads
       << ", " << (pi + 1 == P.passes.size() ? "true" : "false") << ", " << (tma ? "true" : "false") << ", " << (tma && !std::getenv("PTSBE_NO_TMA_STORE") ? "true" : "false")
       << ", " << (std::getenv("PTSBE_TMA_LANES") ? std::atoi(std::getenv("PTSBE_TMA_LANES")) : 32)
       << ", " << stages_for(gp.L, P.c64 ? 8 : 16) << ", " << (std::getenv("PTSBE_TMA_PREFETCH") ? "true" : "false")
-      << ">(p, &tm, "
+      << ", " << teams << ">(p, &tm, "
       << swname << "(), " << swname << "Inv(),\n"
       << "    " << scatter_fn(comp, "uint64_t") << ",\n"
       << "    " << scatter_fn(hmask, "uint32_t") << ",\n"
       << "    " << err_mask_fn(gp) << ",\n"
-      << "    [&](V* cur, int b, const uint8_t* sel, long long tile, uint64_t base, double scale, double* red,\n"
+      << "    [&](V* cur, uint32_t kofs, int b, const uint8_t* sel, long long tile, uint64_t base, double scale, double* red,\n"
       << "        uint64_t emask, const uint64_t* hits) {\n"
       << "    const bool active = "
-      << (all_active ? std::string("true") : "threadIdx.x < " + std::to_string(groups) + "u") << ";\n"
+      << (all_active ? std::string("true") : tix + " < " + std::to_string(groups) + "u") << ";\n"
       << "    V a[" << N << "];\n";
     for (size_t ph = 0; ph < gp.phases.size(); ++ph) {
       const DevPhase& D = gp.phases[ph];
@@ -739,11 +765,11 @@ inline std::string generate(const GenProgram& P) {
               << "          const V* m_ = reinterpret_cast<const V*>(p.mats) + (size_t)(" << ch.mat_base
               << " + o_) * 16;\n";
             if (ch.identity_mask & 1ull) {   // through the tile slots (no register shuffle on the no-hit path)
-              k << "          if (active) { ptg::stg<V, " << N << ", " << pb[0] << ">(a, cur, sg, so, true);\n"
+              k << "          if (active) { ptg::stg<V, " << N << ", " << pb[0] << ", " << lowm << "u>(a, cur, sg, so, true);\n"
                 << "            ptg::err_apply<V, " << GB << ", " << swname << ">(cur, gb, " << D.pbits << "u, "
             << op.arity << ", "
                 << op.k0 << ", " << k1 << ", m_);\n"
-                << "            ptg::ldg<V, " << N << ", " << pb[0] << ">(a, cur, sg, so, true, 1.0); }\n";
+                << "            ptg::ldg<V, " << N << ", " << pb[0] << ", " << lowm << "u>(a, cur, sg, so, true, 1.0); }\n";
             } else {
               if (op.arity == 1) k << "          ptg::g1<" << op.k0 << ">(a, m_[0], m_[1], m_[4], m_[5]);\n";
               else k << "          ptg::g2<" << op.k0 << ", " << k1 << ">(a, m_);\n";
@@ -763,8 +789,8 @@ inline std::string generate(const GenProgram& P) {
             k << "      { double s_ = 0.0;\n"
               << "#pragma unroll\n"
               << "        for (int j = 0; j < " << N << "; ++j) s_ += ptg::prob64(a[j]);\n"
-              << "        s_ = ptg::block_sum(s_, red);\n"
-              << "        if (threadIdx.x == 0) p.partials[((size_t)" << op.slot
+              << "        s_ = ptg::block_sum<" << threads << ">(s_, red);\n"
+              << "        if (" << tix << " == 0) p.partials[((size_t)" << op.slot
               << " * p.B + b) * p.tiles + tile] = s_; }\n";
           }
         }
@@ -773,15 +799,15 @@ inline std::string generate(const GenProgram& P) {
       };
       auto emit_block = [&](bool slow) {
         if (gloop > 1)
-          k << "    #pragma unroll 1\n    for (uint32_t g = threadIdx.x; g < " << groups << "u; g += " << threads
+          k << "    #pragma unroll 1\n    for (uint32_t g = " << tix << "; g < " << groups << "u; g += " << threads
             << "u) {\n";
         else
-          k << "    { const uint32_t g = threadIdx.x;\n";
+          k << "    { const uint32_t g = " << tix << ";\n";
         k << "      const uint32_t gb = ";
         for (int q = 0; q < GB; ++q) k << "ptg::ins0(";
         k << "g";
         for (int q = 0; q < GB; ++q) k << ", " << pb[q] << ")";
-        k << ";\n      const uint32_t sg = " << swname << "()(gb);\n      const uint32_t so[" << N << "] = {";
+        k << ";\n      const uint32_t sg = " << swname << "()(gb) | kofs;\n      const uint32_t so[" << N << "] = {";
         for (int j = 0; j < N; ++j) k << so[j] << "u" << (j + 1 < N ? ", " : "");
         k << "};\n";
         if (ph == 0) {
@@ -789,18 +815,18 @@ inline std::string generate(const GenProgram& P) {
           for (int j = 0; j < N; ++j) k << off[j] << "u" << (j + 1 < N ? ", " : "");
           k << "};\n"
             << "      if (p.gen_zero) ptg::zerog(a, base, gb, off, active && p.gen_zero == 1, GZERO_RE, GZERO_IM);\n"
-            << "      else ptg::ldg<V, " << N << ", " << pb[0] << ">(a, cur, sg, so, active, scale);\n";
+            << "      else ptg::ldg<V, " << N << ", " << pb[0] << ", " << lowm << "u>(a, cur, sg, so, active, scale);\n";
           if (pi == 0)   // a loaded (not synthesized) input also needs the global phase G
             k << "      if (!p.gen_zero) ptg::cscale(a, ptg::mk((V*)0, GZERO_RE, GZERO_IM));\n";
         } else {
-          k << "      ptg::ldg<V, " << N << ", " << pb[0] << ">(a, cur, sg, so, active, 1.0);\n";
+          k << "      ptg::ldg<V, " << N << ", " << pb[0] << ", " << lowm << "u>(a, cur, sg, so, active, 1.0);\n";
         }
         const Cx f = emit_ops(slow);
         if (last) {
           const double mag = cxabs(cxmul(F, f));
           if (mag != 1.0) k << "      ptg::rscale(a, " << hexd(mag) << ");\n";
         }
-        k << "      ptg::stg<V, " << N << ", " << pb[0] << ">(a, cur, sg, so, active);\n"
+        k << "      ptg::stg<V, " << N << ", " << pb[0] << ", " << lowm << "u>(a, cur, sg, so, active);\n"
           << "    }\n";
         return f;
       };
@@ -820,7 +846,7 @@ inline std::string generate(const GenProgram& P) {
         // segment (the common case) runs a function several times smaller than the full one,
         // which matters because slow code is instruction-fetch bound.
         const std::string base_name = "ptsbe_slow_" + std::to_string(pi) + "_" + std::to_string(ph);
-        const char* args = "(p.mats, p.partials, p.B, p.tiles, p.gen_zero, cur, b, sel, tile, base, scale, red, active, "
+        const char* args = "(p.mats, p.partials, p.B, p.tiles, p.gen_zero, cur + kofs, b, sel, tile, base, scale, red, active, "
                            "hits)";
         auto emit_variant = [&](const std::string& fname, int lo, int hi) {
           const std::string before = k.str();
@@ -834,6 +860,7 @@ inline std::string generate(const GenProgram& P) {
                    << "long long tiles_, int gen_zero_, " << ke.V << "* cur, int b, const uint8_t* sel, long long tile, "
                    << "uint64_t base, double scale, double* red, bool active, const uint64_t* hits) {\n"
                    << "  typedef " << ke.V << " V;\n"
+                   << "  const uint32_t kofs = 0u;   // cur is this tile's buffer\n"
                    << "  struct { const void* mats; double* partials; int B; long long tiles; int gen_zero; } p = "
                    << "{mats_, partials_, B_, tiles_, gen_zero_};\n"
                    << "  V a[" << N << "];\n"
@@ -861,7 +888,7 @@ inline std::string generate(const GenProgram& P) {
         emit_variant(base_name, 0, 1 << 30);
       }
       F = cxmul(F, Fph);
-      k << "      __syncthreads();\n";
+      k << "      ptg::gsync<" << threads << ">();\n";
       k << "    }\n";
     }
     k << "  });\n}\n";
@@ -880,6 +907,7 @@ inline std::string generate(const GenProgram& P) {
 struct Module {
   std::vector<CUmodule> mods;
   std::vector<CUfunction> fns;
+  std::vector<int> teams;   // compute teams per CTA of each pass kernel (kTeamsTag in its source)
 };
 
 // One NVRTC program per pass (shared header: prelude + global-phase defines),
@@ -950,18 +978,21 @@ inline bool compile(const std::string& src, int n_passes, int dev, Module& out, 
     if (A.get_function(&f, mod, kernel_name(i).c_str()) != CUDA_SUCCESS) { err = "cuModuleGetFunction failed"; return false; }
     A.func_set_attr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, 227 * 1024);
     m.fns.push_back(f);
+    const size_t tp = parts[i].find(kTeamsTag, header.size());
+    m.teams.push_back(tp == std::string::npos ? 1 : std::max(1, std::atoi(parts[i].c_str() + tp + std::strlen(kTeamsTag))));
   }
   cache[key] = m;
   out = m;
   return true;
 }
 
-inline size_t smem_bytes_for(int L, size_t amp_bytes) {
-  // [1024-B alignment slack for TMA's 128-B swizzle] tiles | mbarriers | red | emask | hits | TMA row table
-  return 1024 + (size_t)stages_for(L, amp_bytes) * ((size_t)1 << L) * amp_bytes + 16 + 32 * 8 + 16 +
-         8 * kMaxHitWords + 16 * 128;
+inline size_t smem_bytes_for(int L, size_t amp_bytes, int teams) {
+  // [1024-B alignment slack for TMA's 128-B swizzle] tile buffers (three for two teams) |
+  // mbarriers + stamps | red | emask | hits per team | TMA row table (gen_prelude.cuh run_pass)
+  const size_t nbuf = teams > 1 ? 3 : (size_t)stages_for(L, amp_bytes);
+  return 1024 + nbuf * ((size_t)1 << L) * amp_bytes + 64 + 32 * 8 + 16 + 8 * kMaxHitWords * (size_t)teams + 16 * 128;
 }
-inline size_t smem_bytes(int L, int /*c*/, size_t amp_bytes) { return smem_bytes_for(L, amp_bytes); }
+inline size_t smem_bytes(int L, int /*c*/, size_t amp_bytes, int teams = 1) { return smem_bytes_for(L, amp_bytes, teams); }
 
 }  // namespace gen
 }  // namespace ptsbe

@@ -271,22 +271,39 @@ __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_g
 __device__ __forceinline__ void st_stream(float4* p, float4 v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(double2* p, double2 v) { __stcs(p, v); }
 
-__device__ __forceinline__ double block_sum(double v, double* red) {
+// A CTA runs one or two compute TEAMS of NT threads (run_pass TEAMS): generated code
+// addresses its team-local thread index and synchronises its team only (named
+// barrier 1 + team; with one team that is the whole CTA).
+template <int NT> __device__ __forceinline__ uint32_t gtid() { return threadIdx.x & (uint32_t)(NT - 1); }
+template <int NT> __device__ __forceinline__ void gsync() {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(1u + threadIdx.x / (uint32_t)NT), "n"(NT) : "memory");
+}
+
+template <int NT> __device__ __forceinline__ double block_sum(double v, double* red) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
+  const uint32_t t = gtid<NT>();
+  if ((t & 31) == 0) red[t >> 5] = v;
+  gsync<NT>();
   double r = 0.0;
-  if (threadIdx.x == 0) {
-    const int nw = (blockDim.x + 31) >> 5;
-    for (int i = 0; i < nw; ++i) r += red[i];
+  if (t == 0) {
+    for (int i = 0; i < (NT + 31) / 32; ++i) r += red[i];
   }
-  __syncthreads();
+  gsync<NT>();
   return r;
 }
 
 // ---- phase register load / store (N amplitudes at sg ^ so[j]; so[] literal)
-template <typename V, int N, int P0>
+// The swizzle flips only the bits M (codegen.h: OR of its masks), and a phase's register
+// offsets are disjoint from the thread's base outside M, so
+//   sg ^ so[j] == (sg ^ (so[j] & M)) + (so[j] & ~M):
+// one base register per distinct low pattern of the phase and every access an immediate
+// offset from it -- no per-access address arithmetic.
+template <uint32_t M, typename V>
+__device__ __forceinline__ V* slot_ptr(V* cur, uint32_t sg, uint32_t so) {
+  return cur + (sg ^ (so & M)) + (so & ~M);
+}
+template <typename V, int N, int P0, uint32_t M>
 __device__ __forceinline__ void ldg(V (&a)[N], const V* cur, uint32_t sg, const uint32_t* so, bool active,
                                     double scale) {
   if (!active) {
@@ -297,28 +314,28 @@ __device__ __forceinline__ void ldg(V (&a)[N], const V* cur, uint32_t sg, const 
   if (sizeof(V) == 8 && P0 == 0) {      // bit 0 in the phase: adjacent pairs, 16-B accesses
 #pragma unroll
     for (int j = 0; j < N; j += 2) {
-      const float4 w = *reinterpret_cast<const float4*>(cur + (sg ^ so[j]));
+      const float4 w = *reinterpret_cast<const float4*>(slot_ptr<M>(cur, sg, so[j]));
       a[j] = mk((V*)0, w.x, w.y);
       a[j + 1] = mk((V*)0, w.z, w.w);
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < N; ++j) a[j] = cur[sg ^ so[j]];
+    for (int j = 0; j < N; ++j) a[j] = *slot_ptr<M>(cur, sg, so[j]);
   }
   if (scale != 1.0) rscale(a, scale);
 }
-template <typename V, int N, int P0>
+template <typename V, int N, int P0, uint32_t M>
 __device__ __forceinline__ void stg(const V (&a)[N], V* cur, uint32_t sg, const uint32_t* so, bool active) {
   if (!active) return;
   if (sizeof(V) == 8 && P0 == 0) {
 #pragma unroll
     for (int j = 0; j < N; j += 2) {
       float4 w; w.x = a[j].x; w.y = a[j].y; w.z = a[j + 1].x; w.w = a[j + 1].y;
-      *reinterpret_cast<float4*>(cur + (sg ^ so[j])) = w;
+      *reinterpret_cast<float4*>(slot_ptr<M>(cur, sg, so[j])) = w;
     }
   } else {
 #pragma unroll
-    for (int j = 0; j < N; ++j) cur[sg ^ so[j]] = a[j];
+    for (int j = 0; j < N; ++j) *slot_ptr<M>(cur, sg, so[j]) = a[j];
   }
 }
 // A non-default outcome (slow variant of a phase): the thread's N amplitudes are
@@ -387,7 +404,7 @@ __device__ __forceinline__ void zerog(V (&a)[N], uint64_t base, uint32_t gb, con
 // scale, red, emask, hits) runs
 // the pass's phases on one tile.
 template <typename R, int L, int C, int TLOG, int NT, bool SUMS, bool TMA, bool TMA_ST, int TMA_LANES, int STAGES,
-          bool TMA_PF, class Sw, class SlotInv, class TileBase, class RowOff, class ErrMask, class Body>
+          bool TMA_PF, int TEAMS, class Sw, class SlotInv, class TileBase, class RowOff, class ErrMask, class Body>
 __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm, Sw swz_, SlotInv slot_inv,
                                          TileBase tile_base, RowOff row_off, ErrMask err_mask, Body body) {
   typedef typename Cplx<R>::V V;
@@ -412,16 +429,25 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // TMA's 128-B swizzle needs 1024-B aligned tiles (the engine adds the slack)
   unsigned char* smem = TMA ? smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) : smem_raw;
+  // layout (codegen.h smem_bytes_for): tile buffers | 4 mbarriers + 4 stamps | red[32] | emask[2] |
+  // hit words per team | TMA row table
+  constexpr int NBUF = TEAMS > 1 ? 3 : STAGES;
   V* buf0 = reinterpret_cast<V*>(smem);
   V* buf1 = STAGES == 2 ? buf0 + TL : buf0;   // one buffer: tiles load after the previous one is stored
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(buf1 + TL);   // TMA: one transaction barrier per tile buffer
-  double* red = reinterpret_cast<double*>(mbar + 2);
-  uint64_t* emask_s = reinterpret_cast<uint64_t*>(red + 32);
-  uint64_t* hits_s = emask_s + 2;   // per-phase hit words (codegen.h err_mask_fn)
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(buf0 + (size_t)NBUF * TL);   // TMA: one transaction barrier per buffer
+  volatile int* stamp = reinterpret_cast<volatile int*>(mbar + 4);   // teams: tile counter loaded per buffer
+  double* red_all = reinterpret_cast<double*>(mbar + 8);
+  uint64_t* emask_all = reinterpret_cast<uint64_t*>(red_all + 32);
+  uint64_t* hits_all = emask_all + 2;   // per-phase hit words (codegen.h err_mask_fn), one set per team
   // TMA: tile-relative row coordinates of each gather group (shared-memory slots 4g..4g+3)
-  uint4* rowtab = reinterpret_cast<uint4*>(hits_s + PTG_MAX_HIT_WORDS);
+  uint4* rowtab = reinterpret_cast<uint4*>(hits_all + TEAMS * PTG_MAX_HIT_WORDS);
+  static_assert(TEAMS == 1 || NT <= 512, "two teams: at most 16 warps each (red)");
+  const uint32_t team = TEAMS > 1 ? threadIdx.x / (uint32_t)NT : 0u;
+  double* red = red_all + team * 16u;
+  uint64_t* emask_s = emask_all + team;
+  uint64_t* hits_s = hits_all + (size_t)team * PTG_MAX_HIT_WORDS;
   int lb = -1;
-  const uint32_t tid = threadIdx.x;
+  const uint32_t tid = gtid<NT>();   // team-local
   auto roff = [&](uint32_t r) -> uint64_t {
     return ((uint64_t)(r & ((1u << (C - CE)) - 1u)) << CE) | row_off(r >> (C - CE));
   };
@@ -454,7 +480,7 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
       for (int k = 0; k < ITER; ++k)
         cp_async16(dst + (s0 ^ swz_((uint32_t)(k * RSTEP) << CE)), src + g0 + roff((uint32_t)(k * RSTEP)));
     } else {
-      for (uint32_t u = tid; u < NVEC; u += blockDim.x) {
+      for (uint32_t u = tid; u < NVEC; u += NT) {
         const uint32_t r = u >> CPR_LOG, j = u & ((1u << CPR_LOG) - 1u);
         cp_async16(dst + swz_((r << CE) | (j * VPW)), src + roff(r) + (uint64_t)j * VPW);
       }
@@ -472,7 +498,7 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
   const int gi = (int)(tid >> 5) * PERW + (int)lane;            // this thread's gather group
   const bool issuer = TMA && lane < (uint32_t)PERW && gi < NGRP;
   auto tma_load = [&](long long tt, int k) {
-    V* dst = k ? buf1 : buf0;
+    V* dst = buf0 + (size_t)k * TL;   // buffer k (two stages: buf1 = buf0 + TL; teams: three buffers)
     const int e = (int)(tt >> TLOG);
     if (e != le) {
       le = e;
@@ -512,62 +538,9 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
     bulk_commit();
   };
 
-  long long t = blockIdx.x;
-  if (TMA && STAGES == 1) {   // single buffer: loads issued at the top of each iteration
-    for (int g = (int)tid; g < NGRP; g += NT) {
-      uint32_t q4[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t u = slot_inv((uint32_t)(4 * g + q));
-        q4[q] = (uint32_t)((((uint64_t)(u & ((1u << (C - LOGU)) - 1u)) << LOGU) | row_off(u >> (C - LOGU))) >> LOGU);
-      }
-      rowtab[g] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
-    }
-    if (tid == 0) mbar_init(&mbar[0], NISSUE);
-    __syncthreads();
-  } else if (TMA) {
-    for (int g = (int)tid; g < NGRP; g += NT) {
-      uint32_t q4[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {   // tile row in shared-memory slot 4g+q: slot^-1, then its row offset
-        const uint32_t u = slot_inv((uint32_t)(4 * g + q));
-        q4[q] = (uint32_t)((((uint64_t)(u & ((1u << (C - LOGU)) - 1u)) << LOGU) | row_off(u >> (C - LOGU))) >> LOGU);
-      }
-      rowtab[g] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
-    }
-    if (tid == 0) {
-      mbar_init(&mbar[0], NISSUE);
-      mbar_init(&mbar[1], NISSUE);
-    }
-    __syncthreads();
-    if (t < total) tma_load(t, 0);
-  } else if (STAGES == 2) {
-    if (t < total) load_tile(t, buf0);
-    cp_async_commit();
-  }
-  for (int it = 0; t < total; t += gridDim.x, ++it) {
-    V* cur = (it & 1) ? buf1 : buf0;
-    V* nxt = (it & 1) ? buf0 : buf1;
-    if (STAGES == 1) {
-      if (TMA) {
-        tma_load(t, 0);
-        mbar_wait(&mbar[0], (uint32_t)it & 1u);
-        if (TMA_PF && t + gridDim.x < total) tma_prefetch(t + gridDim.x);
-      } else {
-        load_tile(t, buf0);
-        cp_async_commit();
-        cp_async_wait0();
-        __syncthreads();
-      }
-    } else if (TMA) {
-      if (t + gridDim.x < total) tma_load(t + gridDim.x, (it + 1) & 1);
-      mbar_wait(&mbar[it & 1], (uint32_t)(it >> 1) & 1u);
-    } else {
-      if (t + gridDim.x < total) load_tile(t + gridDim.x, nxt);
-      cp_async_commit();
-      cp_async_wait1();
-      __syncthreads();
-    }
+  // One tile: entry bookkeeping, the pass's phases, store (+ fused sampler sums).  Only the
+  // calling team takes part (gsync: the whole CTA when TEAMS == 1).
+  auto process = [&](long long t, V* cur) {
     if ((int)(t >> TLOG) != ce) {
       ce = (int)(t >> TLOG);
       cen = p.ent[ce];
@@ -577,21 +550,26 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
     const int4 en = cen;
     const int b = en.x;                          // trajectory row
     const long long tile = t & ((1ll << TLOG) - 1);
-    if (cdead) continue;
+    if (cdead) return;
     if (b != lb) {   // per trajectory, once: which phases see a non-default outcome
       if (tid == 0) *emask_s = err_mask(p.sel + (size_t)b * p.S, hits_s);
-      __syncthreads();
+      gsync<NT>();
       lb = b;
     }
     const uint64_t emask = *emask_s;
     const uint64_t base = tile_base((uint64_t)tile);
     const double scale = cscale_v;
-    body(cur, b, p.sel + (size_t)b * p.S, tile, base, scale, red, emask, hits_s);
+    // the phases address buf0 + (kofs | slot): tile-buffer offset kofs (a multiple of 2^L) ORed into
+    // each phase's per-thread base, so every shared-memory access keeps a fixed base register
+    // (opaque to the compiler: it would otherwise split the OR back into a per-access add)
+    uint32_t kofs = (uint32_t)(cur - buf0);
+    if (TEAMS > 1) asm volatile("mov.b32 %0, %0;\n" : "+r"(kofs));
+    body(buf0, kofs, b, p.sel + (size_t)b * p.S, tile, base, scale, red, emask, hits_s);
     V* st = reinterpret_cast<V*>(p.states) + ((size_t)en.z << p.n) + base;
     if (TMA && TMA_ST) {
       // the phases' shared-memory writes must be visible to the async proxy before the scatter
       fence_proxy_async();
-      __syncthreads();
+      gsync<NT>();
       tma_store(cur, (long long)en.z << p.n, base);
       if (SUMS && FAST && p.tsum) {   // fused sampler block sums straight from the tile (see below)
         constexpr int PER_THREAD = ITER * VPW;
@@ -639,13 +617,113 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
         st_stream(reinterpret_cast<W*>(st + g0 + roff((uint32_t)(k * RSTEP))), w);
       }
     } else {
-      for (uint32_t u = tid; u < NVEC; u += blockDim.x) {
+      for (uint32_t u = tid; u < NVEC; u += NT) {
         const uint32_t r = u >> CPR_LOG, j = u & ((1u << CPR_LOG) - 1u);
         const W w = *reinterpret_cast<const W*>(cur + swz_((r << CE) | (j * VPW)));
         st_stream(reinterpret_cast<W*>(st + roff(r) + (uint64_t)j * VPW), w);
       }
     }
+    gsync<NT>();
+  };
+  auto fill_rowtab = [&]() {   // tile row in shared-memory slot 4g+q: slot^-1, then its row offset
+    for (int g = (int)threadIdx.x; g < NGRP; g += NT * TEAMS) {
+      uint32_t q4[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t u = slot_inv((uint32_t)(4 * g + q));
+        q4[q] = (uint32_t)((((uint64_t)(u & ((1u << (C - LOGU)) - 1u)) << LOGU) | row_off(u >> (C - LOGU))) >> LOGU);
+      }
+      rowtab[g] = make_uint4(q4[0], q4[1], q4[2], q4[3]);
+    }
+  };
+
+  if constexpr (TEAMS > 1) {
+    // Two compute teams share three tile buffers (single-buffered 64-KB tiles, one CTA of
+    // 2 x NT threads per SM).  The CTA's i-th tile (t = blockIdx + i * grid) lives in buffer
+    // i % 3 and is computed by team i % 2; when a team has stored tile i it loads tile i + 3
+    // -- the other team's -- into the freed buffer.  A team therefore finds its next tile
+    // already in flight while it computes, instead of exposing the whole load latency as a
+    // single-buffered CTA does (ncu, 12-qubit c128 tiles at 2 CTAs/SM: long-scoreboard
+    // stalls on the tile barrier 31 % of the warp cycles).
+    static_assert(TMA && TMA_ST && STAGES == 1, "compute teams need TMA single-buffered tiles");
+    // An mbarrier wait by parity only tells the current phase from the previous one, so a
+    // team must not wait for tile i before the load of tile i was issued (the buffer's
+    // previous phase -- tile i - 3, the other team's -- may still be open, e.g. when this
+    // team raced through dead tiles): the issuing team's thread 0 stamps the buffer with i
+    // once it has consumed tile i - 3, and the waiter first spins on the stamp.
+    fill_rowtab();
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < 3; ++k) {
+        mbar_init(&mbar[k], NISSUE);
+        stamp[k] = k;
+      }
+    }
     __syncthreads();
+    const long long t0 = blockIdx.x, step = gridDim.x;
+    if (team == 0) {
+      if (t0 < total) tma_load(t0, 0);
+      if (t0 + 2 * step < total) tma_load(t0 + 2 * step, 2);
+    } else if (t0 + step < total) {
+      tma_load(t0 + step, 1);
+    }
+    for (long long i = team;; i += 2) {
+      const long long t = t0 + i * step;
+      if (t >= total) break;
+      const int k = (int)(i % 3);
+      V* cur = buf0 + (size_t)k * TL;
+      while (stamp[k] != (int)i) __nanosleep(64);
+      mbar_wait(&mbar[k], (uint32_t)(i / 3) & 1u);
+      process(t, cur);
+      if (t + 3 * step < total) {
+        if (tid == 0) stamp[k] = (int)(i + 3);   // this team has consumed tile i (its phase is complete)
+        tma_load(t + 3 * step, k);   // issuers: after their scatters have read the buffer
+      }
+    }
+    if (issuer) bulk_wait0();   // the last scatters must be done with shared memory before the CTA exits
+    return;
+  }
+
+  long long t = blockIdx.x;
+  if (TMA && STAGES == 1) {   // single buffer: loads issued at the top of each iteration
+    fill_rowtab();
+    if (tid == 0) mbar_init(&mbar[0], NISSUE);
+    __syncthreads();
+  } else if (TMA) {
+    fill_rowtab();
+    if (tid == 0) {
+      mbar_init(&mbar[0], NISSUE);
+      mbar_init(&mbar[1], NISSUE);
+    }
+    __syncthreads();
+    if (t < total) tma_load(t, 0);
+  } else if (STAGES == 2) {
+    if (t < total) load_tile(t, buf0);
+    cp_async_commit();
+  }
+  for (int it = 0; t < total; t += gridDim.x, ++it) {
+    V* cur = (it & 1) ? buf1 : buf0;
+    V* nxt = (it & 1) ? buf0 : buf1;
+    if (STAGES == 1) {
+      if (TMA) {
+        tma_load(t, 0);
+        mbar_wait(&mbar[0], (uint32_t)it & 1u);
+        if (TMA_PF && t + gridDim.x < total) tma_prefetch(t + gridDim.x);
+      } else {
+        load_tile(t, buf0);
+        cp_async_commit();
+        cp_async_wait0();
+        __syncthreads();
+      }
+    } else if (TMA) {
+      if (t + gridDim.x < total) tma_load(t + gridDim.x, (it + 1) & 1);
+      mbar_wait(&mbar[it & 1], (uint32_t)(it >> 1) & 1u);
+    } else {
+      if (t + gridDim.x < total) load_tile(t + gridDim.x, nxt);
+      cp_async_commit();
+      cp_async_wait1();
+      __syncthreads();
+    }
+    process(t, cur);
   }
   if (TMA && TMA_ST) {
     if (issuer) bulk_wait0();   // the last scatters must be done with shared memory before the CTA exits
