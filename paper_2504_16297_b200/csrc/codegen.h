@@ -222,7 +222,7 @@ inline int stages_for(int L, size_t amp_bytes) {
   if (const char* e = std::getenv("PTSBE_STAGES")) return std::atoi(e) == 1 ? 1 : 2;
   return ((size_t)1 << L) * amp_bytes > (48u << 10) ? 1 : 2;
 }
-inline size_t smem_bytes_for(int L, size_t amp_bytes, int teams = 1);   // below (smem_bytes)
+inline size_t smem_bytes_for(int L, size_t amp_bytes, int teams = 1, int stages = 0);   // below (smem_bytes)
 
 // Compute teams per CTA (gen_prelude.cuh run_pass TEAMS): a single-buffered TMA pass runs
 // as ONE CTA per SM of two teams sharing three tile buffers -- each team finds its next
@@ -240,7 +240,17 @@ inline int teams_for(int L, size_t amp_bytes, bool tma, int n_gates) {
   if (force) return force >= 2 ? 2 : 1;
   return n_gates >= min_gates ? 2 : 1;
 }
-constexpr const char* kTeamsTag = "// @@ptsbe-teams@@ ";
+// Tile buffers of a one-team pass.  Light complex128 passes (below the teams threshold:
+// memory-bound, little FP64 work per tile) on single-buffered 64-KB tiles run as ONE CTA
+// per SM with three buffers instead: two tiles stream in while one computes
+// (PTSBE_LIGHT_STAGES = 1 keeps two single-buffered CTAs per SM).
+inline int pass_stages(int L, size_t amp_bytes, bool tma, int teams) {
+  const int st = stages_for(L, amp_bytes);
+  if (teams > 1 || st != 1 || !tma) return st;
+  static const int light = std::getenv("PTSBE_LIGHT_STAGES") ? std::atoi(std::getenv("PTSBE_LIGHT_STAGES")) : 1;
+  return light >= 3 ? 3 : 1;
+}
+constexpr const char* kTeamsTag = "// @@ptsbe-teams@@ ";   // "<teams> <stages>" of a pass kernel
 
 // TMA tile staging for a pass (gen_prelude.cuh run_pass TMA): 128-B rows need the pass's
 // contiguous low run to cover a row (c64: 16 amplitudes, c128: 8) and the row table holds
@@ -422,11 +432,21 @@ struct Emitter {
   void dmul(int j, Cx d) {
     if (d.re == 1.0 && d.im == 0.0) return;
     o << "      ";
-    if (d.im == 0.0 && d.re == -1.0) o << "a[" << j << "] = ptg::pmul(a[" << j << "], ptg::bc<" << V << ">((" << R << ")-1));\n";
-    else if (d.re == 0.0 && (d.im == 1.0 || d.im == -1.0))
-      o << "a[" << j << "] = ptg::pmul(ptg::ix(a[" << j << "]), ptg::bc<" << V << ">((" << R << ")" << (d.im > 0 ? "1" : "-1")
-        << "));\n";
+    // -1, +i, -i: sign flips and a re/im swap (operand modifiers / renaming, no multiply)
+    if (d.im == 0.0 && d.re == -1.0) o << "a[" << j << "] = ptg::neg(a[" << j << "]);\n";
+    else if (d.re == 0.0 && d.im == 1.0) o << "a[" << j << "] = ptg::ix(a[" << j << "]);\n";
+    else if (d.re == 0.0 && d.im == -1.0) o << "a[" << j << "] = ptg::neg(ptg::ix(a[" << j << "]));\n";
     else o << "a[" << j << "] = ptg::cmul(" << lit(d.re, d.im) << ", a[" << j << "]);\n";
+  }
+  // A merged diagonal entry (a product of several gates' entries) within a few ulps of
+  // +-1 or +-i is taken as exactly that value: the product's rounding residue (e.g. T * T =
+  // 2^-52 + i) is below the fp64 parity tolerance, and the exact value costs no multiply.
+  static Cx snap(Cx d) {
+    const double eps = 0x1p-49;
+    auto near = [&](double x, double v) { return std::fabs(x - v) <= eps; };
+    if (std::fabs(d.im) <= eps && (near(d.re, 1.0) || near(d.re, -1.0))) return {d.re > 0 ? 1.0 : -1.0, 0.0};
+    if (std::fabs(d.re) <= eps && (near(d.im, 1.0) || near(d.im, -1.0))) return {0.0, d.im > 0 ? 1.0 : -1.0};
+    return d;
   }
 
   // Emit one gate.  With `scaled`, a factor f is pulled out of the matrix
@@ -649,21 +669,27 @@ inline std::string generate(const GenProgram& P) {
     }
     const std::string swname = "Swz" + std::to_string(pi);
     const int teams = teams_for(gp.L, P.c64 ? 8 : 16, tma, n_gates);
-    if (teams > 1) min_blocks = 1;
+    const int stages = pass_stages(gp.L, P.c64 ? 8 : 16, tma, teams);
+    if (teams > 1 || stages > 2) min_blocks = 1;
+    else if (!P.c64 && stages == 1 && threads == 256) {
+      // light single-buffered c128 passes: CTAs per SM (2: <= 128 registers, 3: <= 85)
+      static const int lb = std::getenv("PTSBE_LIGHT_BLOCKS") ? std::atoi(std::getenv("PTSBE_LIGHT_BLOCKS")) : 2;
+      min_blocks = std::max(1, std::min(lb, 3));
+    }
     const std::string tix = "ptg::gtid<" + std::to_string(threads) + ">()";   // team-local thread index
     Emitter ke(P.c64);
     std::ostringstream slow_fns;   // out-of-line slow variants of this pass's phases
     const std::vector<int> woff = hit_word_offsets(gp);
     std::ostringstream& k = ke.o;
     Cx F{1.0, 0.0};
-    k << kTeamsTag << teams << "\n"
+    k << kTeamsTag << teams << " " << stages << "\n"
       << "extern \"C\" __global__ void __launch_bounds__(" << threads * teams << ", " << min_blocks << ") "
       << kernel_name((int)pi) << "(const ptg::PassParams p, const __grid_constant__ ptg::TMapDesc tm) {\n"
       << "  typedef " << ke.V << " V;\n"
       << "  ptg::run_pass<" << ke.R << ", " << gp.L << ", " << gp.c << ", " << (P.n - gp.L) << ", " << threads
       << ", " << (pi + 1 == P.passes.size() ? "true" : "false") << ", " << (tma ? "true" : "false") << ", " << (tma && !std::getenv("PTSBE_NO_TMA_STORE") ? "true" : "false")
       << ", " << (std::getenv("PTSBE_TMA_LANES") ? std::atoi(std::getenv("PTSBE_TMA_LANES")) : 32)
-      << ", " << stages_for(gp.L, P.c64 ? 8 : 16) << ", " << (std::getenv("PTSBE_TMA_PREFETCH") ? "true" : "false")
+      << ", " << stages << ", " << (std::getenv("PTSBE_TMA_PREFETCH") ? "true" : "false")
       << ", " << teams << ">(p, &tm, "
       << swname << "(), " << swname << "Inv(),\n"
       << "    " << scatter_fn(comp, "uint64_t") << ",\n"
@@ -713,7 +739,7 @@ inline std::string generate(const GenProgram& P) {
         const bool merge_diag = !std::getenv("PTSBE_NO_DIAG_MERGE");
         auto flush = [&]() {
           if (!pmask) return;
-          for (int j = 0; j < N; ++j) ke.dmul(j, pend[j]);
+          for (int j = 0; j < N; ++j) ke.dmul(j, Emitter::snap(pend[j]));
           std::fill(pend.begin(), pend.end(), Cx{1.0, 0.0});
           pmask = 0;
         };
@@ -907,7 +933,8 @@ inline std::string generate(const GenProgram& P) {
 struct Module {
   std::vector<CUmodule> mods;
   std::vector<CUfunction> fns;
-  std::vector<int> teams;   // compute teams per CTA of each pass kernel (kTeamsTag in its source)
+  std::vector<int> teams;    // compute teams per CTA of each pass kernel (kTeamsTag in its source)
+  std::vector<int> stages;   // tile buffers of a one-team pass kernel (kTeamsTag)
 };
 
 // One NVRTC program per pass (shared header: prelude + global-phase defines),
@@ -979,20 +1006,25 @@ inline bool compile(const std::string& src, int n_passes, int dev, Module& out, 
     A.func_set_attr(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, 227 * 1024);
     m.fns.push_back(f);
     const size_t tp = parts[i].find(kTeamsTag, header.size());
-    m.teams.push_back(tp == std::string::npos ? 1 : std::max(1, std::atoi(parts[i].c_str() + tp + std::strlen(kTeamsTag))));
+    int tv = 1, sv = 0;
+    if (tp != std::string::npos) std::sscanf(parts[i].c_str() + tp + std::strlen(kTeamsTag), "%d %d", &tv, &sv);
+    m.teams.push_back(std::max(1, tv));
+    m.stages.push_back(sv);
   }
   cache[key] = m;
   out = m;
   return true;
 }
 
-inline size_t smem_bytes_for(int L, size_t amp_bytes, int teams) {
+inline size_t smem_bytes_for(int L, size_t amp_bytes, int teams, int stages) {
   // [1024-B alignment slack for TMA's 128-B swizzle] tile buffers (three for two teams) |
   // mbarriers + stamps | red | emask | hits per team | TMA row table (gen_prelude.cuh run_pass)
-  const size_t nbuf = teams > 1 ? 3 : (size_t)stages_for(L, amp_bytes);
+  const size_t nbuf = teams > 1 ? 3 : stages > 0 ? (size_t)stages : (size_t)stages_for(L, amp_bytes);
   return 1024 + nbuf * ((size_t)1 << L) * amp_bytes + 64 + 32 * 8 + 16 + 8 * kMaxHitWords * (size_t)teams + 16 * 128;
 }
-inline size_t smem_bytes(int L, int /*c*/, size_t amp_bytes, int teams = 1) { return smem_bytes_for(L, amp_bytes, teams); }
+inline size_t smem_bytes(int L, int /*c*/, size_t amp_bytes, int teams = 1, int stages = 0) {
+  return smem_bytes_for(L, amp_bytes, teams, stages);
+}
 
 }  // namespace gen
 }  // namespace ptsbe

@@ -419,7 +419,8 @@ int launch_passes(ptsbe_engine* h, int B, bool from_zero, int p_begin = 0, int p
     if (h->gen_active) {
       const int teams = pi < h->gen_mod.teams.size() ? h->gen_mod.teams[pi] : 1;
       const unsigned threads = (unsigned)gen::threads_for(ph.L, ph.gb, ph.n_slots > 0) * (unsigned)teams;
-      const size_t gsm = gen::smem_bytes(ph.L, ph.c, sizeof(typename Cplx<R>::V), teams);
+      const int stages = pi < h->gen_mod.stages.size() ? h->gen_mod.stages[pi] : 0;
+      const size_t gsm = gen::smem_bytes(ph.L, ph.c, sizeof(typename Cplx<R>::V), teams, stages);
       CUfunction f = h->gen_mod.fns[pi];
       int per_sm = 0;
       if (gen::api().occupancy(&per_sm, f, (int)threads, gsm) != CUDA_SUCCESS) per_sm = 1;

@@ -64,6 +64,7 @@ __device__ __forceinline__ double2 pmul(double2 a, double2 b) { return make_doub
 __device__ __forceinline__ double2 padd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 template <typename V, typename S> __device__ __forceinline__ V bc(S s) { V r; r.x = s; r.y = s; return r; }
 template <typename V> __device__ __forceinline__ V ix(V x) { V r; r.x = -x.y; r.y = x.x; return r; }   // i * x
+template <typename V> __device__ __forceinline__ V neg(V x) { V r; r.x = -x.x; r.y = -x.y; return r; }
 
 template <typename V> __device__ __forceinline__ V cmul(V d, V x) {     // d * x
   typedef decltype(d.x) R;
@@ -433,7 +434,7 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
   // hit words per team | TMA row table
   constexpr int NBUF = TEAMS > 1 ? 3 : STAGES;
   V* buf0 = reinterpret_cast<V*>(smem);
-  V* buf1 = STAGES == 2 ? buf0 + TL : buf0;   // one buffer: tiles load after the previous one is stored
+  V* buf1 = STAGES >= 2 ? buf0 + TL : buf0;   // one buffer: tiles load after the previous one is stored
   uint64_t* mbar = reinterpret_cast<uint64_t*>(buf0 + (size_t)NBUF * TL);   // TMA: one transaction barrier per buffer
   volatile int* stamp = reinterpret_cast<volatile int*>(mbar + 4);   // teams: tile counter loaded per buffer
   double* red_all = reinterpret_cast<double*>(mbar + 8);
@@ -563,7 +564,7 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
     // each phase's per-thread base, so every shared-memory access keeps a fixed base register
     // (opaque to the compiler: it would otherwise split the OR back into a per-access add)
     uint32_t kofs = (uint32_t)(cur - buf0);
-    if (TEAMS > 1) asm volatile("mov.b32 %0, %0;\n" : "+r"(kofs));
+    if (NBUF > 1) asm volatile("mov.b32 %0, %0;\n" : "+r"(kofs));
     body(buf0, kofs, b, p.sel + (size_t)b * p.S, tile, base, scale, red, emask, hits_s);
     V* st = reinterpret_cast<V*>(p.states) + ((size_t)en.z << p.n) + base;
     if (TMA && TMA_ST) {
@@ -688,20 +689,19 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
     fill_rowtab();
     if (tid == 0) mbar_init(&mbar[0], NISSUE);
     __syncthreads();
-  } else if (TMA) {
+  } else if (TMA) {   // STAGES buffers: the next STAGES - 1 tiles are in flight while one computes
     fill_rowtab();
-    if (tid == 0) {
-      mbar_init(&mbar[0], NISSUE);
-      mbar_init(&mbar[1], NISSUE);
-    }
+    if (tid == 0)
+      for (int k = 0; k < STAGES; ++k) mbar_init(&mbar[k], NISSUE);
     __syncthreads();
-    if (t < total) tma_load(t, 0);
+    for (int k = 0; k < STAGES - 1; ++k)
+      if (t + (long long)k * gridDim.x < total) tma_load(t + (long long)k * gridDim.x, k);
   } else if (STAGES == 2) {
     if (t < total) load_tile(t, buf0);
     cp_async_commit();
   }
   for (int it = 0; t < total; t += gridDim.x, ++it) {
-    V* cur = (it & 1) ? buf1 : buf0;
+    V* cur = (TMA && STAGES > 2) ? buf0 + (size_t)(it % STAGES) * TL : (it & 1) ? buf1 : buf0;
     V* nxt = (it & 1) ? buf0 : buf1;
     if (STAGES == 1) {
       if (TMA) {
@@ -715,8 +715,11 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
         __syncthreads();
       }
     } else if (TMA) {
-      if (t + gridDim.x < total) tma_load(t + gridDim.x, (it + 1) & 1);
-      mbar_wait(&mbar[it & 1], (uint32_t)(it >> 1) & 1u);
+      // (the buffer of tile it + STAGES - 1 last held tile it - 1, stored in the previous
+      // iteration: tma_load's issuers wait for that store's reads first)
+      const long long ahead = t + (long long)(STAGES - 1) * gridDim.x;
+      if (ahead < total) tma_load(ahead, (it + STAGES - 1) % STAGES);
+      mbar_wait(&mbar[it % STAGES], (uint32_t)(it / STAGES) & 1u);
     } else {
       if (t + gridDim.x < total) load_tile(t + gridDim.x, nxt);
       cp_async_commit();

@@ -37,9 +37,12 @@ KIND_GATE = 0
 KIND_SITE = 1
 
 # 32-KB tiles for complex64; 64-KB single-buffered tiles for complex128 (config 4: 12 passes
-# instead of 17 at 11 bits -- 566 K vs 473 K shots/s on one B200)
+# instead of 17 at 11 bits -- 566 K vs 473 K shots/s on one B200).
+# complex128 tiles are made of 512-B rows (5 contiguous low qubits): fewer, longer DRAM
+# bursts per tile, and the layout search still finds 11 passes for config 4 (882 K vs
+# 831 K shots/s with 128-B rows; complex64 keeps 128-B rows: 1.81 M at 256-B vs 1.83 M).
 DEFAULT_TILE_BITS = {"c64": 12, "c128": 12}
-DEFAULT_LOW_BITS = {"c64": 4, "c128": 3}     # 16 x 8 B / 8 x 16 B = 128-B rows
+DEFAULT_LOW_BITS = {"c64": 4, "c128": 5}     # rows of 16 x 8 B = 128 B (c64) / 32 x 16 B = 512 B (c128)
 
 
 @dataclass

@@ -1,11 +1,9 @@
 #!/bin/bash
-# usage (GPU box): tools/gpu_abc.sh TAG "ENV0" "ENV1" "ENV2" [bench args] -- variants interleaved, twice each
+# usage (GPU box): tools/gpu_abc.sh TAG "ENV_B" "ENV_C" -- c128 bench: default (A) vs ENV_B vs ENV_C, interleaved twice
 mkdir -p gpurun_out
-tag=$1; v0=$2; v1=$3; v2=$4; shift 4
-python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
-for rep in 1 2; do
-  for i in 0 1 2; do
-    case $i in 0) e=$v0;; 1) e=$v1;; 2) e=$v2;; esac
-    env $e timeout 900 python bench.py --no-cpu "$@" > gpurun_out/abc_${tag}_v${i}_$rep.log 2>&1
-  done
+tag=$1; eb=$2; ec=$3
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_$tag.log 2>&1
+for run in A1 B1 C1 A2 B2 C2; do
+  case $run in A*) e=PTSBE_X=0;; B*) e=$eb;; C*) e=$ec;; esac
+  env $e timeout 600 python bench.py --no-cpu --dtype c128 --secondary none > gpurun_out/abc_${tag}_$run.log 2>&1
 done
