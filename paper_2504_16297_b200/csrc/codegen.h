@@ -389,6 +389,44 @@ inline std::string slot_inv_struct(const std::string& name, const TmaLayout& t) 
   return o.str();
 }
 
+// TMA row table of a pass as a __constant__ array (the warp-uniform issue path reads it with
+// uniform constant loads straight into uniform registers): gather group g, row q -> tile-relative
+// 128-B row coordinate of shared-memory slot 4g + q (gen_prelude.cuh fill_rowtab computes the
+// same table into shared memory for the per-lane path).
+inline std::string rowtab_struct(const std::string& name, bool tma, bool c64, int C, int L, uint64_t hmask,
+                                 const TmaLayout& t) {
+  std::ostringstream o;
+  if (!tma) {
+    o << "struct " << name << " { __device__ __forceinline__ uint4 operator()(int) const { return make_uint4(0u, 0u, 0u, 0u); } };\n";
+    return o.str();
+  }
+  const int LOGU = c64 ? 4 : 3;
+  const int NGRP = (1 << (L - LOGU)) / 4;
+  auto pdep = [&](uint64_t x) {
+    uint64_t r = 0;
+    for (int q = 0; q < 64; ++q)
+      if ((hmask >> q) & 1) { r |= (x & 1) << q; x >>= 1; }
+    return r;
+  };
+  o << "__constant__ uint4 k" << name << "[" << NGRP << "] = {";
+  for (int g = 0; g < NGRP; ++g) {
+    o << (g ? ", " : "") << "{";
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t sidx = (uint32_t)(4 * g + q);
+      uint32_t u = 0;
+      for (int j = 0; j < t.R; ++j)
+        if ((sidx >> j) & 1u) u ^= t.inv[j];
+      const uint64_t lo = u & ((1u << (C - LOGU)) - 1u);
+      const uint64_t v = ((lo << LOGU) | pdep(u >> (C - LOGU))) >> LOGU;
+      o << (q ? ", " : "") << (uint32_t)v << "u";
+    }
+    o << "}";
+  }
+  o << "};\nstruct " << name << " { __device__ __forceinline__ uint4 operator()(int g) const { return k" << name
+    << "[g]; } };\n";
+  return o.str();
+}
+
 // Device functor for a swizzle (compile-time masks).
 inline std::string swizzle_struct(const std::string& name, const Swizzle& z, int L) {
   std::ostringstream o;
@@ -917,12 +955,14 @@ inline std::string generate(const GenProgram& P) {
       k << "      ptg::gsync<" << threads << ">();\n";
       k << "    }\n";
     }
-    k << "  });\n}\n";
+    k << "  }, RowTab" << pi << "());\n}\n";
     const double mag = cxabs(F);
     G = cxmul(G, Cx{F.re / mag, F.im / mag});
-    kernels.push_back(swizzle_struct(swname, sw, gp.L) + slot_inv_struct(swname + "Inv", tl) + slow_fns.str() +
-                      k.str());
+    kernels.push_back(swizzle_struct(swname, sw, gp.L) + slot_inv_struct(swname + "Inv", tl) +
+                      rowtab_struct("RowTab" + std::to_string(pi), tma, P.c64, gp.c, gp.L, hmask, tl) +
+                      slow_fns.str() + k.str());
   }
+  if (std::getenv("PTSBE_TEAM_TAIL_SYNC")) o << "#define PTG_TEAM_TAIL_SYNC 1\n";
   o << kGenPrelude << "\n"
     << "#define GZERO_RE " << hexd(G.re) << "\n#define GZERO_IM " << hexd(G.im) << "\n";
   for (auto& kt : kernels) o << kSplit << kt;   // compile() builds one NVRTC program per pass

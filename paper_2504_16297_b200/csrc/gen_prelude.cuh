@@ -25,6 +25,9 @@ typedef long long int64_t;
 
 namespace ptg {
 
+#ifndef PTG_TEAM_TAIL_SYNC
+#define PTG_TEAM_TAIL_SYNC 0   // 1: team barrier after every tile's TMA store (PTSBE_TEAM_TAIL_SYNC)
+#endif
 #define PTG_MAX_HIT_WORDS 480   // = codegen.h kMaxHitWords (shared-memory room for the hit words)
 
 struct DevOp { int32_t kind, arity, b0, b1, ref, slot, k0, k1; };
@@ -263,6 +266,38 @@ __device__ __forceinline__ void tma_prefetch4(const TMapDesc* tm, int r0, int r1
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile::gather4 [%0, {%1, %2, %3, %4, %5}];\n"
                ::"l"(tm), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3) : "memory");
 }
+// Warp-uniform issue: the whole (converged) warp executes these with warp-uniform operands;
+// elect.sync keeps the copy to one issue, and because the operands are uniform ptxas emits
+// a single UTMALDG / UTMASTG from uniform registers (no per-lane ELECT / R2UR.BROADCAST /
+// BRA.U.ANY waterfall loop, which the per-lane form above compiles to).
+__device__ __forceinline__ void tma_gather4_w(void* dst, const TMapDesc* tm, int r0, int r1, int r2, int r3,
+                                              uint64_t* bar) {
+  asm volatile(
+      "{\n .reg .pred P;\n elect.sync _|P, 0xffffffff;\n"
+      "@P cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n}\n" ::"r"(smem_u32(dst)), "l"(tm), "r"(0), "r"(r0), "r"(r1),
+      "r"(r2), "r"(r3), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tma_scatter4_w(const TMapDesc* tm, int r0, int r1, int r2, int r3, const void* src) {
+  asm volatile(
+      "{\n .reg .pred P;\n elect.sync _|P, 0xffffffff;\n"
+      "@P cp.async.bulk.tensor.2d.global.shared::cta.tile::scatter4.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];\n}\n"
+      ::"l"(tm), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(src)) : "memory");
+}
+__device__ __forceinline__ void tma_prefetch4_w(const TMapDesc* tm, int r0, int r1, int r2, int r3) {
+  asm volatile("{\n .reg .pred P;\n elect.sync _|P, 0xffffffff;\n"
+               "@P cp.async.bulk.prefetch.tensor.2d.L2.global.tile::gather4 [%0, {%1, %2, %3, %4, %5}];\n}\n"
+               ::"l"(tm), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx_w(uint64_t* bar, uint32_t bytes) {
+  asm volatile("{\n .reg .pred P;\n elect.sync _|P, 0xffffffff;\n"
+               "@P mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_w(uint64_t* bar) {
+  asm volatile("{\n .reg .pred P;\n elect.sync _|P, 0xffffffff;\n"
+               "@P mbarrier.arrive.shared::cta.b64 _, [%0];\n}\n" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
@@ -405,9 +440,11 @@ __device__ __forceinline__ void zerog(V (&a)[N], uint64_t base, uint32_t gb, con
 // scale, red, emask, hits) runs
 // the pass's phases on one tile.
 template <typename R, int L, int C, int TLOG, int NT, bool SUMS, bool TMA, bool TMA_ST, int TMA_LANES, int STAGES,
-          bool TMA_PF, int TEAMS, class Sw, class SlotInv, class TileBase, class RowOff, class ErrMask, class Body>
+          bool TMA_PF, int TEAMS, class Sw, class SlotInv, class TileBase, class RowOff, class ErrMask, class Body,
+          class RowTabC>
 __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm, Sw swz_, SlotInv slot_inv,
-                                         TileBase tile_base, RowOff row_off, ErrMask err_mask, Body body) {
+                                         TileBase tile_base, RowOff row_off, ErrMask err_mask, Body body,
+                                         RowTabC rowtab_c) {
   typedef typename Cplx<R>::V V;
   typedef typename Cplx<R>::W W;
   constexpr int VPW = sizeof(W) / sizeof(V);
@@ -493,11 +530,16 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
   // per-CTA table of tile-relative row coordinates (the same for every tile of the pass)
   constexpr int NWARP = NT / 32;
   constexpr int PERW = TMA ? (NGRP + NWARP - 1) / NWARP : 1;   // gather4s per warp
-  constexpr int NISSUE = TMA ? (NGRP < NWARP * PERW ? NGRP : NWARP * PERW) : 1;
-  static_assert(PERW <= 32, "TMA: more gather groups per warp than lanes");
+  // TMA_LANES == 0: each warp issues its PERW gather4s as one warp-uniform sequence (one
+  // mbarrier arrival per issuing warp); otherwise one gather4 per issuing lane
+  constexpr bool WISSUE = TMA_LANES == 0;
+  constexpr int NIW = TMA ? (NGRP + PERW - 1) / PERW : 1;   // issuing warps
+  constexpr int NISSUE = !TMA ? 1 : WISSUE ? NIW : (NGRP < NWARP * PERW ? NGRP : NWARP * PERW);
+  static_assert(WISSUE || PERW <= 32, "TMA: more gather groups per warp than lanes");
   const uint32_t lane = tid & 31u;
-  const int gi = (int)(tid >> 5) * PERW + (int)lane;            // this thread's gather group
-  const bool issuer = TMA && lane < (uint32_t)PERW && gi < NGRP;
+  const int wid = __shfl_sync(0xffffffffu, (int)(tid >> 5), 0);   // warp-uniform
+  const int gi = wid * PERW + (int)lane;            // this thread's gather group (per-lane issue)
+  const bool issuer = TMA && (WISSUE ? wid * PERW < NGRP : (lane < (uint32_t)PERW && gi < NGRP));
   auto tma_load = [&](long long tt, int k) {
     V* dst = buf0 + (size_t)k * TL;   // buffer k (two stages: buf1 = buf0 + TL; teams: three buffers)
     const int e = (int)(tt >> TLOG);
@@ -509,6 +551,26 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
     }
     if (!issuer) return;
     if (TMA_ST) bulk_wait_read0();
+    if constexpr (WISSUE) {
+      if (!lsrc) {
+        mbar_arrive_w(&mbar[k]);
+        return;
+      }
+      const int g0 = wid * PERW;
+      const int cnt = NGRP - g0 < PERW ? NGRP - g0 : PERW;
+      mbar_arrive_tx_w(&mbar[k], 512u * (uint32_t)cnt);   // cnt x 4 rows x 128 B
+      const unsigned long long row0 = __shfl_sync(0xffffffffu, (unsigned long long)(
+          ((uint64_t)(lsrc - reinterpret_cast<const V*>(p.states)) +
+           tile_base((uint64_t)(tt & ((1ll << TLOG) - 1)))) >> LOGU), 0);
+#pragma unroll
+      for (int j = 0; j < PERW; ++j) {
+        if (NIW * PERW != NGRP && j >= cnt) break;
+        const uint4 r = rowtab_c(g0 + j);
+        tma_gather4_w(dst + ((size_t)(g0 + j) << (LOGU + 2)), tm, (int)(row0 + r.x), (int)(row0 + r.y),
+                      (int)(row0 + r.z), (int)(row0 + r.w), &mbar[k]);
+      }
+      return;
+    }
     if (!lsrc) {
       mbar_arrive(&mbar[k]);
       return;
@@ -527,11 +589,35 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
     const int4 en = p.ent[(int)(tt >> TLOG)];
     if (p.gen_zero || p.status[en.x] != 0) return;
     const uint64_t row0 = (((uint64_t)en.y << p.n) + tile_base((uint64_t)(tt & ((1ll << TLOG) - 1)))) >> LOGU;
+    if constexpr (WISSUE) {
+      const unsigned long long r0u = __shfl_sync(0xffffffffu, (unsigned long long)row0, 0);
+#pragma unroll
+      for (int j = 0; j < PERW; ++j) {
+        if (NIW * PERW != NGRP && wid * PERW + j >= NGRP) break;
+        const uint4 r = rowtab_c(wid * PERW + j);
+        tma_prefetch4_w(tm, (int)(r0u + r.x), (int)(r0u + r.y), (int)(r0u + r.z), (int)(r0u + r.w));
+      }
+      return;
+    }
     const uint4 r = rowtab[gi];
     tma_prefetch4(tm, (int)(row0 + r.x), (int)(row0 + r.y), (int)(row0 + r.z), (int)(row0 + r.w));
   };
   auto tma_store = [&](const V* src, long long slot_base_amp, uint64_t base) {
     if (!issuer) return;
+    if constexpr (WISSUE) {
+      const int g0 = wid * PERW;
+      const unsigned long long row0 =
+          __shfl_sync(0xffffffffu, (unsigned long long)(((uint64_t)slot_base_amp + base) >> LOGU), 0);
+#pragma unroll
+      for (int j = 0; j < PERW; ++j) {
+        if (NIW * PERW != NGRP && g0 + j >= NGRP) break;
+        const uint4 r = rowtab_c(g0 + j);
+        tma_scatter4_w(tm, (int)(row0 + r.x), (int)(row0 + r.y), (int)(row0 + r.z), (int)(row0 + r.w),
+                       src + ((size_t)(g0 + j) << (LOGU + 2)));
+      }
+      bulk_commit();
+      return;
+    }
     const uint64_t row0 = ((uint64_t)slot_base_amp + base) >> LOGU;
     const uint4 r = rowtab[gi];
     tma_scatter4(tm, (int)(row0 + r.x), (int)(row0 + r.y), (int)(row0 + r.z), (int)(row0 + r.w),
@@ -624,7 +710,11 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
         st_stream(reinterpret_cast<W*>(st + roff(r) + (uint64_t)j * VPW), w);
       }
     }
-    gsync<NT>();
+    // Compute teams, TMA stores, no fused sums: no team barrier after the store.  Every thread
+    // passed the pre-store barrier (done with the tile's phases, hit words and reductions); the
+    // buffer is next written only by the gathers of tile i + 3, which each issuing warp issues
+    // into the slot groups its own scatters read, after waiting for those reads.
+    if (!(TEAMS > 1 && TMA && TMA_ST && !PTG_TEAM_TAIL_SYNC && !(SUMS && FAST && p.tsum))) gsync<NT>();
   };
   auto fill_rowtab = [&]() {   // tile row in shared-memory slot 4g+q: slot^-1, then its row offset
     for (int g = (int)threadIdx.x; g < NGRP; g += NT * TEAMS) {
