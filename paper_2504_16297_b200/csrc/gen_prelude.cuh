@@ -562,7 +562,7 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
       const unsigned long long row0 = __shfl_sync(0xffffffffu, (unsigned long long)(
           ((uint64_t)(lsrc - reinterpret_cast<const V*>(p.states)) +
            tile_base((uint64_t)(tt & ((1ll << TLOG) - 1)))) >> LOGU), 0);
-#pragma unroll
+#pragma unroll 1
       for (int j = 0; j < PERW; ++j) {
         if (NIW * PERW != NGRP && j >= cnt) break;
         const uint4 r = rowtab_c(g0 + j);
@@ -608,7 +608,7 @@ __device__ __forceinline__ void run_pass(const PassParams& p, const TMapDesc* tm
       const int g0 = wid * PERW;
       const unsigned long long row0 =
           __shfl_sync(0xffffffffu, (unsigned long long)(((uint64_t)slot_base_amp + base) >> LOGU), 0);
-#pragma unroll
+#pragma unroll 1
       for (int j = 0; j < PERW; ++j) {
         if (NIW * PERW != NGRP && g0 + j >= NGRP) break;
         const uint4 r = rowtab_c(g0 + j);
