@@ -441,3 +441,31 @@ def test_tree_schedule_renormalising_groups(monkeypatch):
         if out["1"][1][b] == 0:
             ref, rw = O.prepare(c, specs[b].selections)
             assert rel(x, ref) <= 1e-12 and out["1"][0][b] == pytest.approx(rw, rel=1e-12)
+
+
+def test_tma_issue_forms_and_team_tail_barrier_are_bit_identical(monkeypatch):
+    """Steane blocks at 21 q (c128: generated TMA passes, compute teams on the heavy ones): the
+    per-lane TMA issue (default), the warp-uniform issue from the __constant__ row table
+    (PTSBE_TMA_LANES=0) and the team barrier after every store (PTSBE_TEAM_TAIL_SYNC=1) must
+    give exactly the same states and weights."""
+    ctext, ntext = workloads.steane_blocks(3)
+    c = P.attach_noise(P.parse_circuit(ctext), P.parse_noise_model(ntext))
+    specs = P.presample_probabilistic(c, 200, 10, np.random.default_rng(21))[:4]
+    prog = compile_circuit(c, "c128")
+    out = {}
+    for name, env in (("default", {}), ("warp", {"PTSBE_TMA_LANES": "0"}), ("tail", {"PTSBE_TEAM_TAIL_SYNC": "1"})):
+        for k in ("PTSBE_TMA_LANES", "PTSBE_TEAM_TAIL_SYNC"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        with Engine(c.n_qubits, "c128", batch_cap=len(specs)) as eng:
+            eng.load_program(prog)
+            assert eng.info()["codegen"] == 1
+            w, st = eng.run(selection_matrix(prog, specs))
+            out[name] = (w, st, [eng.get_state(b) for b in range(len(specs))])
+    ref = out["default"]
+    assert all(abs(np.linalg.norm(s) - 1) <= 1e-12 for s in ref[2])
+    for name in ("warp", "tail"):
+        assert np.array_equal(out[name][0], ref[0]) and np.array_equal(out[name][1], ref[1])
+        for a, b in zip(out[name][2], ref[2]):
+            assert np.array_equal(a, b)
